@@ -1,0 +1,296 @@
+/* scls_capi.h — C-ABI boundary of the B200-native SCLS scheduling core.
+ *
+ * Plain C types only (no torch, no C++), so any FFI (ctypes, cgo, JNI) or the
+ * C++ drop-in layer (include/slicesim_b200/*.hpp) can bind it.  Every entry point
+ * replaces one public function of the reference library `slicesim`
+ * (/root/reference/proj/core/include/slicesim/*.h); the replaced interface is
+ * cited on each declaration as reference file:line.
+ *
+ * Conventions
+ *   - A context (scls_ctx) binds one CUDA device and one stream.  Calls are
+ *     stream-ordered and synchronous with respect to the host: when a call
+ *     returns, its outputs are valid.  One context per host thread.
+ *   - `mem` selects where the caller's array arguments live: SCLS_MEM_HOST
+ *     (pageable or pinned host memory; the library copies in/out inside the
+ *     call) or SCLS_MEM_DEVICE (device pointers on the context's device).
+ *   - Errors map 1:1 onto the reference exception classes (errors.h:26-87).
+ *     scls_last_error() returns the message, scls_last_request_id() the
+ *     offending request of an InfeasibleRequestError (errors.h:51-56).
+ *   - There is no CPU fallback: without a usable CUDA device every compute
+ *     entry point fails with SCLS_ERR_CUDA.
+ */
+#ifndef SCLS_CAPI_H_
+#define SCLS_CAPI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCLS_ABI_VERSION 1
+#define SCLS_MAX_RULES 32
+
+/* errors.h:26-87 — one code per exception class. */
+typedef enum scls_status {
+  SCLS_OK = 0,
+  SCLS_ERR_ERROR = 1,                /* slicesim::Error (validation)          */
+  SCLS_ERR_INSUFFICIENT_SAMPLES = 2, /* InsufficientSamplesError              */
+  SCLS_ERR_DEGENERATE_MODEL = 3,     /* DegenerateModelError                  */
+  SCLS_ERR_WRONG_KIND = 4,           /* WrongKindError                        */
+  SCLS_ERR_INFEASIBLE_REQUEST = 5,   /* InfeasibleRequestError{request_id}    */
+  SCLS_ERR_NO_WORKERS = 6,           /* NoWorkersError                        */
+  SCLS_ERR_PARSE = 7,                /* ParseError                            */
+  SCLS_ERR_LIMIT_VIOLATION = 8,      /* LimitViolationError                   */
+  SCLS_ERR_EMPTY_LOG = 9,            /* EmptyLogError                         */
+  SCLS_ERR_NON_TERMINATION = 10,     /* NonTerminationError                   */
+  SCLS_ERR_INVALID_ARGUMENT = 11,    /* C-ABI misuse (null pointer, bad size) */
+  SCLS_ERR_CUDA = 12,                /* no device / launch failure            */
+  SCLS_ERR_CAPACITY = 13             /* caller buffer (event log) too small   */
+} scls_status;
+
+enum { SCLS_MEM_HOST = 0, SCLS_MEM_DEVICE = 1 };
+
+/* cost_model.h:29-39 LatencyModel. */
+typedef struct scls_latency {
+  double p1, p2, p3, p4; /* prefill: p1*n*l + p2*n + p3*l + p4 */
+  double d1, d2, d3, d4; /* decode step: d1*n*l + d2*n + d3*l + d4 */
+  double rmse_prefill, rmse_decode;
+  int32_t n_cap, l_cap;
+} scls_latency;
+
+enum { SCLS_MEM_ANALYTIC = 0, SCLS_MEM_RULE_TABLE = 1 };
+
+/* memory_model.h:20-53 MemoryModel (rule rows inline, <= SCLS_MAX_RULES). */
+typedef struct scls_memory {
+  int32_t kind;    /* SCLS_MEM_ANALYTIC | SCLS_MEM_RULE_TABLE */
+  int32_t n_rules;
+  double m_cap, m_model, m_engine, delta, zeta;
+  int32_t rule_threshold[SCLS_MAX_RULES]; /* strictly decreasing */
+  int32_t rule_max_n[SCLS_MAX_RULES];
+} scls_memory;
+
+enum { SCLS_POLICY_SCLS = 0, SCLS_POLICY_SLS = 1, SCLS_POLICY_ILS = 2 };
+
+/* sched_policies.h:39-48 SchedulerConfig (+ the Simulator horizon,
+ * sim_engine.h:61-62). */
+typedef struct scls_sched_cfg {
+  int32_t policy;
+  int32_t slice_len;
+  int32_t max_gen_limit;
+  int32_t fixed_batch_size;
+  int32_t max_concurrent;
+  int32_t worker_count;
+  double lambda;
+  double gamma;
+  double horizon_s;
+} scls_sched_cfg;
+
+enum { SCLS_DIST_UNIFORM = 0, SCLS_DIST_LOGNORMAL = 1, SCLS_DIST_HISTOGRAM = 2 };
+#define SCLS_MAX_BUCKETS 30
+
+/* workload.h:32-50 LengthDist (histogram buckets inline). */
+typedef struct scls_length_dist {
+  int32_t kind;
+  int32_t lo, hi;  /* uniform */
+  double mu, sigma; /* log-normal */
+  int32_t cap;
+  int32_t n_buckets; /* histogram: n_buckets weights, n_buckets+1 edges */
+  int32_t edges[SCLS_MAX_BUCKETS + 1];
+  double weights[SCLS_MAX_BUCKETS];
+} scls_length_dist;
+
+/* workload.h:54-62 WorkloadSpec. */
+typedef struct scls_workload_spec {
+  double rate;
+  double duration_s;
+  scls_length_dist input_len_dist;
+  scls_length_dist gen_len_dist;
+  int32_t max_input_limit;
+  int32_t max_gen_limit;
+  uint64_t seed;
+} scls_workload_spec;
+
+typedef struct scls_ctx scls_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+int32_t scls_abi_version(void);
+/* stream: a cudaStream_t (NULL = a private non-blocking stream). */
+scls_status scls_ctx_create(int32_t device, void* stream, scls_ctx** out);
+void scls_ctx_destroy(scls_ctx* ctx);
+/* Message of the last failed call on this context (thread-local when ctx is
+ * NULL); returns the full message length. */
+size_t scls_last_error(const scls_ctx* ctx, char* buf, size_t cap);
+int64_t scls_last_request_id(const scls_ctx* ctx);
+/* Device time (ms, CUDA events on the context stream) of the phases of the
+ * last call: [0]=total, [1]=sort, [2]=estimate/window tables, [3]=DP chain,
+ * [4]=backtrack+emit, [5]=offload, [6]=simulate. */
+void scls_last_timings(const scls_ctx* ctx, float out_ms[8]);
+/* Number of CUDA kernel launches issued by the last call. */
+int64_t scls_last_launch_count(const scls_ctx* ctx);
+
+/* ---- validation (host only; mirrors the reference validators) ----------- */
+scls_status scls_validate_latency(const scls_latency* m);   /* cost_model.cpp:70-87    */
+scls_status scls_validate_memory(const scls_memory* m);     /* memory_model.cpp:92-120 */
+scls_status scls_validate_sched(const scls_sched_cfg* cfg); /* sched_policies.cpp:45-57 */
+
+/* ---- estimators: batched device evaluation ------------------------------
+ * Replaces cost_model.h:54-66 batch_serve_time and memory_model.h:62-66
+ * would_oom / max_batch_size, evaluated for `count` candidates at once with
+ * the reference's exact fp64 operation order. */
+scls_status scls_batch_serve_time(scls_ctx* ctx, int64_t count, const int32_t* n,
+                                  const int32_t* l_in, const int32_t* l_out,
+                                  const scls_latency* lat, double* out, int32_t mem);
+scls_status scls_would_oom(scls_ctx* ctx, int64_t count, const int32_t* n,
+                           const int32_t* l_in, int32_t slice_len,
+                           const scls_memory* memm, uint8_t* out, int32_t mem);
+scls_status scls_max_batch_size(scls_ctx* ctx, int64_t count, const int32_t* l_in,
+                                int32_t slice_len, const scls_memory* memm,
+                                int32_t* out, int32_t mem);
+
+/* ---- batcher: batcher.h:40-43 batch_requests ------------------------------
+ * Inputs (length n): effective input length, arrival time, id.
+ * Outputs (caller-allocated; capacities n, n+1, n, n, n, n):
+ *   order[p]      input index of the p-th request in (eff, arrival, id) order
+ *   seg_begin[b]  first sorted position of batch b; seg_begin[n_batches] = n
+ *   l_in[b], est[b]  batch input length and est_serve_time
+ *   member_id[p]  id of the p-th member in batch order (= id[order[p]]); may be NULL
+ * Batch b has id first_batch_id + b and planned_l_out = slice_len. */
+typedef struct scls_batches {
+  int64_t n_batches;
+  int32_t* order;
+  int32_t* seg_begin;
+  int32_t* l_in;
+  double* est;
+  int64_t* member_id;
+} scls_batches;
+
+scls_status scls_batch_requests(scls_ctx* ctx, int64_t n, const int32_t* eff_len,
+                                const double* arrival, const int64_t* id,
+                                int32_t slice_len, const scls_latency* lat,
+                                const scls_memory* memm, int64_t first_batch_id,
+                                scls_batches* out, int32_t mem);
+
+/* ---- offloader: offloader.h:39-44 offload ----------------------------------
+ * Batches in creation order (ids, estimates); workers (ids, loads, mutated in
+ * place).  Outputs the (batch_id, worker_id) assignment sequence. */
+scls_status scls_offload(scls_ctx* ctx, int64_t n_batches, const int64_t* batch_id,
+                         const double* est, int32_t n_workers, const int32_t* worker_id,
+                         double* load_inout, int64_t* out_batch_id, int32_t* out_worker,
+                         int32_t mem);
+
+/* Fused batch_requests + offload (the SCLS tick, sched_policies.cpp:93-112).
+ * out_batch_id/out_worker have capacity n. */
+scls_status scls_schedule(scls_ctx* ctx, int64_t n, const int32_t* eff_len,
+                          const double* arrival, const int64_t* id, int32_t slice_len,
+                          const scls_latency* lat, const scls_memory* memm,
+                          int64_t first_batch_id, int32_t n_workers,
+                          const int32_t* worker_id, double* load_inout,
+                          scls_batches* out, int64_t* out_batch_id, int32_t* out_worker,
+                          int32_t mem);
+
+/* ---- simulator: sim_engine.h:61-67 Simulator::run + metrics.h:41 compute ---
+ * Runs `n_traces` independent simulations.  Trace t owns requests
+ * [req_offset[t], req_offset[t+1]) of the concatenated arrays, given in
+ * arrival order with ids 0..n_t-1 (sim_engine.cpp:102-114), and config
+ * cfg[cfg_index[t]] (cfg_index may be NULL: cfg[0] for all).
+ *
+ * Per-trace results: the MetricsReport fields (metrics.h:26-36), the status
+ * (NonTermination / Infeasible / EmptyLog map to codes, never traps), and
+ * FNV-1a-64 hashes of the completion order, the dispatch sequence and the
+ * completion times, plus a word-wise hash of the whole
+ * event log.  slice_hist[t*hist_bins + s] counts requests completed after s
+ * slices (fraction = count / completed, metrics.cpp:109-111). */
+typedef struct scls_trace_result {
+  int32_t status;
+  int32_t worker_count;
+  int64_t error_request_id;
+  int64_t n_requests;
+  int64_t completed;
+  double throughput;
+  double avg_response_s;
+  double p95_response_s;
+  double ct_std_s;
+  double avg_pad_tokens;
+  double avg_invalid_tokens;
+  double avg_batch_size;
+  double early_return_ratio;
+  int64_t total_pad;
+  int64_t total_invalid;
+  int64_t batch_count;
+  int64_t batch_members;
+  int64_t early_returns;
+  int64_t n_events;     /* EventRecords the reference log would hold */
+  int64_t n_dispatches;
+  int64_t n_ticks;
+  uint64_t h_complete_ids;
+  uint64_t h_dispatch;
+  uint64_t h_complete_t;
+  uint64_t h_log;
+  double sim_clock;     /* clock at the last processed event */
+} scls_trace_result;
+
+/* Optional full event log (EventRecord, event_log.h:52-69; members
+ * event_log.h:41-47) for traces whose index is < n_logged.  Trace t writes
+ * records [rec_offset[t], rec_offset[t]+rec_count[t]) and members likewise;
+ * capacity per trace = rec_cap / mem_cap.  Device pointers when mem =
+ * SCLS_MEM_DEVICE. */
+typedef struct scls_event_record {
+  double t;
+  double est_serve_s;
+  double response_s;
+  double next_interval_s;
+  int64_t request;
+  int64_t batch;
+  int32_t kind; /* event_log.h:27-34 order: arrival, tick, dispatch, batch_start, batch_end, complete */
+  int32_t worker;
+  int32_t n;
+  int32_t l_in;
+  int32_t planned_l_out;
+  int32_t served_l_out;
+  int32_t input_len;
+  int32_t gen_len;
+  int32_t slices;
+  int32_t member_count;
+  int64_t member_offset; /* into the member array, relative to the trace */
+} scls_event_record;
+
+typedef struct scls_member {
+  int64_t request;
+  int32_t effective_input;
+  int32_t pad;
+  int32_t gen;
+  int32_t invalid;
+} scls_member;
+
+typedef struct scls_event_log {
+  int32_t n_logged;
+  int64_t rec_cap;     /* records per trace */
+  int64_t mem_cap;     /* members per trace */
+  scls_event_record* records; /* n_logged * rec_cap */
+  scls_member* members;       /* n_logged * mem_cap */
+  int64_t* rec_count;         /* n_logged */
+  int64_t* mem_count;         /* n_logged */
+} scls_event_log;
+
+scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int64_t* req_offset,
+                          const double* arrival, const int32_t* input_len,
+                          const int32_t* gen_len, int32_t n_cfgs,
+                          const scls_sched_cfg* cfgs, const int32_t* cfg_index,
+                          const scls_latency* lat, const scls_memory* memm,
+                          scls_trace_result* results, int32_t hist_bins,
+                          int64_t* slice_hist, scls_event_log* log, int32_t mem);
+
+/* ---- workload: workload.h:78 generate ------------------------------------
+ * Host-side Poisson trace generation (mt19937_64 + glibc log, the reference's
+ * exact sampler; workload.cpp:100-181).  Writes up to `cap` requests and sets
+ * *n to the full count; SCLS_ERR_CAPACITY when cap < *n. */
+scls_status scls_generate(const scls_workload_spec* spec, int64_t cap, int64_t* n,
+                          double* arrival, int32_t* input_len, int32_t* gen_len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCLS_CAPI_H_ */
