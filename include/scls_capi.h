@@ -289,6 +289,12 @@ scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int64_t* req_of
 scls_status scls_generate(const scls_workload_spec* spec, int64_t cap, int64_t* n,
                           double* arrival, int32_t* input_len, int32_t* gen_len);
 
+/* The reference microbenchmark's synthetic pool (bench_batcher.cpp:27-42):
+ * mt19937_64(seed); request i: id i, arrival U*100, input 1+floor(U*1024),
+ * generation 1+floor(U*1024).  Host-side input preparation. */
+scls_status scls_make_pool(int64_t n, uint64_t seed, int32_t* input_len, double* arrival,
+                           int64_t* id, int32_t* gen_len);
+
 #ifdef __cplusplus
 }
 #endif

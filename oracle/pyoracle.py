@@ -228,6 +228,18 @@ class RefLib(_Checker):
 class OracleLib(_Checker):
     prefix = "orc_"
 
+    def make_pool(self, n, seed=7):
+        """bench_batcher.cpp:27-42 -> (eff, arrival, ids, gen_len)."""
+        fn = self.lib.orc_make_pool
+        fn.restype = C.c_int32
+        eff = np.zeros(max(n, 1), np.int32)
+        arr = np.zeros(max(n, 1), np.float64)
+        ids = np.zeros(max(n, 1), np.int64)
+        gen = np.zeros(max(n, 1), np.int32)
+        fn(C.c_int64(n), C.c_uint64(seed), _p(eff, C.c_int32), _p(arr, C.c_double),
+           _p(ids, C.c_int64), _p(gen, C.c_int32))
+        return eff[:n], arr[:n], ids[:n], gen[:n]
+
 
 _cache = {}
 

@@ -451,6 +451,21 @@ scls_status orc_generate(const scls_workload_spec* s, int64_t cap, int64_t* n, d
   return k > cap ? SCLS_ERR_CAPACITY : SCLS_OK;
 }
 
+/* bench_batcher.cpp:27-42 make_pool (the reference microbenchmark's pool) */
+scls_status orc_make_pool(int64_t n, uint64_t seed, int32_t* input_len, double* arrival,
+                          int64_t* id, int32_t* gen_len) {
+  mt64 g;
+  mt_seed(&g, seed);
+  for (int64_t i = 0; i < n; ++i) {
+    id[i] = i;
+    arrival[i] = next_uniform(&g) * 100.0;
+    input_len[i] = 1 + (int)(next_uniform(&g) * 1024.0);
+    const int gl = 1 + (int)(next_uniform(&g) * 1024.0);
+    if (gen_len) gen_len[i] = gl;
+  }
+  return SCLS_OK;
+}
+
 /* ---- simulator (sim_engine.cpp, sched_policies.cpp) ---------------------- */
 
 #define GROW(ptr, len, cap)                                                   \

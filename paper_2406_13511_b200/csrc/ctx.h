@@ -1,0 +1,72 @@
+// ctx.h — the per-(thread, device, stream) context behind scls_ctx: error
+// state, a grow-only device scratch arena, pinned staging memory and the
+// CUDA events that time each phase of a call.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "scls_capi.h"
+
+struct scls_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int64_t err_request = -1;
+  int64_t launches = 0;
+  float timings[8] = {0};
+  cudaEvent_t ev[16] = {};
+  int sm_count = 148;
+
+  // Named grow-only device buffers (scratch reused across calls).
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  std::vector<Buf> bufs;
+  // Pinned host staging for small readbacks.
+  void* pinned = nullptr;
+  size_t pinned_cap = 0;
+
+  void* buf(int slot, size_t bytes);
+  void* host_pinned(size_t bytes);
+};
+
+namespace scls {
+
+// Scratch slots (ctx->buf).  0..29 belong to the entry points, the rest to
+// shared primitives, so nested calls never alias each other's buffers.
+enum ScratchSlot : int {
+  kSlotRadixCounts = 30,
+  kSlotRadixOffs = 31,
+  kSlotScan = 40,     // 40..55: two per recursion level
+  kSlotStage = 60,    // 60..79: host<->device staging of entry-point arguments
+  kSlotSim = 80,      // 80..99: simulator
+  kNumSlots = 100,
+};
+
+// Status plumbing shared by the C-ABI entry points.
+scls_status set_error(scls_ctx* ctx, scls_status st, const std::string& msg);
+scls_status cuda_error(scls_ctx* ctx, cudaError_t e, const char* where);
+
+#define SCLS_CUDA(call)                                             \
+  do {                                                              \
+    cudaError_t _e = (call);                                        \
+    if (_e != cudaSuccess) return ::scls::cuda_error(ctx, _e, #call); \
+  } while (0)
+
+#define SCLS_LAUNCHED()                                                         \
+  do {                                                                          \
+    ++ctx->launches;                                                            \
+    cudaError_t _e = cudaPeekAtLastError();                                     \
+    if (_e != cudaSuccess) return ::scls::cuda_error(ctx, _e, "kernel launch"); \
+  } while (0)
+
+inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace scls

@@ -1,0 +1,336 @@
+"""ctypes binding of libscls_b200.so (the C-ABI in include/scls_capi.h).
+
+This is the Python face of the CUDA scheduling core.  There is no CPU
+fallback: if the shared library is missing the import of `load()` raises, and
+if no CUDA device is usable `Context()` raises SclsError(CudaError).
+
+Method names and argument meanings mirror the reference API
+(/root/reference/proj/core/include/slicesim/*.h):
+  batch_requests   batcher.h:40-43       offload        offloader.h:39-40
+  schedule         sched_policies.cpp:93-112 (batch_requests + offload)
+  simulate         sim_engine.h:61-67 + metrics.h:41 for many traces
+  generate         workload.h:78         batch_serve_time/would_oom/max_batch_size
+                                          cost_model.h:54-66, memory_model.h:62-66
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import capi
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libscls_b200.so")
+
+# Every symbol include/scls_capi.h declares (checked by tests/test_capi_symbols.py).
+EXPORTS = [
+    "scls_abi_version", "scls_ctx_create", "scls_ctx_destroy", "scls_last_error",
+    "scls_last_request_id", "scls_last_timings", "scls_last_launch_count",
+    "scls_validate_latency", "scls_validate_memory", "scls_validate_sched",
+    "scls_batch_serve_time", "scls_would_oom", "scls_max_batch_size",
+    "scls_batch_requests", "scls_offload", "scls_schedule", "scls_simulate",
+    "scls_generate", "scls_make_pool",
+]
+
+
+class SclsError(RuntimeError):
+    """Carries the scls_status code; `name` is the reference exception class."""
+
+    def __init__(self, status, msg, request_id=-1):
+        self.status = status
+        self.name = capi.STATUS_NAMES.get(status, str(status))
+        self.request_id = request_id
+        super().__init__(f"{self.name}: {msg}")
+
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built (run __graft_entry__.build()); "
+                          "the scheduling core has no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    i32, i64, f64, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
+    L, M, S = P(capi.Latency), P(capi.Memory), P(capi.SchedCfg)
+    sigs = {
+        "scls_abi_version": (i32, []),
+        "scls_ctx_create": (i32, [i32, vp, P(vp)]),
+        "scls_ctx_destroy": (None, [vp]),
+        "scls_last_error": (C.c_size_t, [vp, C.c_char_p, C.c_size_t]),
+        "scls_last_request_id": (i64, [vp]),
+        "scls_last_timings": (None, [vp, P(C.c_float)]),
+        "scls_last_launch_count": (i64, [vp]),
+        "scls_validate_latency": (i32, [L]),
+        "scls_validate_memory": (i32, [M]),
+        "scls_validate_sched": (i32, [S]),
+        "scls_batch_serve_time": (i32, [vp, i64, vp, vp, vp, L, vp, i32]),
+        "scls_would_oom": (i32, [vp, i64, vp, vp, i32, M, vp, i32]),
+        "scls_max_batch_size": (i32, [vp, i64, vp, i32, M, vp, i32]),
+        "scls_batch_requests": (i32, [vp, i64, vp, vp, vp, i32, L, M, i64, P(capi.Batches), i32]),
+        "scls_offload": (i32, [vp, i64, vp, vp, i32, vp, vp, vp, vp, i32]),
+        "scls_schedule": (i32, [vp, i64, vp, vp, vp, i32, L, M, i64, i32, vp, vp,
+                                P(capi.Batches), vp, vp, i32]),
+        "scls_simulate": (i32, [vp, i32, vp, vp, vp, vp, i32, S, vp, L, M,
+                                P(capi.TraceResult), i32, vp, P(capi.EventLog), i32]),
+        "scls_generate": (i32, [P(capi.WorkloadSpec), i64, P(i64), vp, vp, vp]),
+        "scls_make_pool": (i32, [i64, C.c_uint64, vp, vp, vp, vp]),
+    }
+    for name, (res, args) in sigs.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.scls_abi_version() != capi.SCLS_ABI_VERSION:
+        raise ImportError("libscls_b200.so ABI version mismatch")
+    _lib = lib
+    return lib
+
+
+def _ptr(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _dev_ptr(t):
+    """torch CUDA tensor -> device pointer (mem=SCLS_MEM_DEVICE calls)."""
+    return C.c_void_p(t.data_ptr())
+
+
+class Context:
+    """One scls_ctx: a CUDA device + stream (NULL: a private stream)."""
+
+    def __init__(self, device=0, stream=None):
+        self.lib = load()
+        h = C.c_void_p()
+        st = self.lib.scls_ctx_create(device, stream, C.byref(h))
+        if st:
+            raise self._error(st, None)
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.scls_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- diagnostics ------------------------------------------------------------
+    def _error(self, st, h):
+        lib = self.lib if hasattr(self, "lib") else load()
+        buf = C.create_string_buffer(4096)
+        lib.scls_last_error(h, buf, 4096)
+        return SclsError(st, buf.value.decode(errors="replace"), lib.scls_last_request_id(h))
+
+    def _check(self, st):
+        if st:
+            raise self._error(st, self.h)
+
+    def timings(self):
+        """Device ms of the last call: total, sort, estimate, dp, backtrack+emit,
+        offload, simulate."""
+        out = (C.c_float * 8)()
+        self.lib.scls_last_timings(self.h, out)
+        return dict(zip(["total", "sort", "estimate", "dp", "backtrack", "offload", "simulate", "x"],
+                        list(out)))
+
+    def launches(self):
+        return self.lib.scls_last_launch_count(self.h)
+
+    # -- estimators (batched) -----------------------------------------------------
+    def batch_serve_time(self, n, l_in, l_out, lat):
+        n = np.ascontiguousarray(n, np.int32)
+        l_in = np.ascontiguousarray(l_in, np.int32)
+        l_out = np.ascontiguousarray(l_out, np.int32)
+        out = np.zeros(len(n), np.float64)
+        self._check(self.lib.scls_batch_serve_time(self.h, len(n), _ptr(n), _ptr(l_in), _ptr(l_out),
+                                                   C.byref(lat), _ptr(out), capi.MEM_HOST))
+        return out
+
+    def would_oom(self, n, l_in, slice_len, mem):
+        n = np.ascontiguousarray(n, np.int32)
+        l_in = np.ascontiguousarray(l_in, np.int32)
+        out = np.zeros(len(n), np.uint8)
+        self._check(self.lib.scls_would_oom(self.h, len(n), _ptr(n), _ptr(l_in), slice_len,
+                                            C.byref(mem), _ptr(out), capi.MEM_HOST))
+        return out.astype(bool)
+
+    def max_batch_size(self, l_in, slice_len, mem):
+        l_in = np.ascontiguousarray(l_in, np.int32)
+        out = np.zeros(len(l_in), np.int32)
+        self._check(self.lib.scls_max_batch_size(self.h, len(l_in), _ptr(l_in), slice_len,
+                                                 C.byref(mem), _ptr(out), capi.MEM_HOST))
+        return out
+
+    # -- batcher / offloader ----------------------------------------------------------
+    def batch_requests(self, eff, arrival, ids, slice_len, lat, mem, first_batch_id=0):
+        """batcher.h:40-43 -> dict(order, seg_begin, l_in, est, batch_id, member_id)."""
+        eff = np.ascontiguousarray(eff, np.int32)
+        arrival = np.ascontiguousarray(arrival, np.float64)
+        ids = np.ascontiguousarray(ids, np.int64)
+        n = len(eff)
+        order = np.zeros(max(n, 1), np.int32)
+        seg = np.zeros(n + 1, np.int32)
+        l_in = np.zeros(max(n, 1), np.int32)
+        est = np.zeros(max(n, 1), np.float64)
+        mid = np.zeros(max(n, 1), np.int64)
+        out = capi.Batches(0, order.ctypes.data_as(C.POINTER(C.c_int32)),
+                           seg.ctypes.data_as(C.POINTER(C.c_int32)),
+                           l_in.ctypes.data_as(C.POINTER(C.c_int32)),
+                           est.ctypes.data_as(C.POINTER(C.c_double)),
+                           mid.ctypes.data_as(C.POINTER(C.c_int64)))
+        self._check(self.lib.scls_batch_requests(self.h, n, _ptr(eff), _ptr(arrival), _ptr(ids),
+                                                 slice_len, C.byref(lat), C.byref(mem),
+                                                 first_batch_id, C.byref(out), capi.MEM_HOST))
+        k = out.n_batches
+        return dict(n_batches=k, order=order[:n], seg_begin=seg[:k + 1], l_in=l_in[:k],
+                    est=est[:k], batch_id=np.arange(first_batch_id, first_batch_id + k, dtype=np.int64),
+                    member_id=mid[:n])
+
+    def offload(self, batch_id, est, worker_id, loads):
+        """offloader.h:39-40 -> (assigned batch ids, workers, new loads)."""
+        batch_id = np.ascontiguousarray(batch_id, np.int64)
+        est = np.ascontiguousarray(est, np.float64)
+        worker_id = np.ascontiguousarray(worker_id, np.int32)
+        loads = np.array(loads, np.float64)
+        nb = len(est)
+        ob = np.zeros(max(nb, 1), np.int64)
+        ow = np.zeros(max(nb, 1), np.int32)
+        self._check(self.lib.scls_offload(self.h, nb, _ptr(batch_id), _ptr(est), len(worker_id),
+                                          _ptr(worker_id), _ptr(loads), _ptr(ob), _ptr(ow),
+                                          capi.MEM_HOST))
+        return ob[:nb], ow[:nb], loads
+
+    def schedule(self, eff, arrival, ids, slice_len, lat, mem, worker_id, loads, first_batch_id=0):
+        """One SCLS tick: batch_requests then offload (sched_policies.cpp:93-112)."""
+        eff = np.ascontiguousarray(eff, np.int32)
+        arrival = np.ascontiguousarray(arrival, np.float64)
+        ids = np.ascontiguousarray(ids, np.int64)
+        worker_id = np.ascontiguousarray(worker_id, np.int32)
+        loads = np.array(loads, np.float64)
+        n = len(eff)
+        seg = np.zeros(n + 1, np.int32)
+        l_in = np.zeros(max(n, 1), np.int32)
+        est = np.zeros(max(n, 1), np.float64)
+        mid = np.zeros(max(n, 1), np.int64)
+        ob = np.zeros(max(n, 1), np.int64)
+        ow = np.zeros(max(n, 1), np.int32)
+        out = capi.Batches(0, None, seg.ctypes.data_as(C.POINTER(C.c_int32)),
+                           l_in.ctypes.data_as(C.POINTER(C.c_int32)),
+                           est.ctypes.data_as(C.POINTER(C.c_double)),
+                           mid.ctypes.data_as(C.POINTER(C.c_int64)))
+        self._check(self.lib.scls_schedule(self.h, n, _ptr(eff), _ptr(arrival), _ptr(ids), slice_len,
+                                           C.byref(lat), C.byref(mem), first_batch_id,
+                                           len(worker_id), _ptr(worker_id), _ptr(loads),
+                                           C.byref(out), _ptr(ob), _ptr(ow), capi.MEM_HOST))
+        k = out.n_batches
+        return dict(n_batches=k, seg_begin=seg[:k + 1], l_in=l_in[:k], est=est[:k],
+                    member_id=mid[:n], assign_batch=ob[:k], assign_worker=ow[:k], loads=loads)
+
+    def schedule_device(self, n, eff, arrival, ids, slice_len, lat, mem, worker_id, loads, out_bufs,
+                        first_batch_id=0):
+        """Device-resident tick: every array is a torch CUDA tensor (mem=DEVICE)."""
+        seg, l_in, est, mid, ob, ow = out_bufs
+        out = capi.Batches(0, None, C.cast(C.c_void_p(seg.data_ptr()), C.POINTER(C.c_int32)),
+                           C.cast(C.c_void_p(l_in.data_ptr()), C.POINTER(C.c_int32)),
+                           C.cast(C.c_void_p(est.data_ptr()), C.POINTER(C.c_double)),
+                           C.cast(C.c_void_p(mid.data_ptr()), C.POINTER(C.c_int64)))
+        self._check(self.lib.scls_schedule(self.h, n, _dev_ptr(eff), _dev_ptr(arrival), _dev_ptr(ids),
+                                           slice_len, C.byref(lat), C.byref(mem), first_batch_id,
+                                           worker_id.numel(), _dev_ptr(worker_id), _dev_ptr(loads),
+                                           C.byref(out), _dev_ptr(ob), _dev_ptr(ow), capi.MEM_DEVICE))
+        return out.n_batches
+
+    # -- simulator ------------------------------------------------------------------------
+    def simulate(self, traces, cfgs, lat, mem, cfg_index=None, hist_bins=64, n_logged=0,
+                 rec_cap=0, mem_cap=0):
+        """Simulator::run + compute for every trace (list of (arrival, input_len,
+        gen_len)).  Returns (results, hist[, log])."""
+        offs = np.zeros(len(traces) + 1, np.int64)
+        for i, t in enumerate(traces):
+            offs[i + 1] = offs[i] + len(t[0])
+        tot = max(int(offs[-1]), 1)
+        arr = np.zeros(tot, np.float64)
+        inp = np.zeros(tot, np.int32)
+        gen = np.zeros(tot, np.int32)
+        for i, (a, b, g) in enumerate(traces):
+            arr[offs[i]:offs[i + 1]] = a
+            inp[offs[i]:offs[i + 1]] = b
+            gen[offs[i]:offs[i + 1]] = g
+        return self.simulate_flat(offs, arr, inp, gen, cfgs, lat, mem, cfg_index, hist_bins,
+                                  n_logged, rec_cap, mem_cap)
+
+    def simulate_flat(self, offs, arr, inp, gen, cfgs, lat, mem, cfg_index=None, hist_bins=64,
+                      n_logged=0, rec_cap=0, mem_cap=0):
+        if isinstance(cfgs, capi.SchedCfg):
+            cfgs = [cfgs]
+        ntr = len(offs) - 1
+        cfg_arr = (capi.SchedCfg * len(cfgs))(*cfgs)
+        idx = None if cfg_index is None else np.ascontiguousarray(cfg_index, np.int32)
+        res = (capi.TraceResult * max(ntr, 1))()
+        hist = np.zeros(max(ntr * hist_bins, 1), np.int64)
+        log = None
+        if n_logged:
+            recs = (capi.EventRecord * (n_logged * rec_cap))()
+            mems = (capi.Member * max(n_logged * mem_cap, 1))()
+            rc = np.zeros(n_logged, np.int64)
+            mc = np.zeros(n_logged, np.int64)
+            st = capi.EventLog(n_logged, rec_cap, mem_cap, recs, mems,
+                               rc.ctypes.data_as(C.POINTER(C.c_int64)),
+                               mc.ctypes.data_as(C.POINTER(C.c_int64)))
+            log = dict(struct=st, records=recs, members=mems, rec_count=rc, mem_count=mc,
+                       rec_cap=rec_cap, mem_cap=mem_cap)
+        self._check(self.lib.scls_simulate(self.h, ntr, _ptr(np.ascontiguousarray(offs, np.int64)),
+                                           _ptr(arr), _ptr(inp), _ptr(gen), len(cfgs), cfg_arr,
+                                           _ptr(idx), C.byref(lat), C.byref(mem), res, hist_bins,
+                                           _ptr(hist), C.byref(log["struct"]) if log else None,
+                                           capi.MEM_HOST))
+        hist = hist[:ntr * hist_bins].reshape(ntr, hist_bins)
+        if log is not None:
+            return res, hist, log
+        return res, hist
+
+
+def generate(spec):
+    """workload.h:78 (host) -> (arrival, input_len, gen_len)."""
+    lib = load()
+    n = C.c_int64(0)
+    st = lib.scls_generate(C.byref(spec), 0, C.byref(n), None, None, None)
+    if st not in (0, capi.ERR_CAPACITY):
+        buf = C.create_string_buffer(4096)
+        lib.scls_last_error(None, buf, 4096)
+        raise SclsError(st, buf.value.decode())
+    k = n.value
+    arr = np.zeros(max(k, 1), np.float64)
+    inp = np.zeros(max(k, 1), np.int32)
+    gen = np.zeros(max(k, 1), np.int32)
+    st = lib.scls_generate(C.byref(spec), k, C.byref(n), _ptr(arr), _ptr(inp), _ptr(gen))
+    if st:
+        raise SclsError(st, "generate failed")
+    return arr[:k], inp[:k], gen[:k]
+
+
+def make_pool(n, seed=7):
+    """bench_batcher.cpp:27-42 -> (eff, arrival, ids, gen_len)."""
+    lib = load()
+    eff = np.zeros(max(n, 1), np.int32)
+    arr = np.zeros(max(n, 1), np.float64)
+    ids = np.zeros(max(n, 1), np.int64)
+    gen = np.zeros(max(n, 1), np.int32)
+    st = lib.scls_make_pool(n, seed, _ptr(eff), _ptr(arr), _ptr(ids), _ptr(gen))
+    if st:
+        raise SclsError(st, "make_pool failed")
+    return eff[:n], arr[:n], ids[:n], gen[:n]

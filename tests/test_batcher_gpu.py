@@ -1,0 +1,193 @@
+"""GPU parity of the scheduling core (batch_requests, offload, schedule,
+batched estimators) against the C oracle and the golden fixtures.
+Bit-exact: batch boundaries, members, l_in, est bits, assignments, loads."""
+import numpy as np
+import pytest
+
+from paper_2406_13511_b200 import capi
+from paper_2406_13511_b200.lib import SclsError
+from tests.helpers import (MEMORIES, padding_heavy_model, planned_total, random_instances,
+                           reference_model, sha)
+
+pytestmark = pytest.mark.gpu
+
+
+def assert_same_batches(a, b, ctx_msg=""):
+    assert a["n_batches"] == b["n_batches"], ctx_msg
+    for k in ("seg_begin", "l_in", "est", "member_id"):
+        assert np.array_equal(a[k], b[k]), (ctx_msg, k)
+
+
+def test_golden_pools(ctx, orc, golden):
+    """bench_batcher.cpp pools up to 2^20 (configs[2]) vs the reference's
+    fingerprints; the 1M analytic pool is SURVEY's C3 (11,820 batches)."""
+    lat = capi.builtin_latency_model()
+    for case in golden["batcher"]:
+        eff, arr, ids, _ = orc.make_pool(case["n"], case["seed"])
+        res = ctx.batch_requests(eff, arr, ids, case["slice_len"], lat, MEMORIES[case["memory"]]())
+        msg = (case["n"], case["slice_len"], case["memory"])
+        assert res["n_batches"] == case["n_batches"], msg
+        assert float(planned_total(res["est"])).hex() == case["sum_est"], msg
+        assert sha(res["seg_begin"].astype(np.int32)) == case["seg"], msg
+        assert sha(res["l_in"].astype(np.int32)) == case["l_in"], msg
+        assert sha(res["est"].astype(np.float64)) == case["est"], msg
+        assert sha(res["member_id"].astype(np.int64)) == case["member"], msg
+
+
+def test_random_instances_vs_oracle(ctx, orc):
+    """batcher_test.cpp:126-166 instances (600), incl. arrival ties."""
+    lat = reference_model()
+    for i, (eff, arr, ids, s, mem) in enumerate(random_instances(trials=600)):
+        a = ctx.batch_requests(eff, arr, ids, s, lat, mem, 3)
+        b = orc.batch_requests(eff, arr, ids, s, lat, mem, 3)
+        assert_same_batches(a, b, i)
+        # order[] is the sorted permutation
+        assert np.array_equal(ids[a["order"]], a["member_id"])
+
+
+def test_medium_pools_all_models(ctx, orc):
+    rng = np.random.default_rng(11)
+    for n in (31, 32, 33, 63, 64, 65, 1000, 4097, 20000):
+        eff = rng.integers(1, 2048, n).astype(np.int32)
+        arr = rng.random(n) * 50
+        ids = rng.permutation(n).astype(np.int64) - n // 2  # negative ids too
+        for mname in ("rule", "analytic", "tight"):
+            for s in (1, 16, 128):
+                lat = capi.builtin_latency_model()
+                a = ctx.batch_requests(eff, arr, ids, s, lat, MEMORIES[mname]())
+                b = orc.batch_requests(eff, arr, ids, s, lat, MEMORIES[mname]())
+                assert_same_batches(a, b, (n, mname, s))
+
+
+def test_huge_windows_use_global_path(ctx, orc):
+    """Analytic model with S=1: K(L) reaches ~28k, beyond the smem ring."""
+    rng = np.random.default_rng(5)
+    n = 40000
+    eff = np.sort(rng.integers(1, 64, n)).astype(np.int32)
+    arr = rng.random(n)
+    ids = np.arange(n, dtype=np.int64)
+    mem = capi.builtin_analytic_memory_model()
+    lat = capi.builtin_latency_model()
+    a = ctx.batch_requests(eff, arr, ids, 1, lat, mem)
+    b = orc.batch_requests(eff, arr, ids, 1, lat, mem)
+    assert_same_batches(a, b)
+
+
+def test_ties_and_degenerate_keys(ctx, orc):
+    rule = MEMORIES["rule"]()
+    flat = capi.latency_model(p2=1.0)  # every partition costs the same: pure tie-breaking
+    for n in (2, 33, 100, 3000):
+        eff = np.full(n, 100, np.int32)
+        arr = np.zeros(n)
+        ids = np.arange(n, dtype=np.int64)[::-1].copy()
+        assert_same_batches(ctx.batch_requests(eff, arr, ids, 128, flat, rule),
+                            orc.batch_requests(eff, arr, ids, 128, flat, rule), n)
+    # -0.0 vs +0.0 arrivals compare equal (ties fall to id)
+    eff = np.array([5, 5, 5, 5], np.int32)
+    arr = np.array([0.0, -0.0, 0.0, -0.0])
+    ids = np.array([3, 2, 1, 0], np.int64)
+    assert_same_batches(ctx.batch_requests(eff, arr, ids, 128, reference_model(), rule),
+                        orc.batch_requests(eff, arr, ids, 128, reference_model(), rule))
+
+
+def test_known_answers(ctx):
+    rule = MEMORIES["rule"]()
+    r = ctx.batch_requests([100, 100], [0.0, 0.0], [0, 1], 128, capi.latency_model(p2=1.0), rule)
+    assert r["n_batches"] == 2
+    r = ctx.batch_requests([10] * 8 + [1024], [0.0] * 9, list(range(9)), 128,
+                           padding_heavy_model(), rule)
+    assert r["n_batches"] == 2 and r["member_id"][-1] == 8 and r["l_in"].tolist() == [10, 1024]
+    r = ctx.batch_requests([600, 600, 10, 10], [2.0, 1.0, 3.0, 0.5], [3, 1, 2, 0], 128,
+                           padding_heavy_model(), rule)
+    assert r["member_id"].tolist() == [0, 2, 1, 3] and r["seg_begin"].tolist() == [0, 2, 4]
+    r = ctx.batch_requests([10, 310, 610, 910, 1210, 1510], [0.0] * 6, list(range(6)), 128,
+                           reference_model(), rule, first_batch_id=42)
+    assert r["batch_id"][0] == 42
+    r = ctx.batch_requests([], [], [], 128, reference_model(), rule)
+    assert r["n_batches"] == 0
+
+
+def test_infeasible_singleton(ctx, orc):
+    mem = capi.analytic(105.0, 3.0, 2.0, 1.0, 1.0)
+    with pytest.raises(SclsError) as e:
+        ctx.batch_requests([200], [0.0], [7], 10, reference_model(), mem)
+    assert e.value.status == capi.ERR_INFEASIBLE_REQUEST and e.value.request_id == 7
+    # the first offender in sorted order (batcher.cpp:40-46)
+    with pytest.raises(SclsError) as e:
+        ctx.batch_requests([50, 300, 200, 90], [0.0, 1.0, 2.0, 3.0], [10, 11, 12, 13], 10,
+                           reference_model(), mem)
+    assert e.value.request_id == 12
+
+
+def test_offload_fixtures(ctx, orc, golden):
+    ob, ow, nl = ctx.offload([0, 1, 2, 3], [6.0, 10.0, 2.0, 6.0], [0, 1], [0.0, 0.0])
+    assert list(zip(ob.tolist(), ow.tolist())) == [(1, 0), (0, 1), (3, 1), (2, 0)]
+    assert nl.tolist() == [12.0, 12.0]
+    ob, ow, nl = ctx.offload([5], [4.0], [0, 1, 2], [5.0, 3.0, 9.0])
+    assert ow.tolist() == [1] and nl.tolist() == [5.0, 7.0, 9.0]
+    ob, ow, _ = ctx.offload([0, 1], [1.0, 1.0], [0, 1, 2], [2.0, 2.0, 2.0])
+    assert ow.tolist() == [0, 1]
+    ob, ow, _ = ctx.offload([10, 11, 12], [3.0, 3.0, 3.0], [0], [0.0])
+    assert ob.tolist() == [10, 11, 12]
+    with pytest.raises(SclsError) as e:
+        ctx.offload([0], [1.0], [], [])
+    assert e.value.status == capi.ERR_NO_WORKERS
+    lat = capi.builtin_latency_model()
+    for case in golden["offload"]:
+        eff, arr, ids, _ = orc.make_pool(case["n"], 7)
+        res = orc.batch_requests(eff, arr, ids, 128, lat, MEMORIES[case["memory"]]())
+        loads = [float.fromhex(x) for x in case["loads"]]
+        ob, ow, nl = ctx.offload(res["batch_id"], res["est"], np.arange(8, dtype=np.int32), loads)
+        assert sha(ob) == case["batch"] and sha(ow) == case["worker"]
+        assert [float(x).hex() for x in nl] == case["final_loads"]
+
+
+def test_offload_random_vs_oracle(ctx, orc):
+    rng = np.random.default_rng(12345)
+    for trial in range(200):
+        nw = int(rng.integers(1, 40))
+        nb = int(rng.integers(0, 300))
+        loads = rng.random(nw) * 10
+        if trial % 4 == 0:
+            loads = np.round(loads)  # load ties
+        est = 0.01 + rng.random(nb) * 5
+        if trial % 3 == 0:
+            est = np.round(est, 1)  # estimate ties
+        wid = rng.permutation(nw).astype(np.int32)
+        bid = np.arange(nb, dtype=np.int64) + 100
+        a = ctx.offload(bid, est, wid, loads)
+        b = orc.offload(bid, est, wid, loads)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), trial
+
+
+def test_schedule_equals_batch_then_offload(ctx, orc):
+    eff, arr, ids, _ = orc.make_pool(50000, 3)
+    lat = capi.builtin_latency_model()
+    mem = MEMORIES["analytic"]()
+    loads = [0.5 * w for w in range(8)]
+    s = ctx.schedule(eff, arr, ids, 128, lat, mem, np.arange(8, dtype=np.int32), loads, 7)
+    b = orc.batch_requests(eff, arr, ids, 128, lat, mem, 7)
+    ob, ow, nl = orc.offload(b["batch_id"], b["est"], np.arange(8, dtype=np.int32), loads)
+    assert_same_batches(s, b)
+    assert np.array_equal(s["assign_batch"], ob) and np.array_equal(s["assign_worker"], ow)
+    assert np.array_equal(s["loads"], nl)
+
+
+def test_batched_estimators(ctx, orc):
+    rng = np.random.default_rng(2)
+    lat = capi.builtin_latency_model()
+    n = rng.integers(1, 500, 5000).astype(np.int32)
+    l_in = rng.integers(1, 4096, 5000).astype(np.int32)
+    l_out = rng.integers(-2, 1024, 5000).astype(np.int32)
+    got = ctx.batch_serve_time(n, l_in, l_out, lat)
+    want = np.array([orc.batch_serve_time(lat, int(a), int(b), int(c)) for a, b, c in zip(n, l_in, l_out)])
+    assert np.array_equal(got, want)
+    for mname in ("rule", "analytic", "tight"):
+        mem = MEMORIES[mname]()
+        got = ctx.would_oom(n[:2000], l_in[:2000], 128, mem)
+        want = np.array([orc.would_oom(mem, int(a), int(b), 128) for a, b in zip(n[:2000], l_in[:2000])])
+        assert np.array_equal(got, want), mname
+        got = ctx.max_batch_size(l_in[:2000], 32, mem)
+        want = np.array([orc.max_batch_size(mem, int(b), 32) for b in l_in[:2000]])
+        assert np.array_equal(got, want), mname
