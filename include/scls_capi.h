@@ -129,6 +129,10 @@ int64_t scls_last_request_id(const scls_ctx* ctx);
 void scls_last_timings(const scls_ctx* ctx, float out_ms[8]);
 /* Number of CUDA kernel launches issued by the last call. */
 int64_t scls_last_launch_count(const scls_ctx* ctx);
+/* Diagnostics: enable/disable clock64 phase counters in the DP chain kernel
+ * and read-and-reset them (cycles: main chain, main barrier wait, helper
+ * staging, helper far candidates, helper wait, helper-warp count). */
+scls_status scls_debug_dp_profile(scls_ctx* ctx, int32_t enable, uint64_t out[8]);
 
 /* ---- validation (host only; mirrors the reference validators) ----------- */
 scls_status scls_validate_latency(const scls_latency* m);   /* cost_model.cpp:70-87    */

@@ -22,6 +22,7 @@
 
 #include "batcher.cuh"
 #include "radix.cuh"
+#include "dp_chain.cuh"
 #include "scls_common.cuh"
 
 namespace scls {
@@ -149,6 +150,12 @@ __global__ void runs_kernel(int64_t n, const int32_t* __restrict__ flag,
   if (p == n - 1 || flag[p + 1]) run_need[run] = Krow[p];
 }
 
+__global__ void row_cbase_kernel(int64_t n, const int32_t* __restrict__ run_of_row,
+                                 const int32_t* __restrict__ run_off, int32_t* __restrict__ cbase) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) cbase[p] = run_off[run_of_row[p]] - 1;
+}
+
 __global__ void cost_table_kernel(int32_t n_runs, const int32_t* __restrict__ run_first,
                                   const int32_t* __restrict__ run_need,
                                   const int32_t* __restrict__ run_off,
@@ -164,137 +171,6 @@ __global__ void cost_table_kernel(int32_t n_runs, const int32_t* __restrict__ ru
       cost[off + k - 1] = __dadd_rn(prefill_time(lat, k, L),
                                     decode_time_from_sum(lat, k, sum_l, slice));
     }
-  }
-}
-
-// ---- 4. the DP chain ------------------------------------------------------------
-//
-// One CTA, 16 warps.  Rows are processed in tiles of 32; lane m of the main
-// warp (warp 0) owns row r = 32t + 1 + m of tile t.  A row's candidates
-// split into three disjoint k-ranges by the age of T[r-k]:
-//   far   j = r-k <= 32(t-1)        computed by helper warps one tile ahead
-//   mid   32(t-1) < j <= 32t        main warp, at tile start (all final)
-//   near  32t < j < r               main warp, the serial in-tile chain
-// They are merged far -> mid -> near with k strictly decreasing; the update
-// rule `cand <= acc` then makes the smallest k win ties, which is exactly
-// the reference's ascending-k scan with strict `<` (batcher.cpp:42-51).
-// Helpers are the warps with (warp % 4) != 0 so the main warp owns its SMSP.
-
-constexpr int kDpThreads = 512;
-constexpr int kDpRing = 4096;  // smem ring of recent T values (32 KB)
-
-template <bool kGlobalT>
-__global__ void __launch_bounds__(kDpThreads, 1)
-    dp_chain_kernel(int32_t n, const int32_t* __restrict__ Krow,
-                    const int32_t* __restrict__ run_of_row, const int32_t* __restrict__ run_off,
-                    const double* __restrict__ cost, double* __restrict__ T,
-                    int32_t* __restrict__ split) {
-  extern __shared__ double ring[];
-  __shared__ double Fv[2][32];
-  __shared__ int32_t Fk[2][32];
-  constexpr int M = kDpRing - 1;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 32) {
-    Fv[0][lane] = __longlong_as_double(0x7ff0000000000000ll);
-    Fk[0][lane] = 0;
-  }
-  if (tid == 0) {
-    ring[0] = 0.0;
-    T[0] = 0.0;
-    split[0] = 0;
-  }
-  __syncthreads();
-  const int ntiles = (n + 31) >> 5;
-  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-  for (int t = 0; t < ntiles; ++t) {
-    const int buf = t & 1;
-    const int tB = t << 5;
-    if (warp == 0) {
-      const int r = tB + 1 + lane;
-      const bool valid = r <= n;
-      const int Wr = valid ? Krow[r - 1] : 0;
-      const int cbase = valid ? run_off[run_of_row[r - 1]] - 1 : 0;
-      double acc = Fv[buf][lane];
-      int kb = Fk[buf][lane];
-      // near-chain costs, prefetched: step s uses k = lane + 1 - s.
-      double cn[32];
-#pragma unroll
-      for (int s = 0; s < 32; ++s) {
-        const int k = lane + 1 - s;
-        cn[s] = (k >= 1 && k <= Wr) ? cost[cbase + k] : 0.0;
-      }
-      // mid: j = tB-31 .. tB, ascending (k descending).
-#pragma unroll 8
-      for (int jj = 0; jj < 32; ++jj) {
-        const int j = tB - 31 + jj;
-        if (j >= 0) {
-          const int k = r - j;
-          if (k <= Wr) {
-            const double cand = __dadd_rn(ring[j & M], cost[cbase + k]);
-            if (cand <= acc) {
-              acc = cand;
-              kb = k;
-            }
-          }
-        }
-      }
-      // near: the serial chain.  T[tB] is final; each step finalises one row.
-      double Tj = ring[tB & M];
-#pragma unroll
-      for (int s = 0; s < 32; ++s) {
-        if (tB + 1 + s > n) break;
-        const int k = lane + 1 - s;
-        if (k >= 1 && k <= Wr) {
-          const double cand = __dadd_rn(Tj, cn[s]);
-          if (cand <= acc) {
-            acc = cand;
-            kb = k;
-          }
-        }
-        Tj = __shfl_sync(0xffffffffu, acc, s);
-      }
-      if (valid) {
-        T[r] = acc;
-        split[r] = r - kb;
-        ring[r & M] = acc;
-      }
-    } else if ((warp & 3) != 0 && t + 1 < ntiles) {
-      // Helpers: far part of tile t+1 (j <= tB), one row per warp at a time.
-      const int h = warp - 1 - (warp >> 2);  // 0..11
-      constexpr int kHelpers = kDpThreads / 32 - kDpThreads / 128;
-      for (int m = h; m < 32; m += kHelpers) {
-        const int r2 = tB + 32 + 1 + m;
-        double best = kInf;
-        int bk = 0;
-        if (r2 <= n) {
-          const int W2 = Krow[r2 - 1];
-          const int cb2 = run_off[run_of_row[r2 - 1]] - 1;
-          for (int k = 33 + m + lane; k <= W2; k += 32) {
-            const int j = r2 - k;
-            const double tv = kGlobalT ? T[j] : ring[j & M];
-            const double cand = __dadd_rn(tv, cost[cb2 + k]);
-            if (cand < best) {
-              best = cand;
-              bk = k;
-            }
-          }
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-            const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
-            if (ov < best || (ov == best && ok < bk)) {
-              best = ov;
-              bk = ok;
-            }
-          }
-        }
-        if (lane == 0) {
-          Fv[buf ^ 1][m] = best;
-          Fk[buf ^ 1][m] = bk;
-        }
-      }
-    }
-    __syncthreads();
   }
 }
 
@@ -475,15 +351,24 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
   double* T = (double*)ctx->buf(kSlotT, sizeof(double) * (n + 1));
   int32_t* split = (int32_t*)ctx->buf(kSlotSplit, sizeof(int32_t) * (n + 1));
   if (!T || !split) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
-  const size_t ring_bytes = sizeof(double) * kDpRing;
-  if (k_max + 64 <= kDpRing) {
-    dp_chain_kernel<false><<<1, kDpThreads, ring_bytes, s>>>((int32_t)n, Krow, run_excl, run_off,
-                                                             cost, T, split);
-  } else {
-    dp_chain_kernel<true><<<1, kDpThreads, ring_bytes, s>>>((int32_t)n, Krow, run_excl, run_off,
-                                                            cost, T, split);
-  }
+  // cost base per row (cost[cbase[p] + k] = c(L_p, k)), reusing the flag slot
+  int32_t* cbase = flag;
+  row_cbase_kernel<<<grid_n, threads, 0, s>>>(n, run_excl, run_off, cbase);
   SCLS_LAUNCHED();
+  const size_t smem = sizeof(DpSmem);
+  const bool global_t = k_max + 64 > kDpRing;
+  const bool int_cmp = !std::signbit(in.lat->p1) && !std::signbit(in.lat->p2) && !std::signbit(in.lat->p3) &&
+                       !std::signbit(in.lat->p4) && !std::signbit(in.lat->d1) && !std::signbit(in.lat->d2) &&
+                       !std::signbit(in.lat->d3) && !std::signbit(in.lat->d4);
+  auto launch = [&](auto kern) -> scls_status {
+    SCLS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<1, kDpThreads, smem, s>>>((int32_t)n, Krow, cbase, cost, T, split, ctx->dp_prof);
+    SCLS_LAUNCHED();
+    return SCLS_OK;
+  };
+  if (global_t) stt = int_cmp ? launch(dp_chain_kernel<true, true>) : launch(dp_chain_kernel<true, false>);
+  else stt = int_cmp ? launch(dp_chain_kernel<false, true>) : launch(dp_chain_kernel<false, false>);
+  if (stt) return stt;
   SCLS_CUDA(cudaEventRecord(ctx->ev[3], s));
 
   // ---- 5. backtrack: mark the ancestors of n in the split forest

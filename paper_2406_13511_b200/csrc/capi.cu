@@ -212,6 +212,28 @@ void scls_last_timings(const scls_ctx* ctx, float out_ms[8]) {
 
 int64_t scls_last_launch_count(const scls_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+scls_status scls_debug_dp_profile(scls_ctx* ctx, int32_t enable, uint64_t out[8]) {
+  if (!ctx) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null context");
+  SCLS_CUDA(cudaSetDevice(ctx->device));
+  if (enable && !ctx->dp_prof) {
+    SCLS_CUDA(cudaMalloc(&ctx->dp_prof, 8 * sizeof(unsigned long long)));
+    SCLS_CUDA(cudaMemset(ctx->dp_prof, 0, 8 * sizeof(unsigned long long)));
+  }
+  if (out) {
+    for (int i = 0; i < 8; ++i) out[i] = 0;
+    if (ctx->dp_prof) {
+      SCLS_CUDA(cudaStreamSynchronize(ctx->stream));
+      SCLS_CUDA(cudaMemcpy(out, ctx->dp_prof, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+      SCLS_CUDA(cudaMemset(ctx->dp_prof, 0, 8 * sizeof(unsigned long long)));
+    }
+  }
+  if (!enable && ctx->dp_prof) {
+    cudaFree(ctx->dp_prof);
+    ctx->dp_prof = nullptr;
+  }
+  return SCLS_OK;
+}
+
 // ---- validation: cost_model.cpp:70-87, memory_model.cpp:92-120, sched_policies.cpp:45-57
 
 scls_status scls_validate_latency(const scls_latency* m) {

@@ -22,6 +22,7 @@ struct scls_ctx {
   float timings[8] = {0};
   cudaEvent_t ev[16] = {};
   int sm_count = 148;
+  unsigned long long* dp_prof = nullptr;  // device counters when profiling is on
 
   // Named grow-only device buffers (scratch reused across calls).
   struct Buf {

@@ -20,7 +20,7 @@
 namespace scls {
 namespace {
 
-enum : int { kSlotOKeys = 16, kSlotOVals, kSlotOKeysAlt, kSlotOValsAlt, kSlotORange };
+enum : int { kSlotOKeys = 18, kSlotOVals, kSlotOKeysAlt, kSlotOValsAlt, kSlotORange, kSlotOEst, kSlotOSlots };
 
 __global__ void est_keys_kernel(int64_t nb, const double* __restrict__ est,
                                 uint64_t* __restrict__ keys, int32_t* __restrict__ vals,
@@ -55,150 +55,173 @@ __global__ void init_range_kernel(unsigned long long* range) {
   range[1] = 0;
 }
 
-// (load, id, index) lexicographic "a before b" — the reference's selection.
-__device__ __forceinline__ bool wins(double la, int ia, int xa, double lb, int ib, int xb) {
-  return la < lb || (la == lb && (ia < ib || (ia == ib && xa < xb)));
+// Worker slots are renumbered in (worker_id, index) order once per call, so
+// the reference's tie rule (lowest worker_id, then first position,
+// offloader.cpp:39-47) becomes "lowest slot wins ties" and a comparison tree
+// only needs `right < left` on the load.
+__global__ void slot_order_kernel(int32_t nw, const int32_t* __restrict__ worker_id,
+                                  int32_t* __restrict__ slot_src, int32_t* __restrict__ slot_id) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int32_t i = 0; i < nw; ++i) {  // insertion sort by (id, index); W is small
+    const int32_t id = worker_id[i];
+    int32_t j = i;
+    while (j > 0 && slot_id[j - 1] > id) {
+      slot_id[j] = slot_id[j - 1];
+      slot_src[j] = slot_src[j - 1];
+      --j;
+    }
+    slot_id[j] = id;
+    slot_src[j] = i;
+  }
 }
 
+__global__ void gather_sorted_kernel(int64_t nb, const int32_t* __restrict__ order,
+                                     const int64_t* __restrict__ batch_id,
+                                     const double* __restrict__ est, double* __restrict__ est_sorted,
+                                     int64_t* __restrict__ out_b) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nb) return;
+  const int32_t i = order[k];
+  est_sorted[k] = est[i];
+  out_b[k] = batch_id[i];
+}
+
+__global__ void slot_to_worker_kernel(int64_t nb, const int32_t* __restrict__ slot_id,
+                                      int32_t* __restrict__ out_w) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < nb) out_w[k] = slot_id[out_w[k]];
+}
+
+constexpr int kChunk = 2048;
+
+// Thread 0 runs the serial greedy chain over the sorted estimates with the W
+// loads in registers and a log2(W)-deep comparison tree; warp 1 streams the
+// next chunk of estimates into shared memory meanwhile.
 template <int W>
-__global__ void greedy_small_kernel(int64_t nb, const int32_t* __restrict__ order,
-                                    const int64_t* __restrict__ batch_id,
-                                    const double* __restrict__ est, int32_t nw,
-                                    const int32_t* __restrict__ worker_id,
-                                    double* __restrict__ load, int64_t* __restrict__ out_b,
-                                    int32_t* __restrict__ out_w) {
-  if (threadIdx.x != 0) return;
-  double l[W];
-  int id[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) {
-    l[w] = w < nw ? load[w] : __longlong_as_double(0x7ff0000000000000ll);
-    id[w] = w < nw ? worker_id[w] : 0x7fffffff;
+__global__ void __launch_bounds__(64) greedy_small_kernel(int64_t nb, const double* __restrict__ est_sorted,
+                                                          int32_t nw, const int32_t* __restrict__ slot_src,
+                                                          double* __restrict__ load,
+                                                          int32_t* __restrict__ out_slot) {
+  __shared__ double se[2][kChunk];
+  const int tid = threadIdx.x;
+  const int nchunks = (int)((nb + kChunk - 1) / kChunk);
+  if (tid >= 32) {
+    for (int i = tid - 32; i < kChunk && i < nb; i += 32) se[0][i] = est_sorted[i];
   }
-  int32_t nxt = nb > 0 ? order[0] : 0;
-  double e_nxt = nb > 0 ? est[nxt] : 0.0;
-  for (int64_t k = 0; k < nb; ++k) {
-    const int32_t cur = nxt;
-    const double e = e_nxt;
-    if (k + 1 < nb) {  // prefetch the next batch off the chain
-      nxt = order[k + 1];
-      e_nxt = est[nxt];
+  double l[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) l[w] = (tid == 0 && w < nw) ? load[slot_src[w]] : __longlong_as_double(0x7ff0000000000000ll);
+  __syncthreads();
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t base = (int64_t)c * kChunk;
+    if (tid >= 32 && c + 1 < nchunks) {
+      const int64_t nb2 = base + kChunk;
+      for (int i = tid - 32; i < kChunk && nb2 + i < nb; i += 32) se[(c + 1) & 1][i] = est_sorted[nb2 + i];
     }
-    // Tournament over the W slots.
-    double bl[W];
-    int bi[W], bx[W];
+    if (tid == 0) {
+      const int cnt = (int)min((int64_t)kChunk, nb - base);
+      const double* e = se[c & 1];
+      for (int i = 0; i < cnt; ++i) {
+        double bl[W];
+        int bx[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-      bl[w] = l[w];
-      bi[w] = id[w];
-      bx[w] = w;
-    }
-#pragma unroll
-    for (int span = 1; span < W; span <<= 1) {
-#pragma unroll
-      for (int w = 0; w + span < W; w += 2 * span) {
-        if (wins(bl[w + span], bi[w + span], bx[w + span], bl[w], bi[w], bx[w])) {
-          bl[w] = bl[w + span];
-          bi[w] = bi[w + span];
-          bx[w] = bx[w + span];
+        for (int w = 0; w < W; ++w) {
+          bl[w] = l[w];
+          bx[w] = w;
         }
+#pragma unroll
+        for (int span = 1; span < W; span <<= 1) {
+#pragma unroll
+          for (int w = 0; w + span < W; w += 2 * span) {
+            if (bl[w + span] < bl[w]) {
+              bl[w] = bl[w + span];
+              bx[w] = bx[w + span];
+            }
+          }
+        }
+        const double ei = e[i];
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          if (w == bx[0]) l[w] = __dadd_rn(l[w], ei);
+        out_slot[base + i] = bx[0];
       }
     }
-    const int t = bx[0];
+    __syncthreads();
+  }
+  if (tid == 0) {
 #pragma unroll
     for (int w = 0; w < W; ++w)
-      if (w == t) l[w] = __dadd_rn(l[w], e);
-    out_b[k] = batch_id[cur];
-    out_w[k] = bi[0];
+      if (w < nw) load[slot_src[w]] = l[w];
   }
-#pragma unroll
-  for (int w = 0; w < W; ++w)
-    if (w < nw) load[w] = l[w];
 }
 
-__global__ void greedy_warp_kernel(int64_t nb, const int32_t* __restrict__ order,
-                                   const int64_t* __restrict__ batch_id,
-                                   const double* __restrict__ est, int32_t nw,
-                                   const int32_t* __restrict__ worker_id,
-                                   double* __restrict__ load, int64_t* __restrict__ out_b,
-                                   int32_t* __restrict__ out_w) {
+// 9..32 workers: lane = slot, shuffle argmin with lower lane winning ties.
+__global__ void greedy_warp_kernel(int64_t nb, const double* __restrict__ est_sorted, int32_t nw,
+                                   const int32_t* __restrict__ slot_src, double* __restrict__ load,
+                                   int32_t* __restrict__ out_slot) {
   const int lane = threadIdx.x;
-  double l = lane < nw ? load[lane] : __longlong_as_double(0x7ff0000000000000ll);
-  const int id = lane < nw ? worker_id[lane] : 0x7fffffff;
+  double l = lane < nw ? load[slot_src[lane]] : __longlong_as_double(0x7ff0000000000000ll);
+  double e_next = nb > 0 ? est_sorted[0] : 0.0;
   for (int64_t k = 0; k < nb; ++k) {
-    const int32_t cur = order[k];
-    const double e = est[cur];
+    const double e = e_next;
+    if (k + 1 < nb) e_next = est_sorted[k + 1];
     double bl = l;
-    int bi = id, bx = lane;
+    int bx = lane;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const double ol = __shfl_xor_sync(~0u, bl, o);
-      const int oi = __shfl_xor_sync(~0u, bi, o);
       const int ox = __shfl_xor_sync(~0u, bx, o);
-      if (wins(ol, oi, ox, bl, bi, bx)) {
+      if (ol < bl || (ol == bl && ox < bx)) {
         bl = ol;
-        bi = oi;
         bx = ox;
       }
     }
     if (lane == bx) l = __dadd_rn(l, e);
-    if (lane == 0) {
-      out_b[k] = batch_id[cur];
-      out_w[k] = bi;
-    }
+    if (lane == 0) out_slot[k] = bx;
   }
-  if (lane < nw) load[lane] = l;
+  if (lane < nw) load[slot_src[lane]] = l;
 }
 
-// Any W: one CTA, loads in shared memory, block argmin per batch.
-__global__ void greedy_block_kernel(int64_t nb, const int32_t* __restrict__ order,
-                                    const int64_t* __restrict__ batch_id,
-                                    const double* __restrict__ est, int32_t nw,
-                                    const int32_t* __restrict__ worker_id,
-                                    double* __restrict__ load, int64_t* __restrict__ out_b,
-                                    int32_t* __restrict__ out_w) {
+// Any W: one CTA, loads in global memory, block argmin per batch.
+__global__ void greedy_block_kernel(int64_t nb, const double* __restrict__ est_sorted, int32_t nw,
+                                    const int32_t* __restrict__ slot_src, double* __restrict__ load,
+                                    int32_t* __restrict__ out_slot) {
   __shared__ double sl[32];
-  __shared__ int si[32], sx[32];
+  __shared__ int sx[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   for (int64_t k = 0; k < nb; ++k) {
     double bl = __longlong_as_double(0x7ff0000000000000ll);
-    int bi = 0x7fffffff, bx = 0x7fffffff;
+    int bx = 0x7fffffff;
     for (int w = tid; w < nw; w += blockDim.x) {
-      const double lw = load[w];
-      if (wins(lw, worker_id[w], w, bl, bi, bx)) {
+      const double lw = load[slot_src[w]];
+      if (lw < bl || (lw == bl && w < bx)) {
         bl = lw;
-        bi = worker_id[w];
         bx = w;
       }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const double ol = __shfl_xor_sync(~0u, bl, o);
-      const int oi = __shfl_xor_sync(~0u, bi, o);
       const int ox = __shfl_xor_sync(~0u, bx, o);
-      if (wins(ol, oi, ox, bl, bi, bx)) {
+      if (ol < bl || (ol == bl && ox < bx)) {
         bl = ol;
-        bi = oi;
         bx = ox;
       }
     }
     if (lane == 0) {
       sl[warp] = bl;
-      si[warp] = bi;
       sx[warp] = bx;
     }
     __syncthreads();
     if (tid == 0) {
       for (int q = 1; q < nwarps; ++q)
-        if (wins(sl[q], si[q], sx[q], sl[0], si[0], sx[0])) {
+        if (sl[q] < sl[0] || (sl[q] == sl[0] && sx[q] < sx[0])) {
           sl[0] = sl[q];
-          si[0] = si[q];
           sx[0] = sx[q];
         }
-      const int32_t cur = order[k];
-      load[sx[0]] = __dadd_rn(load[sx[0]], est[cur]);
-      out_b[k] = batch_id[cur];
-      out_w[k] = si[0];
+      double* lp = &load[slot_src[sx[0]]];
+      *lp = __dadd_rn(*lp, est_sorted[k]);
+      out_slot[k] = sx[0];
     }
     __syncthreads();
   }
@@ -237,12 +260,22 @@ scls_status offload_device(scls_ctx* ctx, int64_t nb, const int64_t* batch_id, c
     if (st) return st;
     order = swapped ? vals2 : vals;
   }
-  if (nw <= 1) greedy_small_kernel<1><<<1, 32, 0, s>>>(nb, order, batch_id, est, nw, worker_id, load, out_batch_id, out_worker);
-  else if (nw <= 2) greedy_small_kernel<2><<<1, 32, 0, s>>>(nb, order, batch_id, est, nw, worker_id, load, out_batch_id, out_worker);
-  else if (nw <= 4) greedy_small_kernel<4><<<1, 32, 0, s>>>(nb, order, batch_id, est, nw, worker_id, load, out_batch_id, out_worker);
-  else if (nw <= 8) greedy_small_kernel<8><<<1, 32, 0, s>>>(nb, order, batch_id, est, nw, worker_id, load, out_batch_id, out_worker);
-  else if (nw <= 32) greedy_warp_kernel<<<1, 32, 0, s>>>(nb, order, batch_id, est, nw, worker_id, load, out_batch_id, out_worker);
-  else greedy_block_kernel<<<1, 256, 0, s>>>(nb, order, batch_id, est, nw, worker_id, load, out_batch_id, out_worker);
+  double* est_sorted = (double*)ctx->buf(kSlotOEst, sizeof(double) * nb);
+  int32_t* slot_src = (int32_t*)ctx->buf(kSlotOSlots, sizeof(int32_t) * 2 * (size_t)nw);
+  if (!est_sorted || !slot_src) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+  int32_t* slot_id = slot_src + nw;
+  slot_order_kernel<<<1, 1, 0, s>>>(nw, worker_id, slot_src, slot_id);
+  SCLS_LAUNCHED();
+  gather_sorted_kernel<<<div_up(nb, 256), 256, 0, s>>>(nb, order, batch_id, est, est_sorted, out_batch_id);
+  SCLS_LAUNCHED();
+  if (nw <= 1) greedy_small_kernel<1><<<1, 64, 0, s>>>(nb, est_sorted, nw, slot_src, load, out_worker);
+  else if (nw <= 2) greedy_small_kernel<2><<<1, 64, 0, s>>>(nb, est_sorted, nw, slot_src, load, out_worker);
+  else if (nw <= 4) greedy_small_kernel<4><<<1, 64, 0, s>>>(nb, est_sorted, nw, slot_src, load, out_worker);
+  else if (nw <= 8) greedy_small_kernel<8><<<1, 64, 0, s>>>(nb, est_sorted, nw, slot_src, load, out_worker);
+  else if (nw <= 32) greedy_warp_kernel<<<1, 32, 0, s>>>(nb, est_sorted, nw, slot_src, load, out_worker);
+  else greedy_block_kernel<<<1, 256, 0, s>>>(nb, est_sorted, nw, slot_src, load, out_worker);
+  SCLS_LAUNCHED();
+  slot_to_worker_kernel<<<div_up(nb, 256), 256, 0, s>>>(nb, slot_id, out_worker);
   SCLS_LAUNCHED();
   return SCLS_OK;
 }

@@ -30,7 +30,7 @@ EXPORTS = [
     "scls_validate_latency", "scls_validate_memory", "scls_validate_sched",
     "scls_batch_serve_time", "scls_would_oom", "scls_max_batch_size",
     "scls_batch_requests", "scls_offload", "scls_schedule", "scls_simulate",
-    "scls_generate", "scls_make_pool",
+    "scls_generate", "scls_make_pool", "scls_debug_dp_profile",
 ]
 
 
@@ -80,6 +80,7 @@ def load():
                                 P(capi.TraceResult), i32, vp, P(capi.EventLog), i32]),
         "scls_generate": (i32, [P(capi.WorkloadSpec), i64, P(i64), vp, vp, vp]),
         "scls_make_pool": (i32, [i64, C.c_uint64, vp, vp, vp, vp]),
+        "scls_debug_dp_profile": (i32, [vp, i32, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -146,6 +147,12 @@ class Context:
         self.lib.scls_last_timings(self.h, out)
         return dict(zip(["total", "sort", "estimate", "dp", "backtrack", "offload", "simulate", "x"],
                         list(out)))
+
+    def dp_profile(self, enable=True):
+        """Read-and-reset the DP kernel's clock64 phase counters."""
+        out = np.zeros(8, np.uint64)
+        self._check(self.lib.scls_debug_dp_profile(self.h, 1 if enable else 0, _ptr(out)))
+        return out
 
     def launches(self):
         return self.lib.scls_last_launch_count(self.h)
