@@ -129,6 +129,11 @@ int64_t scls_last_request_id(const scls_ctx* ctx);
 void scls_last_timings(const scls_ctx* ctx, float out_ms[8]);
 /* Number of CUDA kernel launches issued by the last call. */
 int64_t scls_last_launch_count(const scls_ctx* ctx);
+/* Context options.  SCLS_OPT_SIM_DIGESTS (default 1): scls_simulate fills
+ * the h_* log digests of scls_trace_result; 0 skips them (the metrics are
+ * computed either way, and the digests are zero). */
+enum { SCLS_OPT_SIM_DIGESTS = 1 };
+scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value);
 /* Diagnostics: enable/disable clock64 phase counters in the DP chain kernel
  * and read-and-reset them (cycles: main chain, main barrier wait, helper
  * staging, helper far candidates, helper wait, helper-warp count). */

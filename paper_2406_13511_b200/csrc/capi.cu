@@ -212,6 +212,15 @@ void scls_last_timings(const scls_ctx* ctx, float out_ms[8]) {
 
 int64_t scls_last_launch_count(const scls_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value) {
+  if (!ctx) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null context");
+  if (option == SCLS_OPT_SIM_DIGESTS) {
+    ctx->sim_digests = value != 0;
+    return SCLS_OK;
+  }
+  return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "unknown option");
+}
+
 scls_status scls_debug_dp_profile(scls_ctx* ctx, int32_t enable, uint64_t out[8]) {
   if (!ctx) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null context");
   SCLS_CUDA(cudaSetDevice(ctx->device));

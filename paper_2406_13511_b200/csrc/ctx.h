@@ -23,6 +23,7 @@ struct scls_ctx {
   cudaEvent_t ev[16] = {};
   int sm_count = 148;
   unsigned long long* dp_prof = nullptr;  // device counters when profiling is on
+  bool sim_digests = true;                // scls_simulate computes the log digests
 
   // Named grow-only device buffers (scratch reused across calls).
   struct Buf {

@@ -1,13 +1,1366 @@
-// sim.cu — placeholder until the device simulator lands.
+// sim.cu — the slice-by-slice discrete-event serving simulator on device:
+// reference sim_engine.cpp:26-168 with the SCLS / SLS / ILS policies of
+// sched_policies.cpp:84-391 and the report of metrics.cpp:30-117, batched as
+// ONE TRACE PER WARP across thousands of independent traces.
+//
+// Exactness.  Events are processed in the reference's (time, seq) order:
+// arrivals carry seq 0..n-1, EndOfRun seq n, every later push the next seq
+// (sim_engine.cpp:43-46, 116-120).  Non-arrival events live in per-lane
+// slots (lane w = worker / instance w; at most one pending BatchDone or ILS
+// boundary per worker, sim_engine.h:100-119), the SCLS tick in one uniform
+// slot, SLS's deferred dispatch checks in a FIFO (pushed at the current
+// clock, hence already in (time, seq) order).  Every fp64 expression keeps
+// the reference's association order; sums that the reference accumulates
+// in a fixed order (response sum, ILS iteration time, ct-std) are
+// accumulated in that order.
+//
+// Per-trace state lives in a per-trace arena (sim_layout) in global memory;
+// worker state lives in the lanes' registers (W <= 32).  The SCLS tick runs
+// the scheduling core warp-wide: LSD radix sort of the pool by
+// (eff, arrival-rank == id), the Eq. 10 DP with a per-config cost table, the
+// backtrack, the stable descending estimate order and the max-min offload.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "radix.cuh"
+#include "scls_common.cuh"
+#include "scls_loghash.h"
 #include "sim.cuh"
 
 namespace scls {
-scls_status set_error(scls_ctx* ctx, scls_status st, const std::string& msg);
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kSimWarps = 4;  // traces per CTA
+constexpr int kSplitSmem = 2048;
+
+struct SimCfg {
+  int32_t policy, S, G, B, MC, W;
+  double lambda, gamma, horizon;
+  int32_t table;  // cost-table index (SCLS), -1 otherwise
+};
+
+struct SimParams {
+  int32_t n_traces;
+  const int64_t* req_off;
+  const double* arr;
+  const int32_t* inp;
+  const int32_t* tg;
+  const SimCfg* cfgs;
+  const int32_t* cfg_index;
+  const uint8_t* cfg_ok;
+  Lat lat;
+  int32_t Lmax;
+  const int32_t* Kt;    // [table][L]
+  const int32_t* coff;  // [table][L] -> offset of c(L, 1) in cost
+  const double* cost;
+  char* arena;
+  const int64_t* trace_base;
+  const int64_t* trace_cap;
+  scls_trace_result* res;
+  int32_t hist_bins;
+  int64_t* hist;
+  scls_event_record* recs;
+  scls_member* mems;
+  int64_t rec_cap, mem_cap;
+  int64_t* rec_count;
+  int64_t* mem_count;
+  int32_t n_logged;
+};
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000ll); }
+
+__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(FULL, v, src); }
+__device__ __forceinline__ int shfl_i(int v, int src) { return __shfl_sync(FULL, v, src); }
+__device__ __forceinline__ long long shfl_l(long long v, int src) { return __shfl_sync(FULL, v, src); }
+
+// ---- event-log sink: counters always, digests / records on demand ------------------
+
+template <bool kHash, bool kLog>
+struct Sink {
+  uint64_t hc, hd, ht, hl;
+  int64_t n_events, n_disp, n_ticks;
+  scls_event_record* rec;
+  scls_member* mem;
+  int64_t rec_cap, mem_cap, rec_n, mem_n;
+
+  __device__ void init(scls_event_record* r, scls_member* m, int64_t rc, int64_t mc) {
+    hc = hd = ht = hl = SCLS_FNV_OFFSET;
+    n_events = n_disp = n_ticks = 0;
+    rec = r;
+    mem = m;
+    rec_cap = rc;
+    mem_cap = mc;
+    rec_n = mem_n = 0;
+  }
+  // Uniform call (all lanes, same arguments); lane 0 writes the record.
+  __device__ void record(int lane, int32_t kind, double t, int64_t request, int32_t worker,
+                         int64_t batch, int32_t n, int32_t l_in, int32_t planned, int32_t served,
+                         double est, int32_t input_len, int32_t gen_len, double response,
+                         int32_t slices, double next_interval, int32_t members) {
+    ++n_events;
+    if (kind == 2) ++n_disp;
+    if (kind == 1) ++n_ticks;
+    if (kHash) {
+      hl = scls_hash_record(hl, kind, t, request, worker, batch, n, l_in, planned, served, est,
+                            input_len, gen_len, response, slices, next_interval, members);
+      if (kind == 5) {
+        hc = scls_fnv_bytes(hc, (uint64_t)request);
+        ht = scls_fnv_bytes(ht, scls_dbits(t));
+      } else if (kind == 2) {
+        hd = scls_fnv_bytes(hd, (uint64_t)batch);
+        hd = scls_fnv_bytes(hd, (uint64_t)(int64_t)worker);
+        hd = scls_fnv_bytes(hd, (uint64_t)(int64_t)n);
+        hd = scls_fnv_bytes(hd, (uint64_t)(int64_t)l_in);
+      }
+    }
+    if (kLog) {
+      if (lane == 0 && rec_n < rec_cap) {
+        scls_event_record& o = rec[rec_n];
+        o.t = t;
+        o.est_serve_s = est;
+        o.response_s = response;
+        o.next_interval_s = next_interval;
+        o.request = request;
+        o.batch = batch;
+        o.kind = kind;
+        o.worker = worker;
+        o.n = n;
+        o.l_in = l_in;
+        o.planned_l_out = planned;
+        o.served_l_out = served;
+        o.input_len = input_len;
+        o.gen_len = gen_len;
+        o.slices = slices;
+        o.member_count = members;
+        o.member_offset = mem_n;
+      }
+      ++rec_n;
+    }
+  }
+  // Members of the last batch_end record: one chunk of up to 32 lanes.
+  __device__ void members(int lane, int cnt, int64_t request, int32_t eff, int32_t pad,
+                          int32_t gen, int32_t inv) {
+    if (kHash) {
+      for (int i = 0; i < cnt; ++i) {
+        hl = scls_hash_member(hl, shfl_l(request, i), shfl_i(eff, i), shfl_i(pad, i),
+                              shfl_i(gen, i), shfl_i(inv, i));
+      }
+    }
+    if (kLog) {
+      if (lane < cnt && mem_n + lane < mem_cap)
+        mem[mem_n + lane] = scls_member{request, eff, pad, gen, inv};
+      mem_n += cnt;
+    }
+  }
+};
+
+// ---- warp helpers -------------------------------------------------------------
+
+// (t, seq) lexicographic min over lanes [0, 2^rounds); returns the winning lane.
+__device__ __forceinline__ int argmin_event(double t, unsigned long long s, int lane, int rounds,
+                                            double* bt, unsigned long long* bs) {
+  int bl = lane;
+  for (int r = 0; r < rounds; ++r) {
+    const int o = 1 << r;
+    const double ot = __shfl_xor_sync(FULL, t, o);
+    const unsigned long long os = __shfl_xor_sync(FULL, s, o);
+    const int ol = __shfl_xor_sync(FULL, bl, o);
+    if (ot < t || (ot == t && os < s)) {
+      t = ot;
+      s = os;
+      bl = ol;
+    }
+  }
+  *bt = shfl_d(t, 0);
+  *bs = __shfl_sync(FULL, s, 0);
+  return shfl_i(bl, 0);
 }
 
-extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t, const int64_t*, const double*, const int32_t*,
-                                     const int32_t*, int32_t, const scls_sched_cfg*, const int32_t*,
-                                     const scls_latency*, const scls_memory*, scls_trace_result*, int32_t,
-                                     int64_t*, scls_event_log*, int32_t) {
-  return scls::set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "scls_simulate: not built yet");
+// Stable LSD radix sort of n (key, val) pairs on key bits [0, bits), warp-wide,
+// ping-ponging between (k, v) and (k2, v2).  Returns true when the result is
+// in (k2, v2).  bins: 256 ints of this warp's shared memory.
+__device__ bool warp_radix_sort(int n, uint64_t* k, int32_t* v, uint64_t* k2, int32_t* v2, int bits,
+                                int lane, int32_t* bins) {
+  bool swapped = false;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int shift = 0; shift < bits; shift += 8) {
+    const uint32_t mask = bits - shift >= 8 ? 0xffu : ((1u << (bits - shift)) - 1u);
+    for (int i = lane; i < 256; i += 32) bins[i] = 0;
+    __syncwarp();
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      if (i < n) atomicAdd(&bins[(k[i] >> shift) & mask], 1);
+    }
+    __syncwarp();
+    {  // exclusive scan of 256 bins: 8 per lane
+      int loc[8], s = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        loc[q] = bins[lane * 8 + q];
+        s += loc[q];
+      }
+      int incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int run = incl - s;
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        bins[lane * 8 + q] = run;
+        run += loc[q];
+      }
+    }
+    __syncwarp();
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const bool ok = i < n;
+      const uint64_t key = ok ? k[i] : 0;
+      const int32_t val = (ok && v) ? v[i] : 0;
+      const int d = ok ? (int)((key >> shift) & mask) : 256 + lane;
+      const unsigned peers = __match_any_sync(FULL, d);
+      const int prior = ok ? bins[d] : 0;
+      const int dst = prior + __popc(peers & lt);
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) bins[d] = prior + __popc(peers);
+      if (ok) {
+        k2[dst] = key;
+        if (v) v2[dst] = val;
+      }
+      __syncwarp();
+    }
+    uint64_t* tk = k;
+    k = k2;
+    k2 = tk;
+    int32_t* tv = v;
+    v = v2;
+    v2 = tv;
+    swapped = !swapped;
+    __syncwarp();
+  }
+  return swapped;
+}
+
+__device__ __forceinline__ int bits_of(uint32_t x) { return x ? 32 - __clz(x) : 0; }
+
+// ---- the per-trace simulation -------------------------------------------------------
+
+template <bool kHash, bool kLog>
+__device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, int32_t* ssplit) {
+  const int64_t r0 = P.req_off[t];
+  const int n = (int)(P.req_off[t + 1] - r0);
+  const double* __restrict__ arr = P.arr + r0;
+  const int32_t* __restrict__ inp = P.inp + r0;
+  const int32_t* __restrict__ tg = P.tg + r0;
+  const int ci = P.cfg_index ? P.cfg_index[t] : 0;
+  const SimCfg C = P.cfgs[ci];
+  scls_trace_result* R = &P.res[t];
+  int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
+  const int W = C.W;
+  const bool logging = kLog && t < P.n_logged;
+
+  // Constructor validation (host-checked per config) and the arrival-order
+  // rule (sim_engine.cpp:102-114).
+  int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
+  if (status == SCLS_OK) {
+    int bad = 0;
+    for (int i = 1 + lane; i < n; i += 32) bad |= arr[i] < arr[i - 1];
+    if (__any_sync(FULL, bad)) status = SCLS_ERR_ERROR;
+  }
+  if (hist)
+    for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
+  if (status != SCLS_OK) {
+    if (lane == 0) {
+      memset(R, 0, sizeof *R);
+      R->status = status;
+      R->worker_count = W;
+      R->error_request_id = -1;
+      R->n_requests = n;
+    }
+    return;
+  }
+
+  char* base = P.arena + P.trace_base[t];
+  const SimLayout Lay = sim_layout(n, W, C.policy, P.trace_cap[t], C.MC);
+  int32_t* gen = (int32_t*)(base + Lay.gen);
+  int32_t* sl = (int32_t*)(base + Lay.sl);
+  double* resp = (double*)(base + Lay.resp);
+  for (int i = lane; i < n; i += 32) {
+    gen[i] = 0;
+    sl[i] = 0;
+  }
+
+  Sink<kHash, kLog> sink;
+  sink.init(logging ? P.recs + (int64_t)t * P.rec_cap : nullptr,
+            logging ? P.mems + (int64_t)t * P.mem_cap : nullptr, logging ? P.rec_cap : 0,
+            logging ? P.mem_cap : 0);
+
+  // Worker / instance registers (lane w < W).
+  double ev_t = dinf();            // pending BatchDone / ILS boundary
+  unsigned long long ev_s = ~0ull;
+  double load = 0.0, last_end = 0.0;
+  int busy = 0, infl = -1, q_head = -1, q_tail = -1;
+  int f_head = 0, f_tail = 0;      // SLS pending / ILS waiting FIFO
+  int inf_start = 0, inf_n = 0, inf_lin = 0, inf_lout = 0;  // SLS in-flight batch
+  long long inf_id = 0;
+  int n_run = 0, boundary = 0, seg_n = 0, seg_lin = 0, seg_it = 0;  // ILS
+  long long seg_id = -1;
+
+  // Trace-wide uniform state.
+  const int rounds = W <= 1 ? 0 : bits_of((uint32_t)(W - 1));
+  unsigned long long next_seq = (unsigned long long)n + 1;  // arrivals 0..n-1, EndOfRun n
+  double clock = 0.0;
+  int cur = 0, completed = 0;
+  long long next_batch = 0, rr = 0;
+  double first_arrival = dinf(), last_completion = -dinf();
+  long long total_pad = 0, total_inv = 0, batch_count = 0, batch_members = 0, early = 0;
+  double tick_t = dinf();
+  unsigned long long tick_s = ~0ull;
+  int pool_len = 0, tl_pos = 0;
+  int pf_head = 0, pf_tail = 0;  // SLS policy FIFO
+  int err_req = -1;
+  status = SCLS_OK;
+
+  // Policy-specific arena views.
+  int32_t* pool = (int32_t*)(base + Lay.pool);
+  uint64_t* sk = (uint64_t*)(base + Lay.sk);
+  uint64_t* sk2 = (uint64_t*)(base + Lay.sk2);
+  int32_t* sv = (int32_t*)(base + Lay.sv);
+  double* Tg = (double*)(base + Lay.T);
+  int32_t* split_g = (int32_t*)(base + Lay.split);
+  int32_t* segs = (int32_t*)(base + Lay.segs);
+  int32_t* tlog = (int32_t*)(base + Lay.tlog);
+  int32_t* b_start = (int32_t*)(base + Lay.b_start);
+  int32_t* b_n = (int32_t*)(base + Lay.b_n);
+  int32_t* b_lin = (int32_t*)(base + Lay.b_lin);
+  int32_t* b_served = (int32_t*)(base + Lay.b_served);
+  int32_t* b_next = (int32_t*)(base + Lay.b_next);
+  double* b_est = (double*)(base + Lay.b_est);
+  const int cap_w = W > 0 ? (n + W - 1) / W : 0;
+  int32_t* fifo = (int32_t*)(base + Lay.fifo) + (lane < W ? lane : 0) * (int64_t)cap_w;
+  int32_t* fifo_base = (int32_t*)(base + Lay.fifo);
+  double* pf_t = (double*)(base + Lay.pf_t);
+  unsigned long long* pf_seq = (unsigned long long*)(base + Lay.pf_seq);
+  int32_t* pf_w = (int32_t*)(base + Lay.pf_w);
+  int32_t* run_base = (int32_t*)(base + Lay.run);
+  int32_t* ex_base = (int32_t*)(base + Lay.ex);
+  const int32_t* Kt = C.table >= 0 ? P.Kt + (int64_t)C.table * (P.Lmax + 1) : nullptr;
+  const int32_t* coff = C.table >= 0 ? P.coff + (int64_t)C.table * (P.Lmax + 1) : nullptr;
+  const double* cost = P.cost;
+  const Lat lat = P.lat;
+
+  if (C.policy == SCLS_POLICY_SCLS) {  // sched_policies.cpp:84: first tick at 0
+    tick_t = 0.0;
+    tick_s = next_seq++;
+  }
+
+  // ---- shared event handlers -------------------------------------------------------
+
+  // sim_engine.cpp:86-99 complete_request for a chunk of `cnt` ids in lane order.
+  auto complete_chunk = [&](int cnt, int id, int worker) {
+    if (lane < cnt) {
+      resp[completed + lane] = clock - arr[id];
+      const int s = sl[id];
+      if (hist && s >= 0 && s < P.hist_bins) atomicAdd((unsigned long long*)&hist[s], 1ull);
+    }
+    for (int i = 0; i < cnt; ++i) {
+      const int rid = shfl_i(id, i);
+      const int s = shfl_i(lane < cnt ? sl[id] : 0, i);
+      sink.record(lane, 5, clock, rid, worker, -1, 0, 0, 0, 0, 0.0, 0, 0, clock - arr[rid], s, 0.0, 0);
+    }
+    completed += cnt;
+    if (cnt > 0) last_completion = clock;
+  };
+
+  // sim_engine.cpp:63-84 start_next_batch (SCLS: batches queued per worker).
+  auto start_next_scls = [&](int w) {
+    const int b = shfl_i(busy, w) ? -1 : shfl_i(q_head, w);
+    if (b < 0) return;
+    const int nb_next = b_next[b];
+    if (lane == w) {
+      q_head = nb_next;
+      if (q_head < 0) q_tail = -1;
+    }
+    const int bn = b_n[b], blin = b_lin[b], bsv = b_served[b];
+    sink.record(lane, 3, clock, -1, w, b, bn, blin, 0, 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
+    const double serve = batch_serve_time(lat, bn, blin, bsv);
+    if (lane == w) {
+      busy = 1;
+      infl = b;
+      ev_t = __dadd_rn(clock, serve);
+      ev_s = next_seq;
+    }
+    ++next_seq;
+  };
+
+  // SLS try_dispatch (sched_policies.cpp:207-243): FCFS batch of <= B from
+  // the worker's FIFO; starts at once (the worker is idle, queue empty).
+  auto sls_try_dispatch = [&](int w) {
+    const int bz = shfl_i(busy, w);
+    const int head = shfl_i(f_head, w), tail = shfl_i(f_tail, w);
+    if (bz || tail == head) return;
+    const int take = min(C.B, tail - head);
+    const int32_t* q = fifo_base + (int64_t)w * cap_w;
+    int lin = 0, lout = 0;
+    for (int b0 = 0; b0 < take; b0 += 32) {
+      const int i = b0 + lane;
+      if (i < take) {
+        const int id = q[head + i];
+        lin = max(lin, inp[id]);
+        lout = max(lout, min(tg[id], C.G));
+      }
+    }
+    lin = __reduce_max_sync(FULL, lin);
+    lout = __reduce_max_sync(FULL, lout);
+    const long long bid = next_batch++;
+    const double est = batch_serve_time(lat, take, lin, lout);
+    sink.record(lane, 2, clock, -1, w, bid, take, lin, lout, 0, est, 0, 0, 0.0, 0, 0.0, 0);
+    sink.record(lane, 3, clock, -1, w, bid, take, lin, 0, 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
+    if (lane == w) {
+      f_head = head + take;
+      busy = 1;
+      inf_start = head;
+      inf_n = take;
+      inf_lin = lin;
+      inf_lout = lout;
+      inf_id = bid;
+      ev_t = __dadd_rn(clock, est);  // serve time == est (served l_out == planned)
+      ev_s = next_seq;
+    }
+    ++next_seq;
+  };
+
+  // ---- the SCLS tick (sched_policies.cpp:90-147) ------------------------------------
+  auto scls_tick = [&]() -> int {
+    int nb = 0;
+    const int P_ = pool_len;
+    if (P_ > 0) {
+      // 1. order the pool by (eff, id); ids are arrival ranks (sim_engine.cpp:110-114)
+      const int idb = bits_of((uint32_t)max(n - 1, 1));
+      uint32_t emax = 0;
+      for (int i = lane; i < P_; i += 32) {
+        const int id = pool[i];
+        const uint32_t e = (uint32_t)(inp[id] + gen[id]);
+        emax = max(emax, e);
+        sk[i] = ((uint64_t)e << idb) | (uint64_t)id;
+      }
+      emax = __reduce_max_sync(FULL, emax);
+      __syncwarp();
+      const bool sw = warp_radix_sort(P_, sk, nullptr, sk2, nullptr, idb + bits_of(emax), lane, bins);
+      const uint64_t* keys = sw ? sk2 : sk;
+      const uint64_t idmask = (1ull << idb) - 1ull;
+      // 2. rows: L, singleton feasibility (batcher.cpp:40-46)
+      int bad = 0x7fffffff;
+      for (int i = lane; i < P_; i += 32) {
+        const uint64_t key = keys[i];
+        const int id = (int)(key & idmask);
+        const int L = (int)(key >> idb);
+        tlog[tl_pos + i] = id;
+        sv[i] = L;
+        if (L > P.Lmax || Kt[L] == 0) bad = min(bad, i);
+      }
+      bad = __reduce_min_sync(FULL, bad);
+      __syncwarp();
+      if (bad != 0x7fffffff) {
+        err_req = tlog[tl_pos + bad];
+        return SCLS_ERR_INFEASIBLE_REQUEST;
+      }
+      // 3. the DP (batcher.cpp:48-67): tiles of 32 rows, far+mid then the chain
+      int32_t* split = P_ <= kSplitSmem ? ssplit : split_g;
+      if (lane == 0) {
+        Tg[0] = 0.0;
+        split[0] = 0;
+      }
+      __syncwarp();
+      const double kInf = dinf();
+      for (int tb = 0; tb < P_; tb += 32) {
+        const int r = tb + 1 + lane;
+        const bool valid = r <= P_;
+        const int L = valid ? sv[r - 1] : 0;
+        const int Wr = valid ? min(Kt[L], r) : 0;
+        const int cb = valid ? coff[L] - 1 : 0;
+        double acc = kInf;
+        int kb = 0;
+        const int wmax = __reduce_max_sync(FULL, Wr);
+        // candidates with j <= tb, ascending j (k descending)
+        for (int j = max(0, tb + 1 - wmax); j <= tb; ++j) {
+          const double Tj = Tg[j];
+          const int k = r - j;
+          if (k <= Wr) {
+            const double cand = __dadd_rn(Tj, cost[cb + k]);
+            if (cand <= acc) {
+              acc = cand;
+              kb = k;
+            }
+          }
+        }
+        // the in-tile chain
+        double Tj = Tg[tb];
+        const int rows = min(32, P_ - tb);
+        for (int s = 1; s <= rows; ++s) {
+          // row tb+s finalises at step s-1 (lane s-1) after T[tb+s-1] arrives
+          const int k = r - (tb + s - 1);
+          if (s - 1 > 0 && k >= 1 && k <= Wr) {
+            const double cand = __dadd_rn(Tj, cost[cb + k]);
+            if (cand <= acc) {
+              acc = cand;
+              kb = k;
+            }
+          }
+          Tj = shfl_d(acc, s - 1);
+        }
+        if (valid) {
+          Tg[r] = acc;
+          split[r] = r - kb;
+        }
+        __syncwarp();
+      }
+      // 4. backtrack (batcher.cpp:69-73): segment ends, reversed
+      int cnt = 0;
+      for (int i = P_; i > 0; i = split[i]) {
+        if (lane == 0) segs[cnt] = i;
+        ++cnt;
+      }
+      __syncwarp();
+      nb = cnt;
+      // 5. emit batches in ascending segment order (batcher.cpp:75-86)
+      for (int b0 = 0; b0 < nb; b0 += 32) {
+        const int b = b0 + lane;
+        if (b < nb) {
+          const int end = segs[nb - 1 - b];
+          const int beg = b == 0 ? 0 : segs[nb - b];
+          const int bi = (int)next_batch + b;
+          const int L = sv[end - 1];
+          b_start[bi] = tl_pos + beg;
+          b_n[bi] = end - beg;
+          b_lin[bi] = L;
+          b_est[bi] = cost[coff[L] - 1 + (end - beg)];
+        }
+      }
+      tl_pos += P_;
+      pool_len = 0;
+      __syncwarp();
+    }
+    const int first = (int)next_batch;
+    next_batch += nb;
+    // 6. offload (offloader.cpp:25-54): stable est-descending order, then the
+    //    greedy min-(load, worker) placement against the lane loads.
+    int32_t* order = segs;  // reuse
+    if (nb > 0) {
+      if (nb <= 32) {
+        const double e = lane < nb ? b_est[first + lane] : -dinf();
+        int rank = 0;
+        for (int q = 0; q < nb; ++q) {
+          const double eq = shfl_d(e, q);
+          rank += (eq > e) || (eq == e && q < lane);
+        }
+        if (lane < nb) order[rank] = lane;
+      } else {
+        for (int i = lane; i < nb; i += 32) {
+          sk[i] = ~ordered_bits(b_est[first + i]);
+          sv[i] = i;
+        }
+        __syncwarp();
+        const bool sw = warp_radix_sort(nb, sk, sv, sk2, (int32_t*)Tg, 64, lane, bins);
+        const int32_t* ord = sw ? (const int32_t*)Tg : sv;
+        for (int i = lane; i < nb; i += 32) order[i] = ord[i];
+      }
+      __syncwarp();
+    }
+    for (int k = 0; k < nb; ++k) {
+      const int b = first + order[k];
+      const double e = b_est[b];
+      double bt;
+      unsigned long long bs;
+      const int w = argmin_event(lane < W ? load : dinf(), (unsigned long long)lane, lane, rounds, &bt, &bs);
+      if (lane == w) load = __dadd_rn(load, e);
+      // dispatch record, slice_served_l_out (sched_policies.cpp:72-80), enqueue
+      const int bn = b_n[b], bst = b_start[b];
+      int served = 0;
+      for (int i = lane; i < bn; i += 32) {
+        const int id = tlog[bst + i];
+        served = max(served, min(tg[id] - gen[id], C.S));
+      }
+      served = __reduce_max_sync(FULL, served);
+      sink.record(lane, 2, clock, -1, w, b, bn, b_lin[b], C.S, 0, e, 0, 0, 0.0, 0, 0.0, 0);
+      if (lane == 0) {
+        b_served[b] = served;
+        b_next[b] = -1;
+      }
+      const int tail = shfl_i(q_tail, w);
+      if (lane == 0 && tail >= 0) b_next[tail] = b;
+      if (lane == w) {
+        if (q_tail < 0) q_head = b;
+        q_tail = b;
+      }
+      __syncwarp();
+      start_next_scls(w);
+    }
+    // sched_policies.cpp:134-146: adaptive interval from the post-offload loads
+    double ml = lane < W ? load : dinf();
+    for (int o = 16; o; o >>= 1) ml = fmin(ml, __shfl_xor_sync(FULL, ml, o));
+    const double a = __dmul_rn(C.lambda, ml);
+    const double interval = a < C.gamma ? C.gamma : a;
+    sink.record(lane, 1, clock, -1, -1, -1, nb, 0, 0, 0, 0.0, 0, 0, 0.0, 0, interval, 0);
+    tick_t = __dadd_rn(clock, interval);
+    tick_s = next_seq++;
+    return SCLS_OK;
+  };
+
+  // SCLS on_batch_done (sched_policies.cpp:149-188) for worker w, batch b.
+  auto scls_done = [&](int w, int b) {
+    const int bn = b_n[b], bst = b_start[b], lin = b_lin[b], served = b_served[b];
+    sink.record(lane, 4, clock, -1, w, b, bn, lin, C.S, served, 0.0, 0, 0, 0.0, 0, 0.0, bn);
+    ++batch_count;
+    batch_members += bn;
+    early += served < C.S;
+    const unsigned lt = (1u << lane) - 1u;
+    int nfin = 0;
+    int32_t* fin = sv;  // finished ids, member order (reused scratch)
+    for (int b0 = 0; b0 < bn; b0 += 32) {
+      const int i = b0 + lane;
+      const bool ok = i < bn;
+      int id = 0, eff = 0, g = 0, pad = 0, inv = 0;
+      bool done = false;
+      if (ok) {
+        id = tlog[bst + i];
+        const int gsf = gen[id];
+        eff = inp[id] + gsf;
+        g = min(tg[id] - gsf, served);
+        pad = lin - eff;
+        inv = served - g;
+        const int ng = gsf + g;
+        gen[id] = ng;
+        sl[id] += 1;
+        done = ng >= tg[id] || ng >= C.G;
+      }
+      const int cnt = min(32, bn - b0);
+      sink.members(lane, cnt, id, eff, pad, g, inv);
+      total_pad += __reduce_add_sync(FULL, ok ? pad : 0);
+      total_inv += __reduce_add_sync(FULL, ok ? inv : 0);
+      const unsigned fm = __ballot_sync(FULL, ok && done);
+      const unsigned pm = __ballot_sync(FULL, ok && !done);
+      if (ok && done) fin[nfin + __popc(fm & lt)] = id;
+      if (ok && !done) pool[pool_len + __popc(pm & lt)] = id;
+      nfin += __popc(fm);
+      pool_len += __popc(pm);
+    }
+    __syncwarp();
+    for (int c0 = 0; c0 < nfin; c0 += 32) {
+      const int cnt = min(32, nfin - c0);
+      const int id = lane < cnt ? fin[c0 + lane] : 0;
+      complete_chunk(cnt, id, w);
+    }
+    if (lane == w) {
+      last_end = fmax(last_end, clock);
+      load = load - b_est[b];  // offloader.cpp:56-59 complete_batch
+      if (load < 0.0) load = 0.0;
+    }
+  };
+
+  // SLS on_batch_done (sched_policies.cpp:245-273).
+  auto sls_done = [&](int w) {
+    const int start = shfl_i(inf_start, w), bn = shfl_i(inf_n, w), lin = shfl_i(inf_lin, w),
+              lout = shfl_i(inf_lout, w);
+    const long long bid = shfl_l(inf_id, w);
+    sink.record(lane, 4, clock, -1, w, bid, bn, lin, lout, lout, 0.0, 0, 0, 0.0, 0, 0.0, bn);
+    ++batch_count;
+    batch_members += bn;
+    const int32_t* q = fifo_base + (int64_t)w * cap_w;
+    for (int b0 = 0; b0 < bn; b0 += 32) {
+      const int i = b0 + lane;
+      const bool ok = i < bn;
+      int id = 0, g = 0, pad = 0, inv = 0, orig = 0;
+      if (ok) {
+        id = q[start + i];
+        orig = inp[id];
+        g = min(tg[id], C.G);
+        pad = lin - orig;
+        inv = lout - g;
+        gen[id] = g;
+        sl[id] = 1;
+      }
+      const int cnt = min(32, bn - b0);
+      sink.members(lane, cnt, id, orig, pad, g, inv);
+      total_pad += __reduce_add_sync(FULL, ok ? pad : 0);
+      total_inv += __reduce_add_sync(FULL, ok ? inv : 0);
+    }
+    __syncwarp();
+    for (int c0 = 0; c0 < bn; c0 += 32) {
+      const int cnt = min(32, bn - c0);
+      const int id = lane < cnt ? q[start + c0 + lane] : 0;
+      complete_chunk(cnt, id, w);
+    }
+    if (lane == w) {
+      last_end = fmax(last_end, clock);
+      busy = 0;
+    }
+    sls_try_dispatch(w);
+  };
+
+  // ILS iteration boundary (sched_policies.cpp:292-391) for instance w.
+  auto ils_event = [&](int w) {
+    const unsigned lt = (1u << lane) - 1u;
+    const double now = clock;
+    int32_t* run = run_base + (int64_t)w * C.MC;
+    const int32_t* wq = fifo_base + (int64_t)w * cap_w;
+    int nr = shfl_i(n_run, w);
+    int nexit = 0, keep = 0;
+    int32_t* exit_ids = ex_base;  // exits in member order (<= max_concurrent)
+    if (nr > 0) {
+      if (lane == w) seg_it += 1;
+      for (int b0 = 0; b0 < nr; b0 += 32) {
+        const int i = b0 + lane;
+        const bool ok = i < nr;
+        int id = 0;
+        bool ex = false;
+        if (ok) {
+          id = run[i];
+          const int g = gen[id] + 1;
+          gen[id] = g;
+          ex = g >= tg[id] || g >= C.G;
+        }
+        const unsigned em = __ballot_sync(FULL, ok && ex);
+        const unsigned km = __ballot_sync(FULL, ok && !ex);
+        __syncwarp();
+        if (ok && ex) exit_ids[nexit + __popc(em & lt)] = id;
+        if (ok && !ex) run[keep + __popc(km & lt)] = id;
+        nexit += __popc(em);
+        keep += __popc(km);
+        __syncwarp();
+      }
+      nr = keep;
+    }
+    // Joins: FCFS from the waiting FIFO up to max_concurrent.
+    const int head = shfl_i(f_head, w), tail = shfl_i(f_tail, w);
+    const int njoin = min(C.MC - nr, tail - head);
+    for (int i = lane; i < njoin; i += 32) run[nr + i] = wq[head + i];
+    __syncwarp();
+    const int nr_new = nr + njoin;
+    if (lane == w) {
+      f_head = head + njoin;
+      n_run = nr_new;
+    }
+    const bool changed = nexit > 0 || njoin > 0;
+    const long long sid = shfl_l(seg_id, w);
+    const int sit = shfl_i(seg_it, w);
+    if (changed && sid >= 0 && sit > 0) {
+      const int sn = shfl_i(seg_n, w), slin = shfl_i(seg_lin, w);
+      sink.record(lane, 4, now, -1, w, sid, sn, slin, sit, sit, 0.0, 0, 0, 0.0, 0, 0.0, 0);
+      ++batch_count;
+      batch_members += sn;
+      if (lane == w) {
+        seg_id = -1;
+        last_end = fmax(last_end, now);
+      }
+    }
+    for (int c0 = 0; c0 < nexit; c0 += 32) {
+      const int cnt = min(32, nexit - c0);
+      const int id = lane < cnt ? exit_ids[c0 + lane] : 0;
+      __syncwarp();
+      complete_chunk(cnt, id, w);
+    }
+    if (nr_new == 0) {
+      if (lane == w) boundary = 0;
+      return;
+    }
+    int mctx = 0;
+    for (int i = lane; i < nr_new; i += 32) {
+      const int id = run[i];
+      mctx = max(mctx, inp[id] + gen[id]);
+    }
+    mctx = __reduce_max_sync(FULL, mctx);
+    long long cur_seg = shfl_l(seg_id, w);
+    if (changed) {
+      cur_seg = next_batch++;
+      if (lane == w) {
+        seg_id = cur_seg;
+        seg_n = nr_new;
+        seg_lin = mctx;
+        seg_it = 0;
+      }
+      sink.record(lane, 3, now, -1, w, cur_seg, nr_new, mctx, 0, 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
+    }
+    double it = decode_step_time(lat, mctx, nr_new);
+    for (int j = 0; j < njoin; ++j) {
+      const int id = run[nr + j];
+      if (lane == 0) sl[id] = 1;
+      it = __dadd_rn(it, prefill_time(lat, 1, inp[id]));
+      // planned_l_out = remaining_gen() (sched_policies.cpp:384)
+      sink.record(lane, 2, now, id, w, cur_seg, 1, inp[id], tg[id] - gen[id], 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
+    }
+    if (lane == w) {
+      ev_t = __dadd_rn(now, it);
+      ev_s = next_seq;
+      boundary = 1;
+    }
+    ++next_seq;
+  };
+
+  // ---- the event loop (sim_engine.cpp:123-166) ------------------------------------
+  bool dirty = true;
+  double na_t = dinf();
+  unsigned long long na_s = ~0ull;
+  int na_w = -1;  // -1: tick / FIFO head, >= 0: lane slot
+  while (completed < n) {
+    if (dirty) {
+      double bt;
+      unsigned long long bs;
+      const int bw = argmin_event(lane < W ? ev_t : dinf(), lane < W ? ev_s : ~0ull, lane, rounds, &bt, &bs);
+      na_t = bt;
+      na_s = bs;
+      na_w = bw;
+      if (C.policy == SCLS_POLICY_SCLS) {
+        if (tick_t < na_t || (tick_t == na_t && tick_s < na_s)) {
+          na_t = tick_t;
+          na_s = tick_s;
+          na_w = -1;
+        }
+      } else if (C.policy == SCLS_POLICY_SLS && pf_head < pf_tail) {
+        const double ft = pf_t[pf_head];
+        const unsigned long long fs = pf_seq[pf_head];
+        if (ft < na_t || (ft == na_t && fs < na_s)) {
+          na_t = ft;
+          na_s = fs;
+          na_w = -1;
+        }
+      }
+      dirty = false;
+    }
+    const double bound = fmin(na_t, C.horizon);
+    if (cur < n && arr[cur] <= bound) {
+      // Arrival(s): seq < n, so they precede any non-arrival event at the same time.
+      if (C.policy == SCLS_POLICY_SCLS) {
+        // SCLS arrivals only append to the pool: take every arrival <= bound.
+        int cnt = 0;
+        for (;;) {
+          const int i = cur + cnt + lane;
+          const bool ok = i < n && arr[i] <= bound;
+          const unsigned m = __ballot_sync(FULL, ok);
+          const int run = (~m) ? __ffs(~m) - 1 : 32;
+          cnt += run;
+          if (run < 32) break;
+        }
+        if (first_arrival == dinf()) first_arrival = arr[cur];
+        for (int c0 = 0; c0 < cnt; c0 += 32) {
+          const int i = cur + c0 + lane;
+          if (c0 + lane < cnt) pool[pool_len + c0 + lane] = i;
+        }
+        if (kHash || kLog) {
+          for (int i = 0; i < cnt; ++i) {
+            const int id = cur + i;
+            sink.record(lane, 0, arr[id], id, -1, -1, 0, 0, 0, 0, 0.0, inp[id], tg[id], 0.0, 0, 0.0, 0);
+          }
+        } else {
+          sink.n_events += cnt;
+        }
+        clock = arr[cur + cnt - 1];
+        pool_len += cnt;
+        cur += cnt;
+        __syncwarp();
+        continue;
+      }
+      const int id = cur++;
+      clock = arr[id];
+      if (first_arrival == dinf()) first_arrival = clock;
+      sink.record(lane, 0, clock, id, -1, -1, 0, 0, 0, 0, 0.0, inp[id], tg[id], 0.0, 0, 0.0, 0);
+      const int w = (int)(rr++ % W);
+      if (C.policy == SCLS_POLICY_SLS) {  // sched_policies.cpp:194-201
+        if (lane == w) fifo[f_tail++] = id;
+        if (lane == 0) {
+          pf_t[pf_tail] = clock;
+          pf_seq[pf_tail] = next_seq;
+          pf_w[pf_tail] = w;
+        }
+        ++pf_tail;
+        ++next_seq;
+        dirty = dirty || pf_tail - pf_head == 1;
+      } else {  // ILS, sched_policies.cpp:279-290
+        if (lane == w) fifo[f_tail++] = id;
+        const int wake = shfl_i(n_run == 0 && !boundary, w);
+        if (wake) {
+          if (lane == w) {
+            ev_t = clock;
+            ev_s = next_seq;
+            boundary = 1;
+          }
+          ++next_seq;
+          dirty = true;
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    if (C.horizon <= na_t) {  // EndOfRun (horizon, n) precedes (na_t, na_s > n)
+      status = SCLS_ERR_NON_TERMINATION;
+      break;
+    }
+    clock = na_t;
+    dirty = true;
+    if (na_w < 0) {
+      if (C.policy == SCLS_POLICY_SCLS) {
+        tick_t = dinf();
+        tick_s = ~0ull;
+        status = scls_tick();
+        if (status != SCLS_OK) break;
+      } else {  // SLS deferred dispatch check
+        const int w = pf_w[pf_head];
+        ++pf_head;
+        sls_try_dispatch(w);
+      }
+    } else {
+      const int w = na_w;
+      if (lane == w) {
+        ev_t = dinf();
+        ev_s = ~0ull;
+      }
+      if (C.policy == SCLS_POLICY_SCLS) {
+        const int b = shfl_i(infl, w);
+        if (lane == w) {
+          busy = 0;
+          infl = -1;
+        }
+        scls_done(w, b);
+        start_next_scls(w);
+      } else if (C.policy == SCLS_POLICY_SLS) {
+        sls_done(w);
+      } else {
+        ils_event(w);
+      }
+    }
+    __syncwarp();
+  }
+
+  // ---- report (metrics.cpp:30-117) ------------------------------------------------------
+  if (status == SCLS_OK && (sink.n_events == 0 || completed == 0)) status = SCLS_ERR_EMPTY_LOG;
+  double thr = 0.0, avg = 0.0, p95 = 0.0, ctstd = 0.0;
+  if (status == SCLS_OK) {
+    const double span = last_completion - first_arrival;
+    const double comp = (double)completed;
+    thr = span > 0.0 ? __ddiv_rn(comp, span) : 0.0;
+    // mean in completion order (metrics.cpp:83-85)
+    double sum = 0.0;
+    if (lane == 0)
+      for (int i = 0; i < completed; ++i) sum = __dadd_rn(sum, resp[i]);
+    sum = shfl_d(sum, 0);
+    avg = __ddiv_rn(sum, comp);
+    // nearest-rank p95 (metrics.cpp:87-91): radix select of the rank-th smallest
+    const size_t rk = (size_t)ceil(__dmul_rn(0.95, comp));
+    int want = (int)(rk > 1 ? rk : 1) - 1;
+    uint64_t prefix = 0;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = lane; i < 256; i += 32) bins[i] = 0;
+      __syncwarp();
+      const uint64_t hi_mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+      for (int i = lane; i < completed; i += 32) {
+        const uint64_t k = ordered_bits(resp[i]);
+        if ((k & hi_mask) == prefix) atomicAdd(&bins[(k >> shift) & 0xff], 1);
+      }
+      __syncwarp();
+      int digit = 0;
+      if (lane == 0) {
+        int acc = 0;
+        for (int d = 0; d < 256; ++d) {
+          if (acc + bins[d] > want) {
+            digit = d;
+            break;
+          }
+          acc += bins[d];
+        }
+        want -= acc;
+      }
+      digit = shfl_i(digit, 0);
+      want = shfl_i(want, 0);
+      prefix |= (uint64_t)digit << shift;
+      __syncwarp();
+    }
+    {
+      const uint64_t u = (prefix & 0x8000000000000000ull) ? (prefix & ~0x8000000000000000ull) : ~prefix;
+      p95 = __longlong_as_double((long long)u);
+    }
+    // population std of per-worker last batch end (metrics.cpp:93-101)
+    double mean = 0.0, var = 0.0;
+    for (int w = 0; w < W; ++w) mean = __dadd_rn(mean, shfl_d(last_end, w));
+    mean = __ddiv_rn(mean, (double)W);
+    for (int w = 0; w < W; ++w) {
+      const double d = __dadd_rn(shfl_d(last_end, w), -mean);
+      var = __dadd_rn(var, __dmul_rn(d, d));
+    }
+    var = __ddiv_rn(var, (double)W);
+    ctstd = __dsqrt_rn(var);
+  }
+  if (lane == 0 && status != SCLS_OK) {
+    // A failed run has no report (the reference throws, metrics.cpp is never
+    // reached): only the status and the offending request are defined.
+    memset(R, 0, sizeof *R);
+    R->status = status;
+    R->worker_count = W;
+    R->error_request_id = status == SCLS_ERR_INFEASIBLE_REQUEST ? err_req : -1;
+    R->n_requests = n;
+    if (logging) {
+      P.rec_count[t] = sink.rec_n;
+      P.mem_count[t] = sink.mem_n;
+    }
+  } else if (lane == 0) {
+    R->status = status;
+    R->worker_count = W;
+    R->error_request_id = -1;
+    R->n_requests = n;
+    R->completed = completed;
+    const double comp = (double)completed;
+    R->throughput = thr;
+    R->avg_response_s = avg;
+    R->p95_response_s = p95;
+    R->ct_std_s = ctstd;
+    R->avg_pad_tokens = status == SCLS_OK ? __ddiv_rn((double)total_pad, comp) : 0.0;
+    R->avg_invalid_tokens = status == SCLS_OK ? __ddiv_rn((double)total_inv, comp) : 0.0;
+    R->avg_batch_size = status == SCLS_OK && batch_count > 0
+                            ? __ddiv_rn((double)batch_members, (double)batch_count) : 0.0;
+    R->early_return_ratio = status == SCLS_OK && batch_count > 0
+                                ? __ddiv_rn((double)early, (double)batch_count) : 0.0;
+    R->total_pad = total_pad;
+    R->total_invalid = total_inv;
+    R->batch_count = batch_count;
+    R->batch_members = batch_members;
+    R->early_returns = early;
+    R->n_events = sink.n_events;
+    R->n_dispatches = sink.n_disp;
+    R->n_ticks = sink.n_ticks;
+    R->h_complete_ids = kHash ? sink.hc : 0;
+    R->h_dispatch = kHash ? sink.hd : 0;
+    R->h_complete_t = kHash ? sink.ht : 0;
+    R->h_log = kHash ? sink.hl : 0;
+    R->sim_clock = clock;
+    if (logging) {
+      P.rec_count[t] = sink.rec_n;
+      P.mem_count[t] = sink.mem_n;
+    }
+  }
+}
+
+template <bool kHash, bool kLog>
+__global__ void __launch_bounds__(kSimWarps * 32) sim_kernel(SimParams p) {
+  __shared__ int32_t bins[kSimWarps][256];
+  __shared__ int32_t ssplit[kSimWarps][kSplitSmem + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * kSimWarps + warp;
+  if (t >= p.n_traces) return;
+  run_trace<kHash, kLog>(p, t, lane, bins[warp], ssplit[warp]);
+}
+
+// Σ_i ceil(min(gen_i, G) / S): the exact number of (request, slice) pairs a
+// SCLS run serves, i.e. the tick-log and batch capacity of the trace.
+__global__ void slice_caps_kernel(int32_t n_traces, const int64_t* __restrict__ req_off,
+                                  const int32_t* __restrict__ tg, const SimCfg* __restrict__ cfgs,
+                                  const int32_t* __restrict__ cfg_index, int64_t* __restrict__ caps) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n_traces) return;
+  const SimCfg c = cfgs[cfg_index ? cfg_index[warp] : 0];
+  long long s = 0;
+  if (c.policy == SCLS_POLICY_SCLS && c.S > 0)
+    for (int64_t i = req_off[warp] + lane; i < req_off[warp + 1]; i += 32) {
+      const int g = min(tg[i], c.G);
+      s += (g + c.S - 1) / c.S;
+    }
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+  if (lane == 0) caps[warp] = s;
+}
+
+// Per-config cost tables: K(L) = max_batch_size(L, S) and c(L, k) for
+// k <= min(K(L), kcap) (cost_model.cpp:49-51, memory_model.cpp:72-90).
+__global__ void k_table_kernel(int32_t Lmax, int32_t S, int32_t kcap, Mem mem, int32_t* __restrict__ Kt,
+                               int32_t* __restrict__ need) {
+  const int L = blockIdx.x * blockDim.x + threadIdx.x;
+  if (L > Lmax) return;
+  if (L == 0) {
+    Kt[0] = 0;
+    need[0] = 0;
+    return;
+  }
+  const int K = would_oom(mem, 1, L, S) ? 0 : max_batch_size(mem, L, S);
+  Kt[L] = K;
+  need[L] = min(K, kcap);
+}
+
+__global__ void cost_fill_kernel(int32_t Lmax, int32_t S, Lat lat, const int32_t* __restrict__ need,
+                                 const int32_t* __restrict__ off, int32_t base, double* __restrict__ cost) {
+  for (int L = blockIdx.x; L <= Lmax; L += gridDim.x) {
+    const int nk = need[L];
+    const double sum_l = decode_sum_l(L, S);
+    for (int k = threadIdx.x + 1; k <= nk; k += blockDim.x)
+      cost[base + off[L] + k - 1] = __dadd_rn(prefill_time(lat, k, L), decode_time_from_sum(lat, k, sum_l, S));
+  }
+}
+
+__global__ void coff_kernel(int32_t Lmax, const int32_t* __restrict__ off, int32_t base, int32_t* __restrict__ coff) {
+  const int L = blockIdx.x * blockDim.x + threadIdx.x;
+  if (L <= Lmax) coff[L] = base + off[L];
+}
+
+}  // namespace
+
+static scls_status validate_cfg_host(const scls_sched_cfg& c) {
+  if (!(c.lambda > 0.0 && c.lambda < 1.0)) return SCLS_ERR_ERROR;
+  if (!(c.gamma > 0.0)) return SCLS_ERR_ERROR;
+  if (c.slice_len < 1 || c.max_gen_limit < c.slice_len) return SCLS_ERR_ERROR;
+  if (c.fixed_batch_size < 1 || c.max_concurrent < 1 || c.worker_count < 1) return SCLS_ERR_ERROR;
+  if (c.policy < 0 || c.policy > 2) return SCLS_ERR_ERROR;
+  if (!(c.horizon_s > 0.0)) return SCLS_ERR_ERROR;
+  return SCLS_OK;
+}
+
+}  // namespace scls
+
+using namespace scls;
+
+extern "C" scls_status scls_validate_latency(const scls_latency* m);
+extern "C" scls_status scls_validate_memory(const scls_memory* m);
+
+extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int64_t* req_offset,
+                                     const double* arrival, const int32_t* input_len,
+                                     const int32_t* gen_len, int32_t n_cfgs, const scls_sched_cfg* cfgs,
+                                     const int32_t* cfg_index, const scls_latency* lat,
+                                     const scls_memory* memm, scls_trace_result* results,
+                                     int32_t hist_bins, int64_t* slice_hist, scls_event_log* log,
+                                     int32_t mem) {
+  if (!ctx) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null context");
+  ctx->err.clear();
+  ctx->err_request = -1;
+  ctx->launches = 0;
+  std::fill(ctx->timings, ctx->timings + 8, 0.f);
+  SCLS_CUDA(cudaSetDevice(ctx->device));
+  if (n_traces < 0 || n_cfgs < 1 || !cfgs || !lat || !memm || !results || !req_offset || hist_bins < 0 ||
+      (hist_bins > 0 && !slice_hist))
+    return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (n_traces == 0) return SCLS_OK;
+  cudaStream_t s = ctx->stream;
+  // Host-side copies of the small arguments.
+  std::vector<int64_t> h_off(n_traces + 1);
+  if (mem == SCLS_MEM_DEVICE) {
+    SCLS_CUDA(cudaMemcpy(h_off.data(), req_offset, sizeof(int64_t) * (n_traces + 1), cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(h_off.data(), req_offset, sizeof(int64_t) * (n_traces + 1));
+  }
+  std::vector<int32_t> h_idx;
+  if (cfg_index) {
+    h_idx.resize(n_traces);
+    if (mem == SCLS_MEM_DEVICE)
+      SCLS_CUDA(cudaMemcpy(h_idx.data(), cfg_index, sizeof(int32_t) * n_traces, cudaMemcpyDeviceToHost));
+    else
+      std::memcpy(h_idx.data(), cfg_index, sizeof(int32_t) * n_traces);
+    for (int32_t v : h_idx)
+      if (v < 0 || v >= n_cfgs) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "cfg_index out of range");
+  }
+  const int64_t total = h_off[n_traces] - h_off[0];
+  if (h_off[0] != 0 || total < 0) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "req_offset must start at 0");
+  int64_t nmax = 0;
+  for (int t = 0; t < n_traces; ++t) {
+    const int64_t nt = h_off[t + 1] - h_off[t];
+    if (nt < 0 || nt >= (1ll << 30)) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad trace size");
+    nmax = std::max(nmax, nt);
+  }
+  // Configs: validate (Simulator::Simulator, sim_engine.cpp:32-35), limits.
+  const bool model_ok = scls_validate_latency(lat) == SCLS_OK && scls_validate_memory(memm) == SCLS_OK;
+  std::vector<SimCfg> hc(n_cfgs);
+  std::vector<uint8_t> hok(n_cfgs);
+  int n_tables = 0;
+  int32_t Gmax = 1;
+  for (int c = 0; c < n_cfgs; ++c) {
+    const scls_sched_cfg& x = cfgs[c];
+    if (x.worker_count > 32 && validate_cfg_host(x) == SCLS_OK)
+      return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "device simulator supports worker_count <= 32");
+    hok[c] = model_ok && validate_cfg_host(x) == SCLS_OK;
+    hc[c] = SimCfg{x.policy, x.slice_len, x.max_gen_limit, x.fixed_batch_size, x.max_concurrent,
+                   x.worker_count, x.lambda, x.gamma, x.horizon_s, -1};
+    if (hok[c] && x.policy == SCLS_POLICY_SCLS) hc[c].table = n_tables++;
+    if (hok[c]) Gmax = std::max(Gmax, x.max_gen_limit);
+    if (hok[c] && x.policy == SCLS_POLICY_ILS) hc[c].MC = std::max(1, std::min<int32_t>(x.max_concurrent, (int32_t)nmax));
+  }
+  // Stage requests.
+  const double* d_arr = arrival;
+  const int32_t* d_inp = input_len;
+  const int32_t* d_tg = gen_len;
+  int64_t* d_off = (int64_t*)ctx->buf(kSlotSim + 0, sizeof(int64_t) * (n_traces + 1));
+  SimCfg* d_cfg = (SimCfg*)ctx->buf(kSlotSim + 1, sizeof(SimCfg) * n_cfgs);
+  uint8_t* d_ok = (uint8_t*)ctx->buf(kSlotSim + 2, n_cfgs);
+  int32_t* d_idx = cfg_index ? (int32_t*)ctx->buf(kSlotSim + 3, sizeof(int32_t) * n_traces) : nullptr;
+  if (!d_off || !d_cfg || !d_ok || (cfg_index && !d_idx)) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+  SCLS_CUDA(cudaEventRecord(ctx->ev[0], s));
+  if (mem == SCLS_MEM_HOST && total > 0) {
+    double* a = (double*)ctx->buf(kSlotSim + 4, sizeof(double) * total);
+    int32_t* b = (int32_t*)ctx->buf(kSlotSim + 5, sizeof(int32_t) * total);
+    int32_t* g = (int32_t*)ctx->buf(kSlotSim + 6, sizeof(int32_t) * total);
+    if (!a || !b || !g) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+    SCLS_CUDA(cudaMemcpyAsync(a, arrival, sizeof(double) * total, cudaMemcpyHostToDevice, s));
+    SCLS_CUDA(cudaMemcpyAsync(b, input_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, s));
+    SCLS_CUDA(cudaMemcpyAsync(g, gen_len, sizeof(int32_t) * total, cudaMemcpyHostToDevice, s));
+    d_arr = a;
+    d_inp = b;
+    d_tg = g;
+  }
+  SCLS_CUDA(cudaMemcpyAsync(d_off, h_off.data(), sizeof(int64_t) * (n_traces + 1), cudaMemcpyHostToDevice, s));
+  SCLS_CUDA(cudaMemcpyAsync(d_cfg, hc.data(), sizeof(SimCfg) * n_cfgs, cudaMemcpyHostToDevice, s));
+  SCLS_CUDA(cudaMemcpyAsync(d_ok, hok.data(), n_cfgs, cudaMemcpyHostToDevice, s));
+  if (d_idx) SCLS_CUDA(cudaMemcpyAsync(d_idx, h_idx.data(), sizeof(int32_t) * n_traces, cudaMemcpyHostToDevice, s));
+  // Max input length (for the L range of the cost tables) and slice caps.
+  int32_t in_max = 1;
+  {
+    if (mem == SCLS_MEM_HOST) {
+      for (int64_t i = 0; i < total; ++i) in_max = std::max(in_max, input_len[i]);
+    } else if (total > 0) {
+      std::vector<int32_t> tmp(total);
+      SCLS_CUDA(cudaMemcpy(tmp.data(), input_len, sizeof(int32_t) * total, cudaMemcpyDeviceToHost));
+      for (int32_t v : tmp) in_max = std::max(in_max, v);
+    }
+  }
+  int64_t* d_caps = (int64_t*)ctx->buf(kSlotSim + 7, sizeof(int64_t) * n_traces);
+  if (!d_caps) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+  slice_caps_kernel<<<div_up((int64_t)n_traces * 32, 256), 256, 0, s>>>(n_traces, d_off, d_tg, d_cfg, d_idx, d_caps);
+  SCLS_LAUNCHED();
+  std::vector<int64_t> caps(n_traces);
+  SCLS_CUDA(cudaMemcpyAsync(caps.data(), d_caps, sizeof(int64_t) * n_traces, cudaMemcpyDeviceToHost, s));
+  SCLS_CUDA(cudaStreamSynchronize(s));
+  // Cost tables (one per SCLS config): L in [0, Lmax], k <= min(K(L), nmax).
+  const int32_t Lmax = (int32_t)std::min<int64_t>((int64_t)in_max + Gmax, 1 << 24);
+  int32_t* d_Kt = nullptr;
+  int32_t* d_coff = nullptr;
+  double* d_cost = nullptr;
+  if (n_tables > 0) {
+    d_Kt = (int32_t*)ctx->buf(kSlotSim + 8, sizeof(int32_t) * (size_t)n_tables * (Lmax + 1));
+    d_coff = (int32_t*)ctx->buf(kSlotSim + 9, sizeof(int32_t) * (size_t)n_tables * (Lmax + 1));
+    int32_t* need = (int32_t*)ctx->buf(kSlotSim + 10, sizeof(int32_t) * (Lmax + 2));
+    int32_t* off = (int32_t*)ctx->buf(kSlotSim + 11, sizeof(int32_t) * (Lmax + 2));
+    if (!d_Kt || !d_coff || !need || !off) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+    const Mem dm = make_mem(*memm);
+    std::vector<int32_t> totals(n_tables);
+    int64_t grand = 0;
+    for (int c = 0; c < n_cfgs; ++c) {
+      if (hc[c].table < 0) continue;
+      int32_t* Kt = d_Kt + (size_t)hc[c].table * (Lmax + 1);
+      k_table_kernel<<<div_up(Lmax + 1, 256), 256, 0, s>>>(Lmax, hc[c].S, (int32_t)std::max<int64_t>(nmax, 1), dm, Kt, need);
+      SCLS_LAUNCHED();
+      scls_status st = scan_exclusive(ctx, Lmax + 1, need, off, off + Lmax + 1);
+      if (st) return st;
+      int32_t tot = 0;
+      SCLS_CUDA(cudaMemcpyAsync(&tot, off + Lmax + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      SCLS_CUDA(cudaStreamSynchronize(s));
+      if (grand + tot > (1ll << 30)) return set_error(ctx, SCLS_ERR_CAPACITY, "simulator cost tables exceed 2^30 entries");
+      totals[hc[c].table] = tot;
+      // c(L, k) entries are written after the buffer is sized; remember the
+      // per-table base via the coff table (base + off[L]).
+      coff_kernel<<<div_up(Lmax + 1, 256), 256, 0, s>>>(Lmax, off, (int32_t)grand, d_coff + (size_t)hc[c].table * (Lmax + 1));
+      SCLS_LAUNCHED();
+      grand += tot;
+    }
+    d_cost = (double*)ctx->buf(kSlotSim + 12, sizeof(double) * (size_t)std::max<int64_t>(grand, 1));
+    if (!d_cost) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+    const Lat dl = make_lat(*lat);
+    int64_t base = 0;
+    for (int c = 0; c < n_cfgs; ++c) {
+      if (hc[c].table < 0) continue;
+      // recompute need/off for this table (cheap) and fill its entries
+      int32_t* Kt = d_Kt + (size_t)hc[c].table * (Lmax + 1);
+      k_table_kernel<<<div_up(Lmax + 1, 256), 256, 0, s>>>(Lmax, hc[c].S, (int32_t)std::max<int64_t>(nmax, 1), dm, Kt, need);
+      SCLS_LAUNCHED();
+      scls_status st = scan_exclusive(ctx, Lmax + 1, need, off, nullptr);
+      if (st) return st;
+      cost_fill_kernel<<<std::min(Lmax + 1, ctx->sm_count * 8), 128, 0, s>>>(Lmax, hc[c].S, dl, need, off, (int32_t)base, d_cost);
+      SCLS_LAUNCHED();
+      base += totals[hc[c].table];
+    }
+  }
+  // Per-trace arenas.
+  std::vector<int64_t> tbase(n_traces + 1, 0);
+  for (int t = 0; t < n_traces; ++t) {
+    const SimCfg& c = hc[cfg_index ? h_idx[t] : 0];
+    const int64_t nt = h_off[t + 1] - h_off[t];
+    tbase[t + 1] = tbase[t] + sim_layout(nt, std::max(c.W, 1), c.policy, caps[t], std::max(c.MC, 1)).total;
+  }
+  int64_t* d_tbase = (int64_t*)ctx->buf(kSlotSim + 13, sizeof(int64_t) * (n_traces + 1));
+  int64_t* d_tcap = (int64_t*)ctx->buf(kSlotSim + 14, sizeof(int64_t) * n_traces);
+  char* arena = (char*)ctx->buf(kSlotSim + 15, (size_t)std::max<int64_t>(tbase[n_traces], 16));
+  if (!d_tbase || !d_tcap || !arena) return set_error(ctx, SCLS_ERR_CUDA, "simulator arena allocation failed");
+  SCLS_CUDA(cudaMemcpyAsync(d_tbase, tbase.data(), sizeof(int64_t) * (n_traces + 1), cudaMemcpyHostToDevice, s));
+  SCLS_CUDA(cudaMemcpyAsync(d_tcap, caps.data(), sizeof(int64_t) * n_traces, cudaMemcpyHostToDevice, s));
+  // Results / histogram / log buffers.
+  scls_trace_result* d_res = results;
+  int64_t* d_hist = slice_hist;
+  if (mem == SCLS_MEM_HOST) {
+    d_res = (scls_trace_result*)ctx->buf(kSlotSim + 16, sizeof(scls_trace_result) * n_traces);
+    d_hist = hist_bins > 0 ? (int64_t*)ctx->buf(kSlotSim + 17, sizeof(int64_t) * (size_t)n_traces * hist_bins) : nullptr;
+    if (!d_res || (hist_bins > 0 && !d_hist)) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+  }
+  SimParams p{};
+  p.n_traces = n_traces;
+  p.req_off = d_off;
+  p.arr = d_arr;
+  p.inp = d_inp;
+  p.tg = d_tg;
+  p.cfgs = d_cfg;
+  p.cfg_index = d_idx;
+  p.cfg_ok = d_ok;
+  p.lat = make_lat(*lat);
+  p.Lmax = Lmax;
+  p.Kt = d_Kt;
+  p.coff = d_coff;
+  p.cost = d_cost;
+  p.arena = arena;
+  p.trace_base = d_tbase;
+  p.trace_cap = d_tcap;
+  p.res = d_res;
+  p.hist_bins = hist_bins;
+  p.hist = d_hist;
+  const bool want_log = log && log->n_logged > 0;
+  if (want_log) {
+    const int64_t nl = std::min<int64_t>(log->n_logged, n_traces);
+    p.n_logged = (int32_t)nl;
+    p.rec_cap = log->rec_cap;
+    p.mem_cap = log->mem_cap;
+    if (mem == SCLS_MEM_HOST) {
+      p.recs = (scls_event_record*)ctx->buf(kSlotSim + 18, sizeof(scls_event_record) * (size_t)nl * log->rec_cap);
+      p.mems = (scls_member*)ctx->buf(kSlotSim + 19, sizeof(scls_member) * (size_t)std::max<int64_t>(nl * log->mem_cap, 1));
+      int64_t* cnts = (int64_t*)ctx->buf(kSlotSim + 20, sizeof(int64_t) * 2 * nl);
+      if (!p.recs || !p.mems || !cnts) return set_error(ctx, SCLS_ERR_CUDA, "log allocation failed");
+      p.rec_count = cnts;
+      p.mem_count = cnts + nl;
+    } else {
+      p.recs = log->records;
+      p.mems = log->members;
+      p.rec_count = log->rec_count;
+      p.mem_count = log->mem_count;
+    }
+  }
+  SCLS_CUDA(cudaEventRecord(ctx->ev[1], s));
+  const int grid = div_up(n_traces, kSimWarps);
+  const bool hash = ctx->sim_digests;
+  if (want_log) sim_kernel<true, true><<<grid, kSimWarps * 32, 0, s>>>(p);
+  else if (hash) sim_kernel<true, false><<<grid, kSimWarps * 32, 0, s>>>(p);
+  else sim_kernel<false, false><<<grid, kSimWarps * 32, 0, s>>>(p);
+  SCLS_LAUNCHED();
+  SCLS_CUDA(cudaEventRecord(ctx->ev[2], s));
+  if (mem == SCLS_MEM_HOST) {
+    SCLS_CUDA(cudaMemcpyAsync(results, d_res, sizeof(scls_trace_result) * n_traces, cudaMemcpyDeviceToHost, s));
+    if (hist_bins > 0)
+      SCLS_CUDA(cudaMemcpyAsync(slice_hist, d_hist, sizeof(int64_t) * (size_t)n_traces * hist_bins, cudaMemcpyDeviceToHost, s));
+    if (want_log) {
+      const int64_t nl = p.n_logged;
+      SCLS_CUDA(cudaMemcpyAsync(log->rec_count, p.rec_count, sizeof(int64_t) * nl, cudaMemcpyDeviceToHost, s));
+      SCLS_CUDA(cudaMemcpyAsync(log->mem_count, p.mem_count, sizeof(int64_t) * nl, cudaMemcpyDeviceToHost, s));
+      SCLS_CUDA(cudaMemcpyAsync(log->records, p.recs, sizeof(scls_event_record) * (size_t)nl * log->rec_cap, cudaMemcpyDeviceToHost, s));
+      if (log->mem_cap > 0)
+        SCLS_CUDA(cudaMemcpyAsync(log->members, p.mems, sizeof(scls_member) * (size_t)nl * log->mem_cap, cudaMemcpyDeviceToHost, s));
+    }
+  }
+  SCLS_CUDA(cudaEventRecord(ctx->ev[3], s));
+  SCLS_CUDA(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&ctx->timings[0], ctx->ev[0], ctx->ev[3]);
+  cudaEventElapsedTime(&ctx->timings[6], ctx->ev[1], ctx->ev[2]);
+  cudaEventElapsedTime(&ctx->timings[2], ctx->ev[0], ctx->ev[1]);
+  return SCLS_OK;
 }

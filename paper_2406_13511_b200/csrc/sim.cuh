@@ -1,5 +1,65 @@
-// sim.cuh — device discrete-event simulator (sim_engine.cpp + the three
-// policies of sched_policies.cpp), one trace per warp.
+// sim.cuh — device discrete-event simulator (reference sim_engine.cpp and
+// the three policies of sched_policies.cpp), one trace per warp.
 #pragma once
 
 #include "ctx.h"
+
+namespace scls {
+
+// Per-trace scratch layout (byte offsets from the trace's arena base).
+struct SimLayout {
+  int64_t gen, sl, resp;                                  // per request
+  int64_t pool, sk, sk2, sv, T, split, segs, tlog;        // SCLS tick
+  int64_t b_start, b_n, b_lin, b_served, b_next, b_est;   // SCLS batches
+  int64_t fifo, pf_t, pf_seq, pf_w, run, ex;              // SLS / ILS
+  int64_t total;
+};
+
+__host__ __device__ inline int64_t sim_align(int64_t x) { return (x + 15) & ~(int64_t)15; }
+
+// n requests, W workers, per-worker FIFO capacity cap_w = ceil(n/W),
+// cap = total slices (SCLS tick-log / batch capacity), mc = ILS running cap.
+__host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t policy, int64_t cap,
+                                                int32_t mc) {
+  SimLayout L{};
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) {
+    const int64_t at = o;
+    o = sim_align(o + bytes);
+    return at;
+  };
+  const int64_t n1 = n + 1;
+  const int64_t cap_w = W > 0 ? (n + W - 1) / W : 0;
+  L.gen = take(4 * n1);
+  L.sl = take(4 * n1);
+  L.resp = take(8 * n1);
+  if (policy == SCLS_POLICY_SCLS) {
+    L.pool = take(4 * n1);
+    L.sk = take(8 * n1);
+    L.sk2 = take(8 * n1);
+    L.sv = take(4 * n1);
+    L.T = take(8 * (n1 + 1));
+    L.split = take(4 * (n1 + 1));
+    L.segs = take(4 * (n1 + 1));
+    L.tlog = take(4 * (cap + 1));
+    L.b_start = take(4 * (cap + 1));
+    L.b_n = take(4 * (cap + 1));
+    L.b_lin = take(4 * (cap + 1));
+    L.b_served = take(4 * (cap + 1));
+    L.b_next = take(4 * (cap + 1));
+    L.b_est = take(8 * (cap + 1));
+  } else if (policy == SCLS_POLICY_SLS) {
+    L.fifo = take(4 * (W * cap_w + 1));
+    L.pf_t = take(8 * n1);
+    L.pf_seq = take(8 * n1);
+    L.pf_w = take(4 * n1);
+  } else {
+    L.fifo = take(4 * (W * cap_w + 1));
+    L.run = take(4 * ((int64_t)W * mc + 1));
+    L.ex = take(4 * ((int64_t)mc + 1));
+  }
+  L.total = o;
+  return L;
+}
+
+}  // namespace scls

@@ -30,7 +30,7 @@ EXPORTS = [
     "scls_validate_latency", "scls_validate_memory", "scls_validate_sched",
     "scls_batch_serve_time", "scls_would_oom", "scls_max_batch_size",
     "scls_batch_requests", "scls_offload", "scls_schedule", "scls_simulate",
-    "scls_generate", "scls_make_pool", "scls_debug_dp_profile",
+    "scls_generate", "scls_make_pool", "scls_debug_dp_profile", "scls_set_option",
 ]
 
 
@@ -81,6 +81,7 @@ def load():
         "scls_generate": (i32, [P(capi.WorkloadSpec), i64, P(i64), vp, vp, vp]),
         "scls_make_pool": (i32, [i64, C.c_uint64, vp, vp, vp, vp]),
         "scls_debug_dp_profile": (i32, [vp, i32, vp]),
+        "scls_set_option": (i32, [vp, i32, i64]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -147,6 +148,10 @@ class Context:
         self.lib.scls_last_timings(self.h, out)
         return dict(zip(["total", "sort", "estimate", "dp", "backtrack", "offload", "simulate", "x"],
                         list(out)))
+
+    def set_digests(self, on):
+        """SCLS_OPT_SIM_DIGESTS: compute the per-trace log digests (default on)."""
+        self._check(self.lib.scls_set_option(self.h, 1, 1 if on else 0))
 
     def dp_profile(self, enable=True):
         """Read-and-reset the DP kernel's clock64 phase counters."""

@@ -1,0 +1,175 @@
+"""GPU parity of the trace-batched simulator (scls_simulate) against the C
+oracle, the compiled reference's golden fixtures and SURVEY Appendix B.
+Every TraceResult field is compared bit for bit (metrics are fp64 values
+computed in the reference's order; digests cover every event record)."""
+import itertools
+
+import numpy as np
+import pytest
+
+from paper_2406_13511_b200 import capi
+from tests.helpers import MEMORIES
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = [f for f, _ in capi.TraceResult._fields_ if f != "sim_clock"]
+
+
+def assert_results_equal(a, b, msg=""):
+    for f in FIELDS:
+        assert getattr(a, f) == getattr(b, f), (msg, f, getattr(a, f), getattr(b, f))
+
+
+def test_golden_runs(ctx, orc, golden):
+    lat = capi.builtin_latency_model()
+    for run in golden["simulate"]:
+        spec = capi.workload_spec(rate=run["rate"], duration_s=run["duration_s"], seed=run["seed"])
+        trace = orc.generate(spec)
+        cfg = capi.sched_cfg(policy=run["policy"], worker_count=run["workers"],
+                             slice_len=run["slice_len"], max_gen_limit=run["max_gen_limit"])
+        res, hist = ctx.simulate([trace], cfg, lat, MEMORIES[run["memory"]]())
+        for f in FIELDS:
+            v = getattr(res[0], f)
+            got = float(v).hex() if isinstance(v, float) else int(v)
+            assert got == run[f], (run["name"], f)
+        assert [int(x) for x in hist[0]] == run["hist"], run["name"]
+
+
+def test_many_traces_one_launch(ctx, orc):
+    """A mixed sweep (3 policies x slices x workers x seeds) in one call."""
+    lat = capi.builtin_latency_model()
+    mem = MEMORIES["rule"]()
+    cfgs, traces, idx = [], [], []
+    for pol, s, w in itertools.product(("scls", "sls", "ils"), (32, 128, 256), (1, 3, 8)):
+        cfgs.append(capi.sched_cfg(policy=pol, slice_len=s, worker_count=w, max_gen_limit=max(s, 512)))
+    for i in range(54):
+        spec = capi.workload_spec(rate=float(5 + i % 20), duration_s=40.0, seed=500 + i)
+        traces.append(orc.generate(spec))
+        idx.append(i % len(cfgs))
+    a, ha = ctx.simulate(traces, cfgs, lat, mem, cfg_index=idx)
+    b, hb = orc.simulate(traces, cfgs, lat, mem, cfg_index=idx)
+    for t in range(len(traces)):
+        assert_results_equal(a[t], b[t], t)
+    assert np.array_equal(ha, hb)
+
+
+def test_random_configs_vs_oracle(ctx, orc):
+    lat = capi.builtin_latency_model()
+    rng = np.random.default_rng(42)
+    traces, cfgs, mems = [], [], []
+    for trial in range(60):
+        pol = ("scls", "sls", "ils")[trial % 3]
+        spec = capi.workload_spec(rate=float(rng.uniform(2, 40)), duration_s=float(rng.uniform(5, 60)),
+                                  seed=1000 + trial,
+                                  gen_dist=(capi.codefuse_like_gen_dist(), capi.long_gen_dist(),
+                                            capi.uniform_dist(1, 300))[(trial // 3) % 3])
+        trace = orc.generate(spec)
+        cfg = capi.sched_cfg(policy=pol, worker_count=int(rng.integers(1, 33)),
+                             slice_len=int(rng.choice([1, 7, 16, 64, 128, 512])), max_gen_limit=1024,
+                             fixed_batch_size=int(rng.integers(1, 40)),
+                             max_concurrent=int(rng.integers(1, 60)),
+                             lambda_=float(rng.uniform(0.05, 0.95)), gamma=float(rng.uniform(0.5, 6)))
+        mname = ("rule", "analytic", "rule")[trial % 3]
+        a, ha = ctx.simulate([trace], cfg, lat, MEMORIES[mname]())
+        b, hb = orc.simulate([trace], cfg, lat, MEMORIES[mname]())
+        assert_results_equal(a[0], b[0], (trial, pol, mname))
+        assert np.array_equal(ha, hb), trial
+
+
+def _log_rows(log, t):
+    recs = log["records"]
+    mems = log["members"]
+    n = int(log["rec_count"][t])
+    m = int(log["mem_count"][t])
+    base = t * log["rec_cap"]
+    mbase = t * log["mem_cap"]
+    out = []
+    for i in range(n):
+        r = recs[base + i]
+        row = tuple(getattr(r, f) for f, _ in capi.EventRecord._fields_ if f != "member_offset")
+        mm = tuple((mems[mbase + r.member_offset + j].request, mems[mbase + r.member_offset + j].effective_input,
+                    mems[mbase + r.member_offset + j].pad, mems[mbase + r.member_offset + j].gen,
+                    mems[mbase + r.member_offset + j].invalid) for j in range(r.member_count))
+        out.append((row, mm))
+    return out, m
+
+
+def test_full_event_logs(ctx, orc):
+    """Record-by-record equality of the event log (event_log.h:52-69)."""
+    lat = capi.builtin_latency_model()
+    traces = [orc.generate(capi.workload_spec(rate=12.0, duration_s=25.0, seed=77 + i)) for i in range(3)]
+    for pol in ("scls", "sls", "ils"):
+        cfg = capi.sched_cfg(policy=pol, worker_count=3, slice_len=64)
+        a, _, la = ctx.simulate(traces, cfg, lat, MEMORIES["rule"](), n_logged=3, rec_cap=20000, mem_cap=20000)
+        b, _, lb = orc.simulate(traces, cfg, lat, MEMORIES["rule"](), n_logged=3, rec_cap=20000, mem_cap=20000)
+        for t in range(3):
+            ra, ma = _log_rows(la, t)
+            rb, mb = _log_rows(lb, t)
+            assert len(ra) == len(rb) and ma == mb, (pol, t)
+            for i, (x, y) in enumerate(zip(ra, rb)):
+                assert x == y, (pol, t, i, x, y)
+
+
+def test_digests_off_keeps_metrics(ctx, orc):
+    lat = capi.builtin_latency_model()
+    trace = orc.generate(capi.workload_spec(rate=20.0, duration_s=60.0))
+    cfg = capi.sched_cfg()
+    a, _ = ctx.simulate([trace], cfg, lat, MEMORIES["rule"]())
+    ctx.set_digests(False)
+    try:
+        b, _ = ctx.simulate([trace], cfg, lat, MEMORIES["rule"]())
+    finally:
+        ctx.set_digests(True)
+    for f in FIELDS:
+        if not f.startswith("h_"):
+            assert getattr(a[0], f) == getattr(b[0], f), f
+    assert b[0].h_log == 0
+
+
+def test_error_statuses(ctx, orc):
+    lat = capi.builtin_latency_model()
+    trace = orc.generate(capi.workload_spec(rate=20.0, duration_s=10.0))
+    # NonTerminationError (sim_engine_test.cpp:176-181)
+    cfg = capi.sched_cfg(worker_count=1, horizon_s=0.5)
+    for pol in ("scls", "sls", "ils"):
+        cfg.policy = capi.POLICIES[pol]
+        a, _ = ctx.simulate([trace], cfg, lat, MEMORIES["rule"]())
+        b, _ = orc.simulate([trace], cfg, lat, MEMORIES["rule"]())
+        assert a[0].status == capi.ERR_NON_TERMINATION == b[0].status
+        assert_results_equal(a[0], b[0], pol)
+    # empty workload -> EmptyLogError
+    empty = (np.zeros(0), np.zeros(0, np.int32), np.zeros(0, np.int32))
+    a, _ = ctx.simulate([empty], capi.sched_cfg(), lat, MEMORIES["rule"]())
+    assert a[0].status == capi.ERR_EMPTY_LOG
+    # arrivals out of order -> Error
+    bad = (np.array([1.0, 0.5]), np.array([10, 10], np.int32), np.array([10, 10], np.int32))
+    a, _ = ctx.simulate([bad], capi.sched_cfg(), lat, MEMORIES["rule"]())
+    assert a[0].status == 1
+    # invalid config -> Error, other traces unaffected
+    a, _ = ctx.simulate([trace, trace], [capi.sched_cfg(), capi.sched_cfg(lambda_=2.0)], lat,
+                        MEMORIES["rule"](), cfg_index=[0, 1])
+    assert a[0].status == 0 and a[1].status == 1
+    # infeasible request under SCLS -> InfeasibleRequestError with the id
+    tight = capi.analytic(1100.0, 1.0, 1.0, 1.0, 1.0)
+    a, _ = ctx.simulate([trace], capi.sched_cfg(), lat, tight)
+    b, _ = orc.simulate([trace], capi.sched_cfg(), lat, tight)
+    assert a[0].status == capi.ERR_INFEASIBLE_REQUEST == b[0].status
+    assert a[0].error_request_id == b[0].error_request_id
+
+
+def test_known_answers(ctx):
+    """sim_engine_test.cpp:62-88, 141-166: one short request; SLS 24 at t=0."""
+    lat = capi.builtin_latency_model()
+    one = (np.array([0.0]), np.array([100], np.int32), np.array([100], np.int32))
+    a, _, log = ctx.simulate([one], capi.sched_cfg(worker_count=1), lat, MEMORIES["rule"](),
+                             n_logged=1, rec_cap=64, mem_cap=64)
+    from oracle.pyoracle import oracle_lib
+    expected = oracle_lib().batch_serve_time(lat, 1, 100, 100)
+    assert a[0].completed == 1 and a[0].avg_response_s == expected
+    sls = (np.zeros(24), np.full(24, 50, np.int32), np.full(24, 60, np.int32))
+    cfg = capi.sched_cfg(policy="sls", worker_count=1, fixed_batch_size=12)
+    a, _, log = ctx.simulate([sls], cfg, lat, MEMORIES["rule"](), n_logged=1, rec_cap=256, mem_cap=256)
+    recs = [log["records"][i] for i in range(int(log["rec_count"][0]))]
+    starts = [r.t for r in recs if r.kind == 3]
+    ends = [r.t for r in recs if r.kind == 4]
+    assert len(starts) == 2 and starts[0] == 0.0 and starts[1] == ends[0]
