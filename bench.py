@@ -1,0 +1,448 @@
+"""bench.py — the driver's benchmark.
+
+Headline (BASELINE.json metric, configs[4]): simulated traces/s of the
+Monte Carlo sweep — 4096 traces (1024 seeds x arrival rates 10/15/20/25 req/s,
+600 s, 8 instances, S = 128, codefuse-like lengths, builtin latency model and
+rule-table memory) x the three policies {SCLS, SLS, ILS}: 12,288 simulations
+per step.  The trace dimension is sharded across ranks (contiguous ranges,
+strong scaling: the sweep is fixed as N grows); each rank simulates its
+shard on its GPU and the per-trace result records are all-gathered over NCCL
+(the only collective).  Device time, CUDA events on the launching stream,
+max over ranks.
+
+The same JSON line carries the scheduling-core number (configs[2]): requests
+scheduled/s for batch_requests + offload of the 1M-request pool
+(bench_batcher.cpp make_pool(2^20, 7), analytic KV cap, S = 128, 8 workers),
+with its phase breakdown.
+
+Inputs are synthetic (the reference's own generators, exact); parity of the
+measured shard is checked against the C oracle outside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("requests scheduled/sec (sort+DP batching+offload) and simulated traces/sec "
+          "at 1/2/4/8 B200")
+RATES = (10.0, 15.0, 20.0, 25.0)
+POLICIES = ("scls", "sls", "ils")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--traces", type=int, default=4096)
+    p.add_argument("--duration", type=float, default=600.0)
+    p.add_argument("--cpu-sample", type=int, default=0,
+                   help="traces per policy in the CPU baseline sample (0 = auto)")
+    p.add_argument("--no-c3", action="store_true")
+    return p.parse_args()
+
+
+def trace_spec(i, duration):
+    from paper_2406_13511_b200 import capi
+    return capi.workload_spec(rate=RATES[i % 4], duration_s=duration, seed=1000 + i // 4)
+
+
+def gen_traces(ids, duration, gen_fn):
+    """Generate traces in parallel host threads (ctypes releases the GIL)."""
+    with cf.ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
+        return list(ex.map(lambda i: gen_fn(trace_spec(i, duration)), ids))
+
+
+def flatten(traces):
+    offs = np.zeros(len(traces) + 1, np.int64)
+    for i, t in enumerate(traces):
+        offs[i + 1] = offs[i] + len(t[0])
+    arr = np.concatenate([t[0] for t in traces]).astype(np.float64)
+    inp = np.concatenate([t[1] for t in traces]).astype(np.int32)
+    gen = np.concatenate([t[2] for t in traces]).astype(np.int32)
+    return offs, arr, inp, gen
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(name):
+    """dram bytes per launch of a kernel from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get(name, {}).get("dram_bytes")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    compiled from /root/reference sources) on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    from oracle.pyoracle import RefLib, REF_SO, OracleLib, ORACLE_SO
+    from paper_2406_13511_b200 import capi
+    kind = "reference"
+    lib = RefLib(REF_SO) if os.path.exists(REF_SO) else None
+    if lib is None:
+        lib, kind = OracleLib(ORACLE_SO), "port"
+    cores = os.cpu_count() or 1
+    per = args.cpu_sample or max(8, min(64, cores * 4))
+    ids = list(range(per))
+    traces = gen_traces(ids, args.duration, lib.generate)
+    lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
+    cfgs = [capi.sched_cfg(policy=p) for p in POLICIES]
+
+    def step():
+        t0 = time.perf_counter()
+        for c in cfgs:
+            lib.simulate(traces, c, lat, mem, threads=cores)
+        return time.perf_counter() - t0
+
+    for _ in range(max(0, min(args.warmup, 1))):
+        step()
+    times = [step() for _ in range(max(1, min(args.steps, 2)))]
+    sec = statistics.median(times)
+    value = 3 * per / sec
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "traces/s",
+            "n_gpus": world, "steps": len(times), "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generators: Poisson arrivals, codefuse-like lengths)",
+            "config": {"workload": f"C5 sweep sample: {per} traces x 3 policies (600 s, 8 instances, "
+                                   "S=128, rates 10/15/20/25)", "host_threads": cores},
+            "cpu_baseline": {"value": value, "unit": "traces/s", "cores": cores, "kind": kind,
+                             "sample": f"{per} traces x 3 policies per step"},
+            "e2e": {"value": value, "unit": "traces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def bench_c3(ctx, torch, lib, capi, stream, steps, warmup):
+    """configs[2]: batch_requests + offload on the 1M pool, device-resident and e2e."""
+    n = 1 << 20
+    eff, arr, ids, _ = lib.make_pool(n, 7)
+    lat, mem = capi.builtin_latency_model(), capi.builtin_analytic_memory_model()
+    dev = torch.device("cuda")
+    d_eff = torch.from_numpy(eff).to(dev)
+    d_arr = torch.from_numpy(arr).to(dev)
+    d_ids = torch.from_numpy(ids).to(dev)
+    wid = torch.arange(8, dtype=torch.int32, device=dev)
+    loads = torch.zeros(8, dtype=torch.float64, device=dev)
+    outs = (torch.empty(n + 1, dtype=torch.int32, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
+            torch.empty(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.int64, device=dev),
+            torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int32, device=dev))
+    for _ in range(warmup):
+        loads.zero_()
+        ctx.schedule_device(n, d_eff, d_arr, d_ids, 128, lat, mem, wid, loads, outs)
+    ms, phases, launches = [], [], 0
+    for _ in range(steps):
+        loads.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        nb = ctx.schedule_device(n, d_eff, d_arr, d_ids, 128, lat, mem, wid, loads, outs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        phases.append(ctx.timings())
+        launches += ctx.launches()
+    # e2e: host buffers through the C-ABI (H2D + D2H inside the call)
+    e2e = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        r = ctx.schedule(eff, arr, ids, 128, lat, mem, np.arange(8, dtype=np.int32), [0.0] * 8)
+        e2e.append(time.perf_counter() - t0)
+    med = statistics.median(ms)
+    ph = {k: round(statistics.median(p[k] for p in phases), 3) for k in ("sort", "estimate", "dp", "backtrack", "offload")}
+    # parity vs the committed reference golden (11,820 batches, sum est)
+    tot = 0.0
+    for e in r["est"]:
+        tot += float(e)
+    return {"metric": "requests scheduled/s", "config": "C3: make_pool(2^20, 7), analytic KV cap, S=128, 8 workers",
+            "value": n / (med / 1e3), "ms_per_call": med, "phases_ms": ph,
+            "e2e_value": n / statistics.median(e2e), "e2e_ms": statistics.median(e2e) * 1e3,
+            "n_batches": int(nb), "sum_est": repr(tot),
+            "parity": "ok" if (nb == 11820 and repr(tot) == "70831.31070040006") else "MISMATCH",
+            "gpu_launches_per_call": launches // max(steps, 1)}
+
+
+def run_ours(args, rank, world, dist):
+    import torch
+
+    from paper_2406_13511_b200 import capi, lib
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    ctx = lib.Context(local, C.c_void_p(stream.cuda_stream))
+    T = args.traces
+    lo, hi = rank * T // world, (rank + 1) * T // world
+    ids = list(range(lo, hi))
+    traces = gen_traces(ids, args.duration, lib.generate)
+    offs, arr, inp, gen = flatten(traces)
+    nreq = int(offs[-1])
+    lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
+    cfgs = [capi.sched_cfg(policy=p) for p in POLICIES]
+    ntr = len(ids)
+    # device-resident inputs
+    d_offs = torch.from_numpy(offs).to(dev)
+    d_arr = torch.from_numpy(arr).to(dev)
+    d_inp = torch.from_numpy(inp).to(dev)
+    d_gen = torch.from_numpy(gen).to(dev)
+    nfields = C.sizeof(capi.TraceResult) // 8
+    d_res = [torch.empty(ntr * nfields, dtype=torch.int64, device=dev) for _ in POLICIES]
+    hist_bins = 16
+    d_hist = [torch.empty(ntr * hist_bins, dtype=torch.int64, device=dev) for _ in POLICIES]
+    ctx.set_digests(False)  # the reference's sweep reports metrics only
+
+    def sim_device(k):
+        cfg_arr = (capi.SchedCfg * 1)(cfgs[k])
+        st = ctx.lib.scls_simulate(ctx.h, ntr, C.c_void_p(d_offs.data_ptr()), C.c_void_p(d_arr.data_ptr()),
+                                   C.c_void_p(d_inp.data_ptr()), C.c_void_p(d_gen.data_ptr()), 1, cfg_arr, None,
+                                   C.byref(lat), C.byref(mem),
+                                   C.cast(C.c_void_p(d_res[k].data_ptr()), C.POINTER(capi.TraceResult)),
+                                   hist_bins, C.c_void_p(d_hist[k].data_ptr()), None, capi.MEM_DEVICE)
+        ctx._check(st)
+
+    def gather():
+        if world == 1:
+            return None
+        outs = []
+        for k in range(3):
+            n_max = (T + world - 1) // world
+            buf = torch.zeros(n_max * nfields, dtype=torch.int64, device=dev)
+            buf[:ntr * nfields] = d_res[k]
+            parts = [torch.empty_like(buf) for _ in range(world)]
+            dist.all_gather(parts, buf)
+            outs.append(parts)
+        return outs
+
+    def step():
+        for k in range(3):
+            sim_device(k)
+        gather()
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    kernel_ms = []
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            for k in range(3):
+                sim_device(k)
+                launches += ctx.launches()
+                kernel_ms.append(ctx.timings()["simulate"])
+            gather()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    elapsed = e0.elapsed_time(e1) / 1e3
+    t_max = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    elapsed = float(t_max.item())
+    total_sims = 3 * T * args.steps
+    value = total_sims / elapsed
+
+    # e2e through the public C-ABI with host buffers (H2D inputs, D2H results)
+    e2e_t = []
+    for _ in range(max(2, args.steps // 2)):
+        t0 = time.perf_counter()
+        for c in cfgs:
+            ctx.simulate_flat(offs, arr, inp, gen, c, lat, mem, hist_bins=hist_bins)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_local = statistics.median(e2e_t)
+    t_e2e = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    h2d = 3 * (nreq * 16 + (ntr + 1) * 8)
+    d2h = 3 * ntr * (C.sizeof(capi.TraceResult) + 8 * hist_bins)
+
+    # parity of this rank's first traces vs the C oracle (outside the timed region)
+    ctx.set_digests(True)
+    from oracle.pyoracle import oracle_lib
+    orc = oracle_lib()
+    k = min(ntr, 6)
+    bad = 0
+    for c in cfgs:
+        a, _ = ctx.simulate(traces[:k], c, lat, mem)
+        b, _ = orc.simulate(traces[:k], c, lat, mem)
+        for i in range(k):
+            for f, _ in capi.TraceResult._fields_:
+                if f != "sim_clock" and getattr(a[i], f) != getattr(b[i], f):
+                    bad += 1
+    statuses = set()
+    for kk in range(3):
+        r = d_res[kk].view(ntr, nfields).cpu().numpy()
+        statuses |= set(int(x) & 0xffffffff for x in r[:, 0])
+
+    if rank != 0:
+        return
+    hbm, peak_src = peaks()
+    sim_ms = statistics.median(kernel_ms) / 1e3
+    bytes_per_launch = nreq * 16 + ntr * (C.sizeof(capi.TraceResult) + 8 * hist_bins)
+    achieved = bytes_per_launch / sim_ms / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "traces/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generators: mt19937_64 Poisson arrivals, codefuse-like lengths)",
+        "config": {"workload": f"C5 Monte Carlo sweep: {T} traces (seeds x rates 10/15/20/25 req/s), "
+                               f"{args.duration:.0f} s, 8 instances, S=128, max_gen 1024, x {{SCLS,SLS,ILS}} "
+                               f"= {3 * T} simulations per step",
+                   "traces": T, "requests_per_rank": nreq, "parallelism": f"trace-sharded dp{world}",
+                   "l2": "inputs (%.0f MB) > L2 per rank" % (nreq * 16 / 1e6)},
+        "e2e": {"value": 3 * T / float(t_e2e.item()), "unit": "traces/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "sim_kernel", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic("sim_kernel"),
+                     "peak_source": peak_src,
+                     "note": "latency/issue-bound event chains; algorithmic bytes = 16 B/request in + "
+                             "result records out"},
+        "parity": {"checked": f"{k} traces x 3 policies vs C oracle, all TraceResult fields bit-exact",
+                   "mismatches": bad, "statuses": sorted(statuses)},
+        "clocks": clk.summary(),
+    }
+    if not args.no_c3:
+        line["scheduler_c3"] = bench_c3(ctx, torch, lib, capi, stream, max(2, args.steps // 2), 2)
+    if world == 1:
+        line["cpu_baseline"] = cpu_baseline(args)
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args):
+    """The reference (oracle/_ref) on this host's cores, bounded sample."""
+    from oracle.pyoracle import RefLib, REF_SO, OracleLib, ORACLE_SO
+    from paper_2406_13511_b200 import capi
+    kind = "reference"
+    try:
+        lib = RefLib(REF_SO)
+    except OSError:
+        lib, kind = OracleLib(ORACLE_SO), "port"
+    cores = os.cpu_count() or 1
+    per = args.cpu_sample or max(8, min(64, cores * 4))
+    traces = gen_traces(list(range(per)), args.duration, lib.generate)
+    lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
+    t0 = time.perf_counter()
+    for p in POLICIES:
+        lib.simulate(traces, capi.sched_cfg(policy=p), lat, mem, threads=cores)
+    sec = time.perf_counter() - t0
+    out = {"value": 3 * per / sec, "unit": "traces/s", "cores": cores, "kind": kind,
+           "sample": f"{per} traces x 3 policies of the C5 sweep, {cores} host threads"}
+    # C3 single-thread (the reference API is one serial call)
+    eff, arr, ids, _ = (OracleLib(ORACLE_SO)).make_pool(1 << 20, 7)
+    t0 = time.perf_counter()
+    res = lib.batch_requests(eff, arr, ids, 128, capi.builtin_latency_model(), capi.builtin_analytic_memory_model())
+    lib.offload(res["batch_id"], res["est"], np.arange(8, dtype=np.int32), [0.0] * 8)
+    sec3 = time.perf_counter() - t0
+    out["scheduler_c3"] = {"value": (1 << 20) / sec3, "unit": "requests scheduled/s", "cores": 1,
+                           "kind": kind, "sample": "one batch_requests + offload of the 1M pool"}
+    return out
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "ours":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1072,6 +1072,14 @@ __global__ void slice_caps_kernel(int32_t n_traces, const int64_t* __restrict__ 
   if (lane == 0) caps[warp] = s;
 }
 
+__global__ void max_reduce_kernel(int64_t n, const int32_t* __restrict__ x, int32_t* __restrict__ out) {
+  int m = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, x[i]);
+  m = __reduce_max_sync(FULL, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 // Per-config cost tables: K(L) = max_batch_size(L, S) and c(L, k) for
 // k <= min(K(L), kcap) (cost_model.cpp:49-51, memory_model.cpp:72-90).
 __global__ void k_table_kernel(int32_t Lmax, int32_t S, int32_t kcap, Mem mem, int32_t* __restrict__ Kt,
@@ -1208,16 +1216,17 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
   SCLS_CUDA(cudaMemcpyAsync(d_cfg, hc.data(), sizeof(SimCfg) * n_cfgs, cudaMemcpyHostToDevice, s));
   SCLS_CUDA(cudaMemcpyAsync(d_ok, hok.data(), n_cfgs, cudaMemcpyHostToDevice, s));
   if (d_idx) SCLS_CUDA(cudaMemcpyAsync(d_idx, h_idx.data(), sizeof(int32_t) * n_traces, cudaMemcpyHostToDevice, s));
-  // Max input length (for the L range of the cost tables) and slice caps.
+  // Max input length (for the L range of the cost tables), on device.
   int32_t in_max = 1;
   {
-    if (mem == SCLS_MEM_HOST) {
-      for (int64_t i = 0; i < total; ++i) in_max = std::max(in_max, input_len[i]);
-    } else if (total > 0) {
-      std::vector<int32_t> tmp(total);
-      SCLS_CUDA(cudaMemcpy(tmp.data(), input_len, sizeof(int32_t) * total, cudaMemcpyDeviceToHost));
-      for (int32_t v : tmp) in_max = std::max(in_max, v);
+    int32_t* d_max = (int32_t*)ctx->buf(kSlotSim + 21, sizeof(int32_t));
+    if (!d_max) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+    SCLS_CUDA(cudaMemsetAsync(d_max, 0, sizeof(int32_t), s));
+    if (total > 0) {
+      max_reduce_kernel<<<std::min(div_up(total, 256), ctx->sm_count * 8), 256, 0, s>>>(total, d_inp, d_max);
+      SCLS_LAUNCHED();
     }
+    SCLS_CUDA(cudaMemcpyAsync(&in_max, d_max, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   }
   int64_t* d_caps = (int64_t*)ctx->buf(kSlotSim + 7, sizeof(int64_t) * n_traces);
   if (!d_caps) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
@@ -1226,6 +1235,7 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
   std::vector<int64_t> caps(n_traces);
   SCLS_CUDA(cudaMemcpyAsync(caps.data(), d_caps, sizeof(int64_t) * n_traces, cudaMemcpyDeviceToHost, s));
   SCLS_CUDA(cudaStreamSynchronize(s));
+  in_max = std::max(in_max, 1);
   // Cost tables (one per SCLS config): L in [0, Lmax], k <= min(K(L), nmax).
   const int32_t Lmax = (int32_t)std::min<int64_t>((int64_t)in_max + Gmax, 1 << 24);
   int32_t* d_Kt = nullptr;
