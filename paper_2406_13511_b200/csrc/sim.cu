@@ -180,6 +180,29 @@ __device__ __forceinline__ int argmin_event(double t, unsigned long long s, int 
   return shfl_i(bl, 0);
 }
 
+// (t, seq) lexicographic min over the lanes with has == true, by warp
+// reductions on the order-preserving bits of t (seq only on exact time ties).
+__device__ __forceinline__ int argmin_event_redux(double t, unsigned long long s, bool has, int lane,
+                                                  double* bt, unsigned long long* bs) {
+  const uint64_t key = has ? ordered_bits(t) : ~0ull;
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mh = __reduce_min_sync(FULL, hi);
+  const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
+  unsigned tie = __ballot_sync(FULL, hi == mh && lo == ml);
+  if (__popc(tie) > 1) {
+    const bool in = (tie >> lane) & 1u;
+    const unsigned sh = (unsigned)(s >> 32), sl = (unsigned)s;
+    const unsigned msh = __reduce_min_sync(FULL, in ? sh : 0xffffffffu);
+    const unsigned msl = __reduce_min_sync(FULL, in && sh == msh ? sl : 0xffffffffu);
+    tie = __ballot_sync(FULL, in && sh == msh && sl == msl);
+  }
+  const int w = __ffs(tie) - 1;
+  *bt = has ? t : dinf();
+  *bt = shfl_d(*bt, w);
+  *bs = __shfl_sync(FULL, s, w);
+  return w;
+}
+
 // Stable LSD radix sort of n (key, val) pairs on key bits [0, bits), warp-wide,
 // ping-ponging between (k, v) and (k2, v2).  Returns true when the result is
 // in (k2, v2).  bins: 256 ints of this warp's shared memory.
@@ -251,7 +274,7 @@ __device__ __forceinline__ int bits_of(uint32_t x) { return x ? 32 - __clz(x) : 
 
 // ---- the per-trace simulation -------------------------------------------------------
 
-template <bool kHash, bool kLog>
+template <int POL, bool kHash, bool kLog>
 __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, int32_t* ssplit) {
   const int64_t r0 = P.req_off[t];
   const int n = (int)(P.req_off[t + 1] - r0);
@@ -287,7 +310,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   }
 
   char* base = P.arena + P.trace_base[t];
-  const SimLayout Lay = sim_layout(n, W, C.policy, P.trace_cap[t], C.MC);
+  const SimLayout Lay = sim_layout(n, W, POL, P.trace_cap[t], C.MC);
   int32_t* gen = (int32_t*)(base + Lay.gen);
   int32_t* sl = (int32_t*)(base + Lay.sl);
   double* resp = (double*)(base + Lay.resp);
@@ -310,6 +333,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   int inf_start = 0, inf_n = 0, inf_lin = 0, inf_lout = 0;  // SLS in-flight batch
   long long inf_id = 0;
   int n_run = 0, boundary = 0, seg_n = 0, seg_lin = 0, seg_it = 0;  // ILS
+  int it_cnt = 0, next_exit = 0, mctx = 0;
   long long seg_id = -1;
 
   // Trace-wide uniform state.
@@ -355,7 +379,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   const double* cost = P.cost;
   const Lat lat = P.lat;
 
-  if (C.policy == SCLS_POLICY_SCLS) {  // sched_policies.cpp:84: first tick at 0
+  if (POL == SCLS_POLICY_SCLS) {  // sched_policies.cpp:84: first tick at 0
     tick_t = 0.0;
     tick_s = next_seq++;
   }
@@ -705,44 +729,65 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   };
 
   // ILS iteration boundary (sched_policies.cpp:292-391) for instance w.
+  // Running requests live in per-instance slots {id, join_iter, lim, inp}
+  // with lim = min(true_gen, max_gen_limit): a request's generated count is
+  // it_cnt - join_iter, and it exits at the first boundary where that
+  // reaches lim.  next_exit = min(join_iter + lim) and mctx (max effective
+  // input over running) are kept per instance, so an iteration that neither
+  // retires nor admits anyone (the common case) is O(1) and touches no memory.
   auto ils_event = [&](int w) {
     const unsigned lt = (1u << lane) - 1u;
     const double now = clock;
-    int32_t* run = run_base + (int64_t)w * C.MC;
+    int4* run = (int4*)run_base + (int64_t)w * C.MC;
     const int32_t* wq = fifo_base + (int64_t)w * cap_w;
-    int nr = shfl_i(n_run, w);
-    int nexit = 0, keep = 0;
-    int32_t* exit_ids = ex_base;  // exits in member order (<= max_concurrent)
-    if (nr > 0) {
-      if (lane == w) seg_it += 1;
-      for (int b0 = 0; b0 < nr; b0 += 32) {
-        const int i = b0 + lane;
-        const bool ok = i < nr;
-        int id = 0;
-        bool ex = false;
-        if (ok) {
-          id = run[i];
-          const int g = gen[id] + 1;
-          gen[id] = g;
-          ex = g >= tg[id] || g >= C.G;
-        }
-        const unsigned em = __ballot_sync(FULL, ok && ex);
-        const unsigned km = __ballot_sync(FULL, ok && !ex);
-        __syncwarp();
-        if (ok && ex) exit_ids[nexit + __popc(em & lt)] = id;
-        if (ok && !ex) run[keep + __popc(km & lt)] = id;
-        nexit += __popc(em);
-        keep += __popc(km);
-        __syncwarp();
-      }
-      nr = keep;
-    }
-    // Joins: FCFS from the waiting FIFO up to max_concurrent.
+    const int nr = shfl_i(n_run, w);
+    const int it1 = shfl_i(it_cnt, w) + (nr > 0 ? 1 : 0);
     const int head = shfl_i(f_head, w), tail = shfl_i(f_tail, w);
-    const int njoin = min(C.MC - nr, tail - head);
-    for (int i = lane; i < njoin; i += 32) run[nr + i] = wq[head + i];
+    const bool exit_possible = nr > 0 && it1 >= shfl_i(next_exit, w);
+    const bool join_possible = tail > head && (nr < C.MC || exit_possible);
+    if (nr > 0 && !exit_possible && !join_possible) {  // unchanged iteration
+      if (lane == w) {
+        it_cnt = it1;
+        seg_it += 1;
+        mctx += 1;
+        ev_t = __dadd_rn(now, decode_step_time(lat, mctx, nr));
+        ev_s = next_seq;
+      }
+      ++next_seq;
+      return;
+    }
+    if (nr > 0 && lane == w) {
+      it_cnt = it1;
+      seg_it += 1;
+    }
+    // retire: survivors compacted in order, exits in member order
+    int nexit = 0, keep = 0;
+    for (int b0 = 0; b0 < nr; b0 += 32) {
+      const int i = b0 + lane;
+      const bool ok = i < nr;
+      int4 v = make_int4(0, 0, 0, 0);
+      bool ex = false;
+      if (ok) {
+        v = run[i];
+        ex = it1 - v.y >= v.z;
+      }
+      const unsigned em = __ballot_sync(FULL, ok && ex);
+      const unsigned km = __ballot_sync(FULL, ok && !ex);
+      __syncwarp();
+      if (ok && ex) ex_base[nexit + __popc(em & lt)] = v.x;
+      if (ok && !ex) run[keep + __popc(km & lt)] = v;
+      nexit += __popc(em);
+      keep += __popc(km);
+      __syncwarp();
+    }
+    // admit FCFS up to max_concurrent
+    const int njoin = min(C.MC - keep, tail - head);
+    for (int j = lane; j < njoin; j += 32) {
+      const int id = wq[head + j];
+      run[keep + j] = make_int4(id, it1, min(tg[id], C.G), inp[id]);
+    }
     __syncwarp();
-    const int nr_new = nr + njoin;
+    const int nr_new = keep + njoin;
     if (lane == w) {
       f_head = head + njoin;
       n_run = nr_new;
@@ -762,7 +807,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     }
     for (int c0 = 0; c0 < nexit; c0 += 32) {
       const int cnt = min(32, nexit - c0);
-      const int id = lane < cnt ? exit_ids[c0 + lane] : 0;
+      const int id = lane < cnt ? ex_base[c0 + lane] : 0;
       __syncwarp();
       complete_chunk(cnt, id, w);
     }
@@ -770,32 +815,36 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       if (lane == w) boundary = 0;
       return;
     }
-    int mctx = 0;
+    int mc = 0, nx = 0x7fffffff;
     for (int i = lane; i < nr_new; i += 32) {
-      const int id = run[i];
-      mctx = max(mctx, inp[id] + gen[id]);
+      const int4 v = run[i];
+      mc = max(mc, v.w + (it1 - v.y));
+      nx = min(nx, v.y + v.z);
     }
-    mctx = __reduce_max_sync(FULL, mctx);
-    long long cur_seg = shfl_l(seg_id, w);
+    mc = __reduce_max_sync(FULL, mc);
+    nx = __reduce_min_sync(FULL, nx);
+    long long cur_seg = sid;
     if (changed) {
       cur_seg = next_batch++;
       if (lane == w) {
         seg_id = cur_seg;
         seg_n = nr_new;
-        seg_lin = mctx;
+        seg_lin = mc;
         seg_it = 0;
       }
-      sink.record(lane, 3, now, -1, w, cur_seg, nr_new, mctx, 0, 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
+      sink.record(lane, 3, now, -1, w, cur_seg, nr_new, mc, 0, 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
     }
-    double it = decode_step_time(lat, mctx, nr_new);
+    double it = decode_step_time(lat, mc, nr_new);
     for (int j = 0; j < njoin; ++j) {
-      const int id = run[nr + j];
-      if (lane == 0) sl[id] = 1;
-      it = __dadd_rn(it, prefill_time(lat, 1, inp[id]));
-      // planned_l_out = remaining_gen() (sched_policies.cpp:384)
-      sink.record(lane, 2, now, id, w, cur_seg, 1, inp[id], tg[id] - gen[id], 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
+      const int4 v = run[keep + j];
+      if (lane == 0) sl[v.x] = 1;
+      it = __dadd_rn(it, prefill_time(lat, 1, v.w));
+      // planned_l_out = remaining_gen() = true_gen (nothing generated yet), sched_policies.cpp:384
+      sink.record(lane, 2, now, v.x, w, cur_seg, 1, v.w, tg[v.x], 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
     }
     if (lane == w) {
+      mctx = mc;
+      next_exit = nx;
       ev_t = __dadd_rn(now, it);
       ev_s = next_seq;
       boundary = 1;
@@ -812,17 +861,17 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     if (dirty) {
       double bt;
       unsigned long long bs;
-      const int bw = argmin_event(lane < W ? ev_t : dinf(), lane < W ? ev_s : ~0ull, lane, rounds, &bt, &bs);
+      const int bw = argmin_event_redux(ev_t, ev_s, lane < W && ev_t != dinf(), lane, &bt, &bs);
       na_t = bt;
       na_s = bs;
       na_w = bw;
-      if (C.policy == SCLS_POLICY_SCLS) {
+      if (POL == SCLS_POLICY_SCLS) {
         if (tick_t < na_t || (tick_t == na_t && tick_s < na_s)) {
           na_t = tick_t;
           na_s = tick_s;
           na_w = -1;
         }
-      } else if (C.policy == SCLS_POLICY_SLS && pf_head < pf_tail) {
+      } else if (POL == SCLS_POLICY_SLS && pf_head < pf_tail) {
         const double ft = pf_t[pf_head];
         const unsigned long long fs = pf_seq[pf_head];
         if (ft < na_t || (ft == na_t && fs < na_s)) {
@@ -836,7 +885,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     const double bound = fmin(na_t, C.horizon);
     if (cur < n && arr[cur] <= bound) {
       // Arrival(s): seq < n, so they precede any non-arrival event at the same time.
-      if (C.policy == SCLS_POLICY_SCLS) {
+      if (POL == SCLS_POLICY_SCLS) {
         // SCLS arrivals only append to the pool: take every arrival <= bound.
         int cnt = 0;
         for (;;) {
@@ -871,7 +920,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       if (first_arrival == dinf()) first_arrival = clock;
       sink.record(lane, 0, clock, id, -1, -1, 0, 0, 0, 0, 0.0, inp[id], tg[id], 0.0, 0, 0.0, 0);
       const int w = (int)(rr++ % W);
-      if (C.policy == SCLS_POLICY_SLS) {  // sched_policies.cpp:194-201
+      if (POL == SCLS_POLICY_SLS) {  // sched_policies.cpp:194-201
         if (lane == w) fifo[f_tail++] = id;
         if (lane == 0) {
           pf_t[pf_tail] = clock;
@@ -904,7 +953,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     clock = na_t;
     dirty = true;
     if (na_w < 0) {
-      if (C.policy == SCLS_POLICY_SCLS) {
+      if (POL == SCLS_POLICY_SCLS) {
         tick_t = dinf();
         tick_s = ~0ull;
         status = scls_tick();
@@ -920,7 +969,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         ev_t = dinf();
         ev_s = ~0ull;
       }
-      if (C.policy == SCLS_POLICY_SCLS) {
+      if (POL == SCLS_POLICY_SCLS) {
         const int b = shfl_i(infl, w);
         if (lane == w) {
           busy = 0;
@@ -928,7 +977,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         }
         scls_done(w, b);
         start_next_scls(w);
-      } else if (C.policy == SCLS_POLICY_SLS) {
+      } else if (POL == SCLS_POLICY_SLS) {
         sls_done(w);
       } else {
         ils_event(w);
@@ -1044,14 +1093,15 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   }
 }
 
-template <bool kHash, bool kLog>
-__global__ void __launch_bounds__(kSimWarps * 32) sim_kernel(SimParams p) {
+template <int POL, bool kHash, bool kLog>
+__global__ void __launch_bounds__(kSimWarps * 32) sim_kernel(SimParams p, const int32_t* __restrict__ list,
+                                                              int32_t count) {
   __shared__ int32_t bins[kSimWarps][256];
-  __shared__ int32_t ssplit[kSimWarps][kSplitSmem + 1];
+  __shared__ int32_t ssplit[POL == SCLS_POLICY_SCLS ? kSimWarps : 1][POL == SCLS_POLICY_SCLS ? kSplitSmem + 1 : 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * kSimWarps + warp;
-  if (t >= p.n_traces) return;
-  run_trace<kHash, kLog>(p, t, lane, bins[warp], ssplit[warp]);
+  const int g = blockIdx.x * kSimWarps + warp;
+  if (g >= count) return;
+  run_trace<POL, kHash, kLog>(p, list[g], lane, bins[warp], ssplit[POL == SCLS_POLICY_SCLS ? warp : 0]);
 }
 
 // Σ_i ceil(min(gen_i, G) / S): the exact number of (request, slice) pairs a
@@ -1347,12 +1397,39 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
     }
   }
   SCLS_CUDA(cudaEventRecord(ctx->ev[1], s));
-  const int grid = div_up(n_traces, kSimWarps);
+  // One launch per policy over that policy's traces (compile-time policy
+  // keeps each kernel lean); invalid configs ride along (status Error).
+  std::vector<int32_t> lists[3];
+  for (int t = 0; t < n_traces; ++t) {
+    const int pol = hc[cfg_index ? h_idx[t] : 0].policy;
+    lists[(pol >= 0 && pol <= 2) ? pol : 0].push_back(t);
+  }
+  int32_t* d_lists = (int32_t*)ctx->buf(kSlotSim + 22, sizeof(int32_t) * (n_traces + 3));
+  if (!d_lists) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+  {
+    std::vector<int32_t> flat;
+    flat.reserve(n_traces);
+    for (auto& l : lists) flat.insert(flat.end(), l.begin(), l.end());
+    SCLS_CUDA(cudaMemcpyAsync(d_lists, flat.data(), sizeof(int32_t) * n_traces, cudaMemcpyHostToDevice, s));
+  }
   const bool hash = ctx->sim_digests;
-  if (want_log) sim_kernel<true, true><<<grid, kSimWarps * 32, 0, s>>>(p);
-  else if (hash) sim_kernel<true, false><<<grid, kSimWarps * 32, 0, s>>>(p);
-  else sim_kernel<false, false><<<grid, kSimWarps * 32, 0, s>>>(p);
-  SCLS_LAUNCHED();
+  int64_t at = 0;
+  for (int pol = 0; pol < 3; ++pol) {
+    const int32_t cnt = (int32_t)lists[pol].size();
+    if (cnt == 0) continue;
+    const int grid = div_up(cnt, kSimWarps);
+    const int32_t* l = d_lists + at;
+    at += cnt;
+#define SCLS_SIM_LAUNCH(POLV)                                                                     \
+  if (want_log) sim_kernel<POLV, true, true><<<grid, kSimWarps * 32, 0, s>>>(p, l, cnt);          \
+  else if (hash) sim_kernel<POLV, true, false><<<grid, kSimWarps * 32, 0, s>>>(p, l, cnt);        \
+  else sim_kernel<POLV, false, false><<<grid, kSimWarps * 32, 0, s>>>(p, l, cnt);
+    if (pol == SCLS_POLICY_SCLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SCLS) }
+    else if (pol == SCLS_POLICY_SLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SLS) }
+    else { SCLS_SIM_LAUNCH(SCLS_POLICY_ILS) }
+#undef SCLS_SIM_LAUNCH
+    SCLS_LAUNCHED();
+  }
   SCLS_CUDA(cudaEventRecord(ctx->ev[2], s));
   if (mem == SCLS_MEM_HOST) {
     SCLS_CUDA(cudaMemcpyAsync(results, d_res, sizeof(scls_trace_result) * n_traces, cudaMemcpyDeviceToHost, s));

@@ -55,7 +55,7 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
     L.pf_w = take(4 * n1);
   } else {
     L.fifo = take(4 * (W * cap_w + 1));
-    L.run = take(4 * ((int64_t)W * mc + 1));
+    L.run = take(16 * ((int64_t)W * mc + 1));
     L.ex = take(4 * ((int64_t)mc + 1));
   }
   L.total = o;
