@@ -246,7 +246,7 @@ def bench_c3(ctx, torch, lib, capi, stream, steps, warmup):
 def run_ours(args, rank, world, dist):
     import torch
 
-    from paper_2406_13511_b200 import capi, lib
+    from paper_2406_13511_b200 import capi, lib, sweep
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -254,7 +254,7 @@ def run_ours(args, rank, world, dist):
     stream = torch.cuda.current_stream()
     ctx = lib.Context(local, C.c_void_p(stream.cuda_stream))
     T = args.traces
-    lo, hi = rank * T // world, (rank + 1) * T // world
+    lo, hi = sweep.shard_range(T, rank, world)
     ids = list(range(lo, hi))
     traces = gen_traces(ids, args.duration, lib.generate)
     offs, arr, inp, gen = flatten(traces)
@@ -283,17 +283,10 @@ def run_ours(args, rank, world, dist):
         ctx._check(st)
 
     def gather():
+        # the sweep's only collective: per-trace result records to every rank
         if world == 1:
             return None
-        outs = []
-        for k in range(3):
-            n_max = (T + world - 1) // world
-            buf = torch.zeros(n_max * nfields, dtype=torch.int64, device=dev)
-            buf[:ntr * nfields] = d_res[k]
-            parts = [torch.empty_like(buf) for _ in range(world)]
-            dist.all_gather(parts, buf)
-            outs.append(parts)
-        return outs
+        return [sweep.gather_records(d_res[k].view(ntr, nfields), T, world, dist) for k in range(3)]
 
     def step():
         for k in range(3):
