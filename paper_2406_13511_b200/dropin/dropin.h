@@ -1,0 +1,41 @@
+// dropin.h — shared glue of the B200 drop-in for the reference library.
+//
+// The files in this directory are meant to REPLACE four translation units of
+// the reference's libslicesim_core (core/src/batcher.cpp, offloader.cpp,
+// sim_engine.cpp, experiment.cpp): they define the same functions with the
+// same signatures and exception behaviour, against the reference's own
+// headers, and run the work on the B200 through the C-ABI
+// (include/scls_capi.h, libscls_b200.so).  See INTEGRATION.md.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "scls_capi.h"
+#include "slicesim/cost_model.h"
+#include "slicesim/errors.h"
+#include "slicesim/memory_model.h"
+#include "slicesim/sched_policies.h"
+
+namespace slicesim {
+namespace b200 {
+
+// One scls_ctx per host thread (the C-ABI contract), created on first use on
+// device 0 (SCLS_DEVICE overrides).  Throws Error when no device is usable:
+// the drop-in has no CPU fallback.
+scls_ctx* context();
+
+// Rethrows the last failure of `ctx` as the matching reference exception
+// (errors.h:26-87).
+[[noreturn]] void raise(scls_ctx* ctx, scls_status st);
+inline void check(scls_ctx* ctx, scls_status st) {
+  if (st != SCLS_OK) raise(ctx, st);
+}
+
+scls_latency to_c(const LatencyModel& m);
+scls_memory to_c(const MemoryModel& m);
+scls_sched_cfg to_c(const SchedulerConfig& c, double horizon_s);
+
+}  // namespace b200
+}  // namespace slicesim

@@ -1,0 +1,190 @@
+// experiment_gpu.cpp — drop-in replacement of the reference's
+// core/src/experiment.cpp.  run_experiment keeps its structure (models →
+// workload → Simulator::run, now on the B200 → compute).  sweep
+// (experiment.h:52-53) is the data-parallel entry point: instead of one run
+// after another it builds every run of the sweep and simulates all of them
+// in ONE scls_simulate call (one warp per trace), reading the reports the
+// device computes online (metrics.cpp:30-117, bit for bit).  Errors surface
+// in value order, as the sequential reference would raise them.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <ostream>
+#include <sstream>
+
+#include "dropin.h"
+#include "slicesim/experiment.h"
+#include "slicesim/sim_engine.h"
+#include "slicesim/workload.h"
+
+namespace slicesim {
+
+LatencyModel resolve_latency_model(const std::string& path) {
+  if (path.empty()) return builtin_latency_model();
+  return load_latency_model(path);
+}
+
+MemoryModel resolve_memory_model(const std::string& path) {
+  if (path.empty()) return builtin_memory_model();
+  if (path == "builtin-analytic") return builtin_analytic_memory_model();
+  return load_memory_model(path);
+}
+
+namespace {
+
+std::vector<Request> load_workload(const RunConfig& cfg) {
+  if (cfg.workload_from_trace) {
+    if (cfg.trace_path.empty()) throw Error("workload.kind = trace requires workload.trace = <path>");
+    return load_trace(cfg.trace_path, cfg.workload.max_input_limit, cfg.workload.max_gen_limit);
+  }
+  return generate(cfg.workload);
+}
+
+RunConfig with_value(const RunConfig& base, const std::string& param, double value) {
+  RunConfig cfg = base;
+  if (param == "rate") cfg.workload.rate = value;
+  else if (param == "slice_len") cfg.sched.slice_len = static_cast<int>(std::llround(value));
+  else if (param == "workers") cfg.sched.worker_count = static_cast<int>(std::llround(value));
+  else throw Error("unknown sweep parameter '" + param + "' (expected rate, slice_len, or workers)");
+  return cfg;
+}
+
+}  // namespace
+
+RunResult run_experiment(const RunConfig& cfg) {
+  const LatencyModel latency = resolve_latency_model(cfg.latency_model_path);
+  const MemoryModel memory = resolve_memory_model(cfg.memory_model_path);
+  std::vector<Request> requests = load_workload(cfg);
+  Simulator sim(cfg.sched, latency, memory, cfg.horizon_s);
+  auto policy = make_scheduler(cfg.sched.policy);
+  RunResult result;
+  result.log = sim.run(std::move(requests), *policy);
+  result.report = compute(result.log);
+  return result;
+}
+
+std::vector<SweepRow> sweep(const RunConfig& base, const std::string& param,
+                            const std::vector<double>& values) {
+  if (values.empty()) throw Error("sweep requires at least one value");
+  const std::size_t nv = values.size();
+  // Host preparation per value; failures are deferred so they surface in value order.
+  std::vector<std::exception_ptr> early(nv);
+  std::vector<std::vector<Request>> work(nv);
+  std::vector<scls_sched_cfg> cfgs(nv);
+  std::vector<scls_latency> lats(nv);
+  std::vector<scls_memory> mems(nv);
+  for (std::size_t v = 0; v < nv; ++v) {
+    try {
+      const RunConfig cfg = with_value(base, param, values[v]);
+      const LatencyModel lat = resolve_latency_model(cfg.latency_model_path);
+      const MemoryModel mem = resolve_memory_model(cfg.memory_model_path);
+      work[v] = load_workload(cfg);
+      Simulator check(cfg.sched, lat, mem, cfg.horizon_s);  // constructor validation
+      cfgs[v] = b200::to_c(cfg.sched, cfg.horizon_s);
+      lats[v] = b200::to_c(lat);
+      mems[v] = b200::to_c(mem);
+    } catch (...) {
+      early[v] = std::current_exception();
+    }
+  }
+  // Runs sharing models go to the device together (models are per call).
+  std::vector<SweepRow> rows(nv);
+  std::vector<scls_trace_result> res(nv);
+  std::vector<int32_t> done(nv, 0);
+  scls_ctx* ctx = b200::context();
+  int32_t hist_bins = 2;
+  for (std::size_t v = 0; v < nv; ++v)
+    if (!early[v] && cfgs[v].slice_len > 0)
+      hist_bins = std::max<int32_t>(hist_bins, (cfgs[v].max_gen_limit + cfgs[v].slice_len - 1) / cfgs[v].slice_len + 2);
+  std::vector<int64_t> hist(nv * static_cast<std::size_t>(hist_bins));
+  for (std::size_t v0 = 0; v0 < nv; ++v0) {
+    if (early[v0] || done[v0]) continue;
+    std::vector<std::size_t> group;
+    for (std::size_t v = v0; v < nv; ++v)
+      if (!early[v] && !done[v] && std::memcmp(&lats[v], &lats[v0], sizeof(scls_latency)) == 0 &&
+          std::memcmp(&mems[v], &mems[v0], sizeof(scls_memory)) == 0)
+        group.push_back(v);
+    std::vector<int64_t> offs(1, 0);
+    std::vector<double> arr;
+    std::vector<int32_t> inp, gen, idx;
+    std::vector<scls_sched_cfg> gc;
+    for (std::size_t g = 0; g < group.size(); ++g) {
+      for (const Request& r : work[group[g]]) {
+        arr.push_back(r.arrival_time);
+        inp.push_back(r.orig_input_len);
+        gen.push_back(r.true_gen_len);
+      }
+      offs.push_back(static_cast<int64_t>(arr.size()));
+      gc.push_back(cfgs[group[g]]);
+      idx.push_back(static_cast<int32_t>(g));
+    }
+    std::vector<scls_trace_result> gr(group.size());
+    std::vector<int64_t> gh(group.size() * hist_bins);
+    b200::check(ctx, scls_simulate(ctx, static_cast<int32_t>(group.size()), offs.data(), arr.data(), inp.data(),
+                                   gen.data(), static_cast<int32_t>(gc.size()), gc.data(), idx.data(), &lats[v0],
+                                   &mems[v0], gr.data(), hist_bins, gh.data(), nullptr, SCLS_MEM_HOST));
+    for (std::size_t g = 0; g < group.size(); ++g) {
+      res[group[g]] = gr[g];
+      std::copy(gh.begin() + g * hist_bins, gh.begin() + (g + 1) * hist_bins, hist.begin() + group[g] * hist_bins);
+      done[group[g]] = 1;
+    }
+  }
+  for (std::size_t v = 0; v < nv; ++v) {
+    if (early[v]) std::rethrow_exception(early[v]);
+    const scls_trace_result& r = res[v];
+    if (r.status == SCLS_ERR_INFEASIBLE_REQUEST)
+      throw InfeasibleRequestError(r.error_request_id, "request " + std::to_string(r.error_request_id) +
+                                                           " does not fit memory even as a singleton batch");
+    if (r.status == SCLS_ERR_NON_TERMINATION) throw NonTerminationError("simulated clock reached horizon");
+    if (r.status == SCLS_ERR_EMPTY_LOG) throw EmptyLogError("cannot compute metrics from an empty log");
+    if (r.status != SCLS_OK) throw Error("device simulation failed with status " + std::to_string(r.status));
+    SweepRow& row = rows[v];
+    row.value = values[v];
+    MetricsReport& m = row.report;
+    m.throughput = r.throughput;
+    m.avg_response_s = r.avg_response_s;
+    m.p95_response_s = r.p95_response_s;
+    m.ct_std_s = r.ct_std_s;
+    m.avg_pad_tokens = r.avg_pad_tokens;
+    m.avg_invalid_tokens = r.avg_invalid_tokens;
+    m.avg_batch_size = r.avg_batch_size;
+    m.early_return_ratio = r.early_return_ratio;
+    const double completed = static_cast<double>(r.completed);
+    for (int32_t s = 0; s < hist_bins; ++s) {
+      const int64_t c = hist[v * hist_bins + s];
+      if (c > 0) m.slice_count_hist[s] = static_cast<double>(c) / completed;
+    }
+  }
+  return rows;
+}
+
+namespace {
+std::string format_double(double v) {
+  std::ostringstream out;
+  out.precision(17);
+  out << v;
+  return out.str();
+}
+}  // namespace
+
+void write_sweep_csv(std::ostream& out, const std::string& param, const std::vector<SweepRow>& rows) {
+  out << param
+      << ",throughput,avg_response_s,p95_response_s,ct_std_s,avg_pad_tokens,avg_invalid_tokens,"
+         "avg_batch_size,slice_count_hist,early_return_ratio\n";
+  for (const SweepRow& row : rows) {
+    const MetricsReport& r = row.report;
+    std::string hist;
+    for (const auto& [slices, fraction] : r.slice_count_hist) {
+      if (!hist.empty()) hist += ';';
+      hist += std::to_string(slices) + ':' + format_double(fraction);
+    }
+    out << format_double(row.value) << ',' << format_double(r.throughput) << ','
+        << format_double(r.avg_response_s) << ',' << format_double(r.p95_response_s) << ','
+        << format_double(r.ct_std_s) << ',' << format_double(r.avg_pad_tokens) << ','
+        << format_double(r.avg_invalid_tokens) << ',' << format_double(r.avg_batch_size) << ',' << hist << ','
+        << format_double(r.early_return_ratio) << '\n';
+  }
+}
+
+}  // namespace slicesim

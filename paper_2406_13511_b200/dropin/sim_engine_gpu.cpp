@@ -1,0 +1,125 @@
+// sim_engine_gpu.cpp — drop-in replacement of the reference's
+// core/src/sim_engine.cpp: Simulator::run (sim_engine.h:61-67) executes on the
+// B200 via scls_simulate (one trace, full event log) and returns the same
+// EventLog record for record.
+//
+// The device runs the three built-in policies (make_scheduler,
+// sched_policies.h:136).  A user-defined Scheduler subclass cannot run on the
+// device and is rejected with Error — there is no CPU fallback.  The hook
+// entry points the policies use from inside a host event loop
+// (enqueue_batch, schedule_tick, ...) are therefore unreachable and throw.
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "dropin.h"
+#include "slicesim/sim_engine.h"
+
+namespace slicesim {
+
+Simulator::Simulator(SchedulerConfig cfg, LatencyModel latency, MemoryModel memory, double horizon_s)
+    : cfg_(std::move(cfg)), latency_(latency), memory_(std::move(memory)), horizon_s_(horizon_s) {
+  // sim_engine.cpp:32-35 semantics: the same validators, the same errors.
+  validate(cfg_);
+  validate(latency_);
+  validate(memory_);
+  if (!(horizon_s_ > 0.0)) throw Error("simulation horizon must be > 0");
+  workers_.resize(static_cast<std::size_t>(cfg_.worker_count));
+  for (std::size_t i = 0; i < workers_.size(); ++i) workers_[i].id = static_cast<WorkerId>(i);
+  log_.worker_count = cfg_.worker_count;
+}
+
+namespace {
+[[noreturn]] void host_hook() {
+  throw Error("the B200 simulator runs the built-in policies on the device; "
+              "Simulator hooks are not callable from host code");
+}
+}  // namespace
+
+void Simulator::enqueue_batch(WorkerId, Batch, int) { host_hook(); }
+void Simulator::schedule_tick(double) { host_hook(); }
+void Simulator::schedule_policy_event(double, WorkerId) { host_hook(); }
+void Simulator::complete_request(RequestId, WorkerId) { host_hook(); }
+
+EventLog Simulator::run(std::vector<Request> workload, Scheduler& policy) {
+  std::stable_sort(workload.begin(), workload.end(), [](const Request& a, const Request& b) {
+    if (a.arrival_time != b.arrival_time) return a.arrival_time < b.arrival_time;
+    return a.id < b.id;
+  });
+  for (std::size_t i = 0; i < workload.size(); ++i)
+    if (workload[i].id != static_cast<RequestId>(i))
+      throw Error("workload request ids must be 0..n-1 in arrival order");
+  scls_sched_cfg c = b200::to_c(cfg_, horizon_s_);
+  if (dynamic_cast<SclsScheduler*>(&policy)) c.policy = SCLS_POLICY_SCLS;
+  else if (dynamic_cast<SlsScheduler*>(&policy)) c.policy = SCLS_POLICY_SLS;
+  else if (dynamic_cast<IlsScheduler*>(&policy)) c.policy = SCLS_POLICY_ILS;
+  else throw Error("custom Scheduler subclasses cannot run on the B200 device simulator");
+  const int64_t n = static_cast<int64_t>(workload.size());
+  requests_ = workload;
+  if (n == 0) return std::move(log_);
+  std::vector<double> arr(n);
+  std::vector<int32_t> inp(n), gen(n);
+  for (int64_t i = 0; i < n; ++i) {
+    arr[i] = workload[i].arrival_time;
+    inp[i] = workload[i].orig_input_len;
+    gen[i] = workload[i].true_gen_len;
+  }
+  const int64_t offs[2] = {0, n};
+  const scls_latency lat = b200::to_c(latency_);
+  const scls_memory mem = b200::to_c(memory_);
+  scls_ctx* ctx = b200::context();
+  int64_t rec_cap = 6 * n + 64, mem_cap = 4 * n + 64;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    std::vector<scls_event_record> recs(rec_cap);
+    std::vector<scls_member> mems(mem_cap);
+    int64_t rc = 0, mc = 0;
+    scls_event_log lg{1, rec_cap, mem_cap, recs.data(), mems.data(), &rc, &mc};
+    scls_trace_result res{};
+    b200::check(ctx, scls_simulate(ctx, 1, offs, arr.data(), inp.data(), gen.data(), 1, &c, nullptr, &lat,
+                                   &mem, &res, 0, nullptr, &lg, SCLS_MEM_HOST));
+    if (rc > rec_cap || mc > mem_cap) {  // the device counts past capacity: resize once
+      rec_cap = rc;
+      mem_cap = mc;
+      continue;
+    }
+    if (res.status != SCLS_OK && res.status != SCLS_ERR_EMPTY_LOG) {
+      if (res.status == SCLS_ERR_INFEASIBLE_REQUEST)
+        throw InfeasibleRequestError(res.error_request_id,
+                                     "request " + std::to_string(res.error_request_id) +
+                                         " does not fit memory even as a singleton batch");
+      if (res.status == SCLS_ERR_NON_TERMINATION)
+        throw NonTerminationError("simulated clock reached horizon " + std::to_string(horizon_s_) + " s");
+      throw Error("device simulation failed with status " + std::to_string(res.status));
+    }
+    log_.events.clear();
+    log_.events.reserve(static_cast<std::size_t>(rc));
+    for (int64_t k = 0; k < rc; ++k) {
+      const scls_event_record& r = recs[k];
+      EventRecord e;
+      e.t = r.t;
+      e.kind = static_cast<EventKind>(r.kind);
+      e.request = r.request;
+      e.worker = r.worker;
+      e.batch = r.batch;
+      e.n = r.n;
+      e.l_in = r.l_in;
+      e.planned_l_out = r.planned_l_out;
+      e.served_l_out = r.served_l_out;
+      e.est_serve_s = r.est_serve_s;
+      e.input_len = r.input_len;
+      e.gen_len = r.gen_len;
+      e.response_s = r.response_s;
+      e.slices = r.slices;
+      e.next_interval_s = r.next_interval_s;
+      for (int32_t j = 0; j < r.member_count; ++j) {
+        const scls_member& m = mems[r.member_offset + j];
+        e.members.push_back(MemberAccounting{m.request, m.effective_input, m.pad, m.gen, m.invalid});
+      }
+      log_.add(std::move(e));
+    }
+    return std::move(log_);
+  }
+  throw Error("device event log capacity could not be established");
+}
+
+}  // namespace slicesim
