@@ -23,7 +23,10 @@
 #include "batcher.cuh"
 #include "radix.cuh"
 #include "dp_chain.cuh"
+#include "dp_mono.cuh"
 #include "scls_common.cuh"
+
+extern "C" scls_status scls_validate_memory(const scls_memory* m);
 
 namespace scls {
 namespace {
@@ -360,14 +363,26 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
   const bool int_cmp = !std::signbit(in.lat->p1) && !std::signbit(in.lat->p2) && !std::signbit(in.lat->p3) &&
                        !std::signbit(in.lat->p4) && !std::signbit(in.lat->d1) && !std::signbit(in.lat->d2) &&
                        !std::signbit(in.lat->d3) && !std::signbit(in.lat->d4);
-  auto launch = [&](auto kern) -> scls_status {
-    SCLS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<1, kDpThreads, smem, s>>>((int32_t)n, Krow, cbase, cost, T, split, ctx->dp_prof);
+  auto launch = [&](auto kern, size_t bytes) -> scls_status {
+    SCLS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    kern<<<1, kDpThreads, bytes, s>>>((int32_t)n, Krow, cbase, cost, T, split, ctx->dp_prof);
     SCLS_LAUNCHED();
     return SCLS_OK;
   };
-  if (global_t) stt = int_cmp ? launch(dp_chain_kernel<true, true>) : launch(dp_chain_kernel<true, false>);
-  else stt = int_cmp ? launch(dp_chain_kernel<false, true>) : launch(dp_chain_kernel<false, false>);
+  // Monotone cost model (dp_mono.cuh): non-negative coefficients and a valid
+  // memory model make T provably non-decreasing -> exact decision rounds.
+  // When every window fits in one tile (k_max <= 32, e.g. the rule-table
+  // engines) the chain kernel's in-tile pushes beat the decision rounds.
+  const bool monotone = int_cmp && scls_validate_memory(in.mem) == SCLS_OK && ctx->dp_mode != 1 &&
+                        (k_max > 32 || ctx->dp_mode == 2);
+  ctx->dp_last_mono = monotone;
+  if (monotone) {
+    stt = global_t ? launch(dp_mono_kernel<true>, sizeof(DpMonoSmem)) : launch(dp_mono_kernel<false>, sizeof(DpMonoSmem));
+  } else if (global_t) {
+    stt = int_cmp ? launch(dp_chain_kernel<true, true>, smem) : launch(dp_chain_kernel<true, false>, smem);
+  } else {
+    stt = int_cmp ? launch(dp_chain_kernel<false, true>, smem) : launch(dp_chain_kernel<false, false>, smem);
+  }
   if (stt) return stt;
   SCLS_CUDA(cudaEventRecord(ctx->ev[3], s));
 

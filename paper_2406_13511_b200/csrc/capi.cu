@@ -218,6 +218,10 @@ scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value) {
     ctx->sim_digests = value != 0;
     return SCLS_OK;
   }
+  if (option == SCLS_OPT_DP_KERNEL) {
+    ctx->dp_mode = (int)value;
+    return SCLS_OK;
+  }
   return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "unknown option");
 }
 
@@ -429,6 +433,7 @@ scls_status scls_batch_requests(scls_ctx* ctx, int64_t n, const int32_t* eff_len
   if ((st = batch_copy_out(ctx, n, d, out, mem))) return st;
   SCLS_CUDA(cudaStreamSynchronize(ctx->stream));
   collect_timings(ctx, 4);
+  ctx->timings[7] = ctx->dp_last_mono ? 1.f : 0.f;
   return SCLS_OK;
 }
 
@@ -514,6 +519,7 @@ scls_status scls_schedule(scls_ctx* ctx, int64_t n, const int32_t* eff_len, cons
   if (n > 0 && (st = batch_copy_out(ctx, n, d, out, mem))) return st;
   SCLS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (n > 0) collect_timings(ctx, 5);
+  ctx->timings[7] = ctx->dp_last_mono ? 1.f : 0.f;
   return SCLS_OK;
 }
 

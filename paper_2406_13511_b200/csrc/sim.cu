@@ -1094,7 +1094,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
 }
 
 template <int POL, bool kHash, bool kLog>
-__global__ void __launch_bounds__(kSimWarps * 32) sim_kernel(SimParams p, const int32_t* __restrict__ list,
+__global__ void __launch_bounds__(kSimWarps * 32, POL == SCLS_POLICY_SCLS ? 4 : 8) sim_kernel(SimParams p, const int32_t* __restrict__ list,
                                                               int32_t count) {
   __shared__ int32_t bins[kSimWarps][256];
   __shared__ int32_t ssplit[POL == SCLS_POLICY_SCLS ? kSimWarps : 1][POL == SCLS_POLICY_SCLS ? kSplitSmem + 1 : 1];

@@ -146,12 +146,16 @@ class Context:
         offload, simulate."""
         out = (C.c_float * 8)()
         self.lib.scls_last_timings(self.h, out)
-        return dict(zip(["total", "sort", "estimate", "dp", "backtrack", "offload", "simulate", "x"],
+        return dict(zip(["total", "sort", "estimate", "dp", "backtrack", "offload", "simulate", "dp_mono"],
                         list(out)))
 
     def set_digests(self, on):
         """SCLS_OPT_SIM_DIGESTS: compute the per-trace log digests (default on)."""
         self._check(self.lib.scls_set_option(self.h, 1, 1 if on else 0))
+
+    def set_dp_kernel(self, mode):
+        """SCLS_OPT_DP_KERNEL: 0 auto (monotone decision kernel when allowed), 1 chain."""
+        self._check(self.lib.scls_set_option(self.h, 2, int(mode)))
 
     def dp_profile(self, enable=True):
         """Read-and-reset the DP kernel's clock64 phase counters."""

@@ -191,3 +191,64 @@ def test_batched_estimators(ctx, orc):
         got = ctx.max_batch_size(l_in[:2000], 32, mem)
         want = np.array([orc.max_batch_size(mem, int(b), 32) for b in l_in[:2000]])
         assert np.array_equal(got, want), mname
+
+
+@pytest.fixture
+def chain_ctx(ctx):
+    ctx.set_dp_kernel(1)
+    yield ctx
+    ctx.set_dp_kernel(0)
+
+
+def test_kernel_choice(ctx, orc):
+    eff, arr, ids, _ = orc.make_pool(4096, 7)
+    ctx.batch_requests(eff, arr, ids, 128, capi.builtin_latency_model(), MEMORIES["analytic"]())
+    assert ctx.timings()["dp_mono"] == 1.0  # builtin analytic model: monotone, windows > 32
+    neg = capi.latency_model(2e-6, 1e-3, 5e-5, 0.02, 1e-7, 2e-4, 3e-6, -0.0)  # sign bit set
+    ctx.batch_requests(eff, arr, ids, 128, neg, MEMORIES["analytic"]())
+    assert ctx.timings()["dp_mono"] == 0.0
+
+
+def test_chain_kernel_golden_pools(chain_ctx, orc, golden):
+    """The serial-chain kernel (non-monotone models' path) on the same goldens."""
+    lat = capi.builtin_latency_model()
+    for case in golden["batcher"]:
+        if case["n"] > 65536:
+            continue
+        eff, arr, ids, _ = orc.make_pool(case["n"], case["seed"])
+        res = chain_ctx.batch_requests(eff, arr, ids, case["slice_len"], lat, MEMORIES[case["memory"]]())
+        assert res["n_batches"] == case["n_batches"]
+        assert sha(res["seg_begin"].astype(np.int32)) == case["seg"]
+        assert sha(res["est"].astype(np.float64)) == case["est"]
+
+
+def test_non_monotone_models_vs_oracle(ctx, orc):
+    """Models outside the monotone conditions take the chain kernel; still exact."""
+    rng = np.random.default_rng(9)
+    lats = [capi.latency_model(2e-6, 1e-3, 5e-5, 0.02, 1e-7, 2e-4, 3e-6, -0.0),
+            capi.latency_model(-1e-7, 1e-3, 5e-5, 0.5, 1e-7, 2e-4, 3e-6, 0.02)]
+    for lat in lats:
+        for n in (100, 5000):
+            eff = rng.integers(1, 1500, n).astype(np.int32)
+            arr = rng.random(n)
+            ids = np.arange(n, dtype=np.int64)
+            for mname in ("rule", "analytic"):
+                assert_same_batches(ctx.batch_requests(eff, arr, ids, 64, lat, MEMORIES[mname]()),
+                                    orc.batch_requests(eff, arr, ids, 64, lat, MEMORIES[mname]()), (n, mname))
+
+
+def test_decision_kernel_forced_small_windows(ctx, orc, golden):
+    """The monotone decision kernel on rule-table pools (windows <= 28) too."""
+    ctx.set_dp_kernel(2)
+    try:
+        lat = capi.builtin_latency_model()
+        for case in golden["batcher"]:
+            if case["n"] > 65536 or case["memory"] != "rule":
+                continue
+            eff, arr, ids, _ = orc.make_pool(case["n"], case["seed"])
+            res = ctx.batch_requests(eff, arr, ids, case["slice_len"], lat, MEMORIES["rule"]())
+            assert ctx.timings()["dp_mono"] == 1.0
+            assert sha(res["seg_begin"].astype(np.int32)) == case["seg"]
+            assert sha(res["est"].astype(np.float64)) == case["est"]
+    finally:
+        ctx.set_dp_kernel(0)

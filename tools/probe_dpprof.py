@@ -16,8 +16,9 @@ for name, mem in (("analytic", capi.builtin_analytic_memory_model()), ("rule", c
     tiles = (n + 31) // 32
     nh = max(int(p[5]), 1)
     print(name, r["n_batches"], "dp ms %.2f" % ctx.timings()["dp"],
-          "per tile cycles: main chain %.0f wait %.0f | helper stage %.0f far %.0f wait %.0f" % (
-              p[0] / tiles, p[1] / tiles, p[2] / tiles / nh, p[3] / tiles / nh, p[4] / tiles / nh))
+          "per tile cycles: main %.0f (mid %.0f, rounds/tile %.2f) wait %.0f | helper stage %.0f far %.0f wait %.0f" % (
+              p[0] / tiles, p[6] / tiles, p[7] / tiles, p[1] / tiles, p[2] / tiles / nh, p[3] / tiles / nh,
+              p[4] / tiles / nh))
 ctx.dp_profile(False)
 r = ctx.batch_requests(eff, arr, ids, 128, lat, capi.builtin_memory_model())
 print("unprofiled rule dp ms %.2f" % ctx.timings()["dp"])
