@@ -341,7 +341,8 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   unsigned long long next_seq = (unsigned long long)n + 1;  // arrivals 0..n-1, EndOfRun n
   double clock = 0.0;
   int cur = 0, completed = 0;
-  long long next_batch = 0, rr = 0;
+  long long next_batch = 0;
+  int rr = 0;  // round-robin cursor (sched_policies.cpp:195,280: rr_++ % W), kept wrapped
   double first_arrival = dinf(), last_completion = -dinf();
   long long total_pad = 0, total_inv = 0, batch_count = 0, batch_members = 0, early = 0;
   double tick_t = dinf();
@@ -377,7 +378,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   const int32_t* Kt = C.table >= 0 ? P.Kt + (int64_t)C.table * (P.Lmax + 1) : nullptr;
   const int32_t* coff = C.table >= 0 ? P.coff + (int64_t)C.table * (P.Lmax + 1) : nullptr;
   const double* cost = P.cost;
-  const Lat lat = P.lat;
+  const Lat& lat = P.lat;  // stays in the kernel parameter (constant) bank: frees 16 registers
 
   if (POL == SCLS_POLICY_SCLS) {  // sched_policies.cpp:84: first tick at 0
     tick_t = 0.0;
@@ -854,10 +855,36 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
 
   // ---- the event loop (sim_engine.cpp:123-166) ------------------------------------
   bool dirty = true;
+  double next_arr = n > 0 ? arr[0] : dinf();
   double na_t = dinf();
   unsigned long long na_s = ~0ull;
   int na_w = -1;  // -1: tick / FIFO head, >= 0: lane slot
   while (completed < n) {
+    if (POL == SCLS_POLICY_ILS) {
+      // Fast lane: consecutive boundary events of instances whose iteration
+      // neither retires nor admits anyone (see ils_event) — the bulk of an
+      // ILS run.  Same (time, seq) order, same arithmetic as ils_event's
+      // unchanged branch; anything else falls through to the general path.
+      for (;;) {
+        double bt;
+        unsigned long long bs;
+        const int w = argmin_event_redux(ev_t, ev_s, lane < W && ev_t != dinf(), lane, &bt, &bs);
+        if (next_arr <= fmin(bt, C.horizon) || C.horizon <= bt) break;
+        const bool mine_fast = lane < W && n_run > 0 && it_cnt + 1 < next_exit &&
+                               !(f_tail > f_head && n_run < C.MC);
+        if (!((__ballot_sync(FULL, mine_fast) >> w) & 1u)) break;
+        clock = bt;
+        if (lane == w) {
+          it_cnt += 1;
+          seg_it += 1;
+          mctx += 1;
+          ev_t = __dadd_rn(bt, decode_step_time(lat, mctx, n_run));
+          ev_s = next_seq;
+        }
+        ++next_seq;
+      }
+      dirty = true;
+    }
     if (dirty) {
       double bt;
       unsigned long long bs;
@@ -883,7 +910,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       dirty = false;
     }
     const double bound = fmin(na_t, C.horizon);
-    if (cur < n && arr[cur] <= bound) {
+    if (next_arr <= bound) {  // next_arr = arr[cur], +INF once all arrived
       // Arrival(s): seq < n, so they precede any non-arrival event at the same time.
       if (POL == SCLS_POLICY_SCLS) {
         // SCLS arrivals only append to the pool: take every arrival <= bound.
@@ -912,14 +939,17 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         clock = arr[cur + cnt - 1];
         pool_len += cnt;
         cur += cnt;
+        next_arr = cur < n ? arr[cur] : dinf();
         __syncwarp();
         continue;
       }
       const int id = cur++;
+      next_arr = cur < n ? arr[cur] : dinf();
       clock = arr[id];
       if (first_arrival == dinf()) first_arrival = clock;
       sink.record(lane, 0, clock, id, -1, -1, 0, 0, 0, 0, 0.0, inp[id], tg[id], 0.0, 0, 0.0, 0);
-      const int w = (int)(rr++ % W);
+      const int w = rr;
+      rr = rr + 1 == W ? 0 : rr + 1;
       if (POL == SCLS_POLICY_SLS) {  // sched_policies.cpp:194-201
         if (lane == w) fifo[f_tail++] = id;
         if (lane == 0) {

@@ -173,3 +173,26 @@ def test_known_answers(ctx):
     starts = [r.t for r in recs if r.kind == 3]
     ends = [r.t for r in recs if r.kind == 4]
     assert len(starts) == 2 and starts[0] == 0.0 and starts[1] == ends[0]
+
+
+def test_c4_scale_trace(ctx, orc):
+    """configs[3] scale: one 100k-request trace (5000 s at 20 req/s) under each
+    policy, bit-exact against the oracle; plus the slice-length grid on a
+    shorter trace."""
+    lat = capi.builtin_latency_model()
+    big = orc.generate(capi.workload_spec(rate=20.0, duration_s=5000.0, seed=42))
+    assert len(big[0]) > 99000
+    for pol in ("scls", "sls", "ils"):
+        cfg = capi.sched_cfg(policy=pol)
+        a, ha = ctx.simulate([big], cfg, lat, MEMORIES["rule"]())
+        b, hb = orc.simulate([big], cfg, lat, MEMORIES["rule"]())
+        assert_results_equal(a[0], b[0], pol)
+        assert np.array_equal(ha, hb)
+    small = orc.generate(capi.workload_spec(rate=20.0, duration_s=300.0, seed=7))
+    cfgs = [capi.sched_cfg(policy=p, slice_len=s, max_gen_limit=g)
+            for p in ("scls", "sls", "ils") for s in (32, 64, 128, 256) for g in (256, 512, 1024) if s <= g]
+    a, ha = ctx.simulate([small] * len(cfgs), cfgs, lat, MEMORIES["rule"](), cfg_index=list(range(len(cfgs))))
+    b, hb = orc.simulate([small] * len(cfgs), cfgs, lat, MEMORIES["rule"](), cfg_index=list(range(len(cfgs))))
+    for i in range(len(cfgs)):
+        assert_results_equal(a[i], b[i], i)
+    assert np.array_equal(ha, hb)
