@@ -225,9 +225,12 @@ def bench_c3(ctx, torch, lib, capi, stream, steps, warmup):
         launches += ctx.launches()
     # e2e: host buffers through the C-ABI (H2D + D2H inside the call)
     e2e = []
+    p_eff = torch.from_numpy(eff).pin_memory().numpy()
+    p_arr = torch.from_numpy(arr).pin_memory().numpy()
+    p_ids = torch.from_numpy(ids).pin_memory().numpy()
     for _ in range(steps):
         t0 = time.perf_counter()
-        r = ctx.schedule(eff, arr, ids, 128, lat, mem, np.arange(8, dtype=np.int32), [0.0] * 8)
+        r = ctx.schedule(p_eff, p_arr, p_ids, 128, lat, mem, np.arange(8, dtype=np.int32), [0.0] * 8)
         e2e.append(time.perf_counter() - t0)
     med = statistics.median(ms)
     ph = {k: round(statistics.median(p[k] for p in phases), 3) for k in ("sort", "estimate", "dp", "backtrack", "offload")}
@@ -299,7 +302,7 @@ def run_ours(args, rank, world, dist):
         dist.barrier()
     torch.cuda.synchronize()
     launches = 0
-    kernel_ms = []
+    kernel_ms = {p: [] for p in POLICIES}
     with ClockSampler(local) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -307,7 +310,7 @@ def run_ours(args, rank, world, dist):
             for k in range(3):
                 sim_device(k)
                 launches += ctx.launches()
-                kernel_ms.append(ctx.timings()["simulate"])
+                kernel_ms[POLICIES[k]].append(ctx.timings()["simulate"])
             gather()
         e1.record(stream)
         torch.cuda.synchronize()
@@ -321,12 +324,18 @@ def run_ours(args, rank, world, dist):
     total_sims = 3 * T * args.steps
     value = total_sims / elapsed
 
-    # e2e through the public C-ABI with host buffers (H2D inputs, D2H results)
+    # e2e through the public C-ABI with host buffers (H2D inputs, D2H results):
+    # inputs staged once in pinned host memory, copied to the device inside
+    # every call (scls_simulate with SCLS_MEM_HOST)
+    p_offs = torch.from_numpy(offs).pin_memory().numpy()
+    p_arr = torch.from_numpy(arr).pin_memory().numpy()
+    p_inp = torch.from_numpy(inp).pin_memory().numpy()
+    p_gen = torch.from_numpy(gen).pin_memory().numpy()
     e2e_t = []
     for _ in range(max(2, args.steps // 2)):
         t0 = time.perf_counter()
         for c in cfgs:
-            ctx.simulate_flat(offs, arr, inp, gen, c, lat, mem, hist_bins=hist_bins)
+            ctx.simulate_flat(p_offs, p_arr, p_inp, p_gen, c, lat, mem, hist_bins=hist_bins)
         e2e_t.append(time.perf_counter() - t0)
     e2e_local = statistics.median(e2e_t)
     t_e2e = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
@@ -356,7 +365,9 @@ def run_ours(args, rank, world, dist):
     if rank != 0:
         return
     hbm, peak_src = peaks()
-    sim_ms = statistics.median(kernel_ms) / 1e3
+    pol_ms = {p: statistics.median(v) for p, v in kernel_ms.items()}
+    dom = max(pol_ms, key=pol_ms.get)  # the dominant launch (ILS on this sweep)
+    sim_ms = pol_ms[dom] / 1e3
     bytes_per_launch = nreq * 16 + ntr * (C.sizeof(capi.TraceResult) + 8 * hist_bins)
     achieved = bytes_per_launch / sim_ms / 1e9
     line = {
@@ -372,11 +383,13 @@ def run_ours(args, rank, world, dist):
         "e2e": {"value": 3 * T / float(t_e2e.item()), "unit": "traces/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "sim_kernel", "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic("sim_kernel"),
-                     "peak_source": peak_src,
-                     "note": "latency/issue-bound event chains; algorithmic bytes = 16 B/request in + "
-                             "result records out"},
+        "roofline": {"bound": "hbm", "kernel": f"sim_kernel<{dom.upper()}>", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(f"sim_kernel_{dom}_{T}"),
+                     "peak_source": peak_src, "bytes_per_launch": bytes_per_launch,
+                     "launch_ms": pol_ms[dom],
+                     "note": "event-chain latency/issue bound (ncu: profiles/ncu_summary.json); algorithmic "
+                             "bytes = 16 B/request in + result records out"},
+        "kernel_ms_per_policy": pol_ms,
         "parity": {"checked": f"{k} traces x 3 policies vs C oracle, all TraceResult fields bit-exact",
                    "mismatches": bad, "statuses": sorted(statuses)},
         "clocks": clk.summary(),
