@@ -865,21 +865,40 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       // neither retires nor admits anyone (see ils_event) — the bulk of an
       // ILS run.  Same (time, seq) order, same arithmetic as ils_event's
       // unchanged branch; anything else falls through to the general path.
+      // Each lane keeps the order-preserving key of its pending event and a
+      // "next boundary is unchanged" flag; only the winner's lane changes
+      // per step, the winner's time is rebuilt from the reduced key, and any
+      // exact time tie is left to the general path (which orders by seq).
+      const bool has = lane < W && ev_t != dinf();
+      uint64_t key = has ? ordered_bits(ev_t) : ~0ull;
+      bool mine_fast = has && n_run > 0 && it_cnt + 1 < next_exit && !(f_tail > f_head && n_run < C.MC);
+      // decode_step_time(mctx, n) = ((d1*n)*l + d2*n) + d3*l + d4: the n terms are fixed in a run
+      const double dn = (double)n_run;
+      const double a1 = __dmul_rn(lat.d1, dn), a2 = __dmul_rn(lat.d2, dn);
       for (;;) {
-        double bt;
-        unsigned long long bs;
-        const int w = argmin_event_redux(ev_t, ev_s, lane < W && ev_t != dinf(), lane, &bt, &bs);
+        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+        const unsigned mh = __reduce_min_sync(FULL, hi);
+        const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
+        const unsigned tie = __ballot_sync(FULL, hi == mh && lo == ml);
+        if (tie & (tie - 1u)) break;  // equal times: the general path orders by seq
+        const int w = __ffs(tie) - 1;
+        const uint64_t kmin = ((uint64_t)mh << 32) | ml;
+        if (kmin == ~0ull) break;
+        const double bt = __longlong_as_double(
+            (long long)((kmin & 0x8000000000000000ull) ? (kmin & ~0x8000000000000000ull) : ~kmin));
         if (next_arr <= fmin(bt, C.horizon) || C.horizon <= bt) break;
-        const bool mine_fast = lane < W && n_run > 0 && it_cnt + 1 < next_exit &&
-                               !(f_tail > f_head && n_run < C.MC);
         if (!((__ballot_sync(FULL, mine_fast) >> w) & 1u)) break;
         clock = bt;
         if (lane == w) {
           it_cnt += 1;
           seg_it += 1;
           mctx += 1;
-          ev_t = __dadd_rn(bt, decode_step_time(lat, mctx, n_run));
+          const double dl = (double)mctx;
+          const double it = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a1, dl), a2), __dmul_rn(lat.d3, dl)), lat.d4);
+          ev_t = __dadd_rn(bt, it);
           ev_s = next_seq;
+          key = ordered_bits(ev_t);
+          mine_fast = it_cnt + 1 < next_exit;
         }
         ++next_seq;
       }

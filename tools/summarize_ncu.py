@@ -73,10 +73,11 @@ def report(path, names):
 
     summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
+    pairs = [n.split("=", 1) if "=" in n else (n, n) for n in names]
     for r in rows[2:]:
         kname = r[h.index("Kernel Name")]
-        for n in names:
-            if n in kname:
+        for pat, n in pairs:
+            if pat in kname:
                 d = {"report": os.path.basename(path), "kernel": kname[:160]}
                 for m, key in WANT.items():
                     if m in h:
@@ -97,7 +98,7 @@ def report(path, names):
                     d["dram_bytes"] = d["dram_read_bytes"] + d["dram_write_bytes"]
                 summ[n] = d
     json.dump(summ, open(summ_path, "w"), indent=1)
-    print(json.dumps({n: summ.get(n) for n in names}, indent=1))
+    print(json.dumps({n: summ.get(n) for _, n in pairs}, indent=1))
 
 
 if __name__ == "__main__":
