@@ -1093,6 +1093,8 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     var = __ddiv_rn(var, (double)W);
     ctstd = __dsqrt_rn(var);
   }
+  if (status != SCLS_OK && hist)  // no report => no slice histogram either
+    for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
   if (lane == 0 && status != SCLS_OK) {
     // A failed run has no report (the reference throws, metrics.cpp is never
     // reached): only the status and the offending request are defined.
@@ -1152,6 +1154,14 @@ __global__ void __launch_bounds__(kSimWarps * 32, POL == SCLS_POLICY_SCLS ? 4 : 
   if (g >= count) return;
   run_trace<POL, kHash, kLog>(p, list[g], lane, bins[warp], ssplit[POL == SCLS_POLICY_SCLS ? warp : 0]);
 }
+
+}  // namespace
+}  // namespace scls
+
+#include "sim_ils.cuh"
+
+namespace scls {
+namespace {
 
 // Σ_i ceil(min(gen_i, G) / S): the exact number of (request, slice) pairs a
 // SCLS run serves, i.e. the tick-log and batch capacity of the trace.
@@ -1475,6 +1485,7 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
   else sim_kernel<POLV, false, false><<<grid, kSimWarps * 32, 0, s>>>(p, l, cnt);
     if (pol == SCLS_POLICY_SCLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SCLS) }
     else if (pol == SCLS_POLICY_SLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SLS) }
+    else if (!want_log && !hash) sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, s>>>(p, l, cnt);
     else { SCLS_SIM_LAUNCH(SCLS_POLICY_ILS) }
 #undef SCLS_SIM_LAUNCH
     SCLS_LAUNCHED();

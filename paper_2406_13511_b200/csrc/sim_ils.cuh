@@ -1,0 +1,327 @@
+// sim_ils.cuh — lean metrics-only ILS simulator (included by sim.cu).
+//
+// The same semantics as run_trace<ILS> (reference sched_policies.cpp:275-391,
+// sim_engine.cpp:101-168, metrics.cpp:30-117) for the sweep path, where only
+// the report is needed (no digests, no event log).  ILS is the event-heaviest
+// policy (~309k boundaries per 600 s trace), so this kernel keeps only what
+// the report depends on: per-instance registers in lane w, running requests
+// as {id, join_iter, lim, inp} slots, the response array, and counters.  For
+// ILS every completion has exactly one slice and segment records carry no
+// members, so pad / invalid / early-return totals are identically zero.
+#pragma once
+
+namespace scls {
+namespace {
+
+__device__ void finish_report(int lane, scls_trace_result* R, int status, int n, int W, int completed,
+                              double first_arrival, double last_completion, double* resp, int32_t* bins,
+                              double last_end, long long total_pad, long long total_inv, long long batch_count,
+                              long long batch_members, long long early, long long n_events, long long n_disp,
+                              long long n_ticks, double clock) {
+  if (status == SCLS_OK && (n_events == 0 || completed == 0)) status = SCLS_ERR_EMPTY_LOG;
+  double thr = 0.0, avg = 0.0, p95 = 0.0, ctstd = 0.0;
+  if (status == SCLS_OK) {
+    const double span = last_completion - first_arrival;
+    const double comp = (double)completed;
+    thr = span > 0.0 ? __ddiv_rn(comp, span) : 0.0;
+    double sum = 0.0;
+    if (lane == 0)
+      for (int i = 0; i < completed; ++i) sum = __dadd_rn(sum, resp[i]);
+    sum = shfl_d(sum, 0);
+    avg = __ddiv_rn(sum, comp);
+    const size_t rk = (size_t)ceil(__dmul_rn(0.95, comp));
+    int want = (int)(rk > 1 ? rk : 1) - 1;
+    uint64_t prefix = 0;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = lane; i < 256; i += 32) bins[i] = 0;
+      __syncwarp();
+      const uint64_t hi_mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+      for (int i = lane; i < completed; i += 32) {
+        const uint64_t k = ordered_bits(resp[i]);
+        if ((k & hi_mask) == prefix) atomicAdd(&bins[(k >> shift) & 0xff], 1);
+      }
+      __syncwarp();
+      int digit = 0;
+      if (lane == 0) {
+        int acc = 0;
+        for (int d = 0; d < 256; ++d) {
+          if (acc + bins[d] > want) {
+            digit = d;
+            break;
+          }
+          acc += bins[d];
+        }
+        want -= acc;
+      }
+      digit = shfl_i(digit, 0);
+      want = shfl_i(want, 0);
+      prefix |= (uint64_t)digit << shift;
+      __syncwarp();
+    }
+    const uint64_t u = (prefix & 0x8000000000000000ull) ? (prefix & ~0x8000000000000000ull) : ~prefix;
+    p95 = __longlong_as_double((long long)u);
+    double mean = 0.0, var = 0.0;
+    for (int w = 0; w < W; ++w) mean = __dadd_rn(mean, shfl_d(last_end, w));
+    mean = __ddiv_rn(mean, (double)W);
+    for (int w = 0; w < W; ++w) {
+      const double d = __dadd_rn(shfl_d(last_end, w), -mean);
+      var = __dadd_rn(var, __dmul_rn(d, d));
+    }
+    var = __ddiv_rn(var, (double)W);
+    ctstd = __dsqrt_rn(var);
+  }
+  if (lane == 0) {
+    memset(R, 0, sizeof *R);
+    R->status = status;
+    R->worker_count = W;
+    R->error_request_id = -1;
+    R->n_requests = n;
+    if (status != SCLS_OK) return;
+    const double comp = (double)completed;
+    R->completed = completed;
+    R->throughput = thr;
+    R->avg_response_s = avg;
+    R->p95_response_s = p95;
+    R->ct_std_s = ctstd;
+    R->avg_pad_tokens = __ddiv_rn((double)total_pad, comp);
+    R->avg_invalid_tokens = __ddiv_rn((double)total_inv, comp);
+    R->avg_batch_size = batch_count > 0 ? __ddiv_rn((double)batch_members, (double)batch_count) : 0.0;
+    R->early_return_ratio = batch_count > 0 ? __ddiv_rn((double)early, (double)batch_count) : 0.0;
+    R->total_pad = total_pad;
+    R->total_invalid = total_inv;
+    R->batch_count = batch_count;
+    R->batch_members = batch_members;
+    R->early_returns = early;
+    R->n_events = n_events;
+    R->n_dispatches = n_disp;
+    R->n_ticks = n_ticks;
+    R->sim_clock = clock;
+  }
+}
+
+__global__ void __launch_bounds__(kSimWarps * 32, 8)
+    sim_ils_lean_kernel(SimParams P, const int32_t* __restrict__ list, int32_t count) {
+  __shared__ int32_t sbins[kSimWarps][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * kSimWarps + warp;
+  if (g >= count) return;
+  const int t = list[g];
+  int32_t* bins = sbins[warp];
+  const int64_t r0 = P.req_off[t];
+  const int n = (int)(P.req_off[t + 1] - r0);
+  const double* __restrict__ arr = P.arr + r0;
+  const int32_t* __restrict__ inp = P.inp + r0;
+  const int32_t* __restrict__ tg = P.tg + r0;
+  const int ci = P.cfg_index ? P.cfg_index[t] : 0;
+  const int W = P.cfgs[ci].W, MC = P.cfgs[ci].MC, G = P.cfgs[ci].G;
+  const double horizon = P.cfgs[ci].horizon;
+  const Lat& lat = P.lat;
+  scls_trace_result* R = &P.res[t];
+  int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
+
+  int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
+  if (status == SCLS_OK) {
+    int bad = 0;
+    for (int i = 1 + lane; i < n; i += 32) bad |= arr[i] < arr[i - 1];
+    if (__any_sync(FULL, bad)) status = SCLS_ERR_ERROR;
+  }
+  if (hist)
+    for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
+  if (status != SCLS_OK) {
+    finish_report(lane, R, status, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0);
+    return;
+  }
+  char* base = P.arena + P.trace_base[t];
+  const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_ILS, P.trace_cap[t], MC);
+  double* resp = (double*)(base + Lay.resp);
+  const int cap_w = (n + W - 1) / W;
+  int32_t* fifo_base = (int32_t*)(base + Lay.fifo);
+  int4* run_base = (int4*)(base + Lay.run);
+  int32_t* ex_base = (int32_t*)(base + Lay.ex);
+
+  // instance registers (lane w < W)
+  double ev_t = dinf(), last_end = 0.0;
+  unsigned long long ev_s = ~0ull;
+  int n_run = 0, boundary = 0, seg_n = 0, seg_lin = 0, seg_it = 0, it_cnt = 0, next_exit = 0, mctx = 0;
+  int seg_id = -1, f_head = 0, f_tail = 0;
+  // trace registers (uniform)
+  unsigned long long next_seq = (unsigned long long)n + 1;
+  double clock = 0.0, next_arr = n > 0 ? arr[0] : dinf();
+  double first_arrival = dinf(), last_completion = -dinf();
+  int cur = 0, completed = 0, rr = 0, next_batch = 0;
+  long long batch_count = 0, batch_members = 0, n_events = 0, n_disp = 0;
+  const unsigned lt = (1u << lane) - 1u;
+
+  while (completed < n) {
+    // ---- fast lane: unchanged iterations (see run_trace<ILS>) -------------------
+    {
+      const bool has = lane < W && ev_t != dinf();
+      uint64_t key = has ? ordered_bits(ev_t) : ~0ull;
+      bool mine_fast = has && n_run > 0 && it_cnt + 1 < next_exit && !(f_tail > f_head && n_run < MC);
+      const double dn = (double)n_run;
+      const double a1 = __dmul_rn(lat.d1, dn), a2 = __dmul_rn(lat.d2, dn);
+      for (;;) {
+        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+        const unsigned mh = __reduce_min_sync(FULL, hi);
+        const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
+        const unsigned tie = __ballot_sync(FULL, hi == mh && lo == ml);
+        if (tie & (tie - 1u)) break;
+        const int w = __ffs(tie) - 1;
+        const uint64_t kmin = ((uint64_t)mh << 32) | ml;
+        if (kmin == ~0ull) break;
+        const double bt = __longlong_as_double(
+            (long long)((kmin & 0x8000000000000000ull) ? (kmin & ~0x8000000000000000ull) : ~kmin));
+        if (next_arr <= fmin(bt, horizon) || horizon <= bt) break;
+        if (!((__ballot_sync(FULL, mine_fast) >> w) & 1u)) break;
+        clock = bt;
+        if (lane == w) {
+          it_cnt += 1;
+          seg_it += 1;
+          mctx += 1;
+          const double dl = (double)mctx;
+          const double it = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a1, dl), a2), __dmul_rn(lat.d3, dl)), lat.d4);
+          ev_t = __dadd_rn(bt, it);
+          ev_s = next_seq;
+          key = ordered_bits(ev_t);
+          mine_fast = it_cnt + 1 < next_exit;
+        }
+        ++next_seq;
+      }
+    }
+    // ---- general step ----------------------------------------------------------------
+    double na_t;
+    unsigned long long na_s;
+    const int na_w = argmin_event_redux(ev_t, ev_s, lane < W && ev_t != dinf(), lane, &na_t, &na_s);
+    if (next_arr <= fmin(na_t, horizon)) {  // arrival (seq < n): sched_policies.cpp:279-290
+      const int id = cur++;
+      clock = next_arr;
+      next_arr = cur < n ? arr[cur] : dinf();
+      if (first_arrival == dinf()) first_arrival = clock;
+      ++n_events;
+      const int w = rr;
+      rr = rr + 1 == W ? 0 : rr + 1;
+      const bool wake = shfl_i(n_run == 0 && !boundary, w);  // idle instance: boundary at `clock`
+      if (lane == w) {
+        fifo_base[(int64_t)w * cap_w + f_tail] = id;
+        ++f_tail;
+        if (wake) {
+          ev_t = clock;
+          ev_s = next_seq;
+          boundary = 1;
+        }
+      }
+      if (wake) ++next_seq;
+      continue;
+    }
+    if (horizon <= na_t) {  // EndOfRun precedes every later event
+      status = SCLS_ERR_NON_TERMINATION;
+      break;
+    }
+    // ---- an instance boundary with a membership change (sched_policies.cpp:292-391)
+    const int w = na_w;
+    clock = na_t;
+    const double now = clock;
+    int4* run = run_base + (int64_t)w * MC;
+    const int32_t* wq = fifo_base + (int64_t)w * cap_w;
+    const int nr = shfl_i(n_run, w);
+    const int it1 = shfl_i(it_cnt, w) + (nr > 0 ? 1 : 0);
+    const int head = shfl_i(f_head, w), tail = shfl_i(f_tail, w);
+    if (lane == w) {
+      ev_t = dinf();
+      ev_s = ~0ull;
+      if (nr > 0) {
+        it_cnt = it1;
+        seg_it += 1;
+      }
+    }
+    int nexit = 0, keep = 0;
+    for (int b0 = 0; b0 < nr; b0 += 32) {
+      const int i = b0 + lane;
+      const bool ok = i < nr;
+      int4 v = make_int4(0, 0, 0, 0);
+      bool ex = false;
+      if (ok) {
+        v = run[i];
+        ex = it1 - v.y >= v.z;
+      }
+      const unsigned em = __ballot_sync(FULL, ok && ex);
+      const unsigned km = __ballot_sync(FULL, ok && !ex);
+      __syncwarp();
+      if (ok && ex) ex_base[nexit + __popc(em & lt)] = v.x;
+      if (ok && !ex) run[keep + __popc(km & lt)] = v;
+      nexit += __popc(em);
+      keep += __popc(km);
+      __syncwarp();
+    }
+    const int njoin = min(MC - keep, tail - head);
+    for (int j = lane; j < njoin; j += 32) {
+      const int id = wq[head + j];
+      run[keep + j] = make_int4(id, it1, min(tg[id], G), inp[id]);
+    }
+    __syncwarp();
+    const int nr_new = keep + njoin;
+    if (lane == w) {
+      f_head = head + njoin;
+      n_run = nr_new;
+    }
+    const bool changed = nexit > 0 || njoin > 0;
+    if (changed && shfl_i(seg_id, w) >= 0 && shfl_i(seg_it, w) > 0) {  // batch_end record
+      ++batch_count;
+      batch_members += shfl_i(seg_n, w);
+      ++n_events;
+      if (lane == w) {
+        seg_id = -1;
+        last_end = fmax(last_end, now);
+      }
+    }
+    for (int c0 = 0; c0 < nexit; c0 += 32) {  // completions, member order
+      const int cnt = min(32, nexit - c0);
+      if (lane < cnt) resp[completed + lane] = now - arr[ex_base[c0 + lane]];
+      completed += cnt;
+      n_events += cnt;
+      last_completion = now;
+    }
+    __syncwarp();
+    if (nr_new == 0) {
+      if (lane == w) boundary = 0;
+      continue;
+    }
+    int mc = 0, nx = 0x7fffffff;
+    for (int i = lane; i < nr_new; i += 32) {
+      const int4 v = run[i];
+      mc = max(mc, v.w + (it1 - v.y));
+      nx = min(nx, v.y + v.z);
+    }
+    mc = __reduce_max_sync(FULL, mc);
+    nx = __reduce_min_sync(FULL, nx);
+    if (changed) {  // batch_start record
+      ++n_events;
+      if (lane == w) {
+        seg_id = next_batch;
+        seg_n = nr_new;
+        seg_lin = mc;
+        seg_it = 0;
+      }
+      ++next_batch;
+    }
+    double it = decode_step_time(lat, mc, nr_new);
+    for (int j = 0; j < njoin; ++j) it = __dadd_rn(it, prefill_time(lat, 1, run[keep + j].w));
+    n_disp += njoin;
+    n_events += njoin;
+    if (lane == w) {
+      mctx = mc;
+      next_exit = nx;
+      ev_t = __dadd_rn(now, it);
+      ev_s = next_seq;
+      boundary = 1;
+    }
+    ++next_seq;
+  }
+  (void)seg_lin;
+  if (hist && status == SCLS_OK && P.hist_bins > 1 && lane == 0) hist[1] = completed;
+  finish_report(lane, R, status, n, W, completed, first_arrival, last_completion, resp, bins, last_end, 0, 0,
+                batch_count, batch_members, 0, n_events, n_disp, 0, clock);
+}
+
+}  // namespace
+}  // namespace scls

@@ -196,3 +196,32 @@ def test_c4_scale_trace(ctx, orc):
     for i in range(len(cfgs)):
         assert_results_equal(a[i], b[i], i)
     assert np.array_equal(ha, hb)
+
+
+def test_metrics_only_path_vs_oracle(ctx, orc):
+    """Digests off selects the lean metrics-only kernels (the sweep/bench path):
+    every report field must still match the oracle bit for bit."""
+    lat = capi.builtin_latency_model()
+    rng = np.random.default_rng(77)
+    traces, cfgs = [], []
+    for trial in range(48):
+        pol = ("ils", "scls", "sls")[trial % 3]
+        traces.append(orc.generate(capi.workload_spec(rate=float(rng.uniform(2, 30)),
+                                                      duration_s=float(rng.uniform(10, 90)), seed=3000 + trial)))
+        cfgs.append(capi.sched_cfg(policy=pol, worker_count=int(rng.integers(1, 33)),
+                                   slice_len=int(rng.choice([16, 64, 128])), max_gen_limit=1024,
+                                   fixed_batch_size=int(rng.integers(1, 30)),
+                                   max_concurrent=int(rng.integers(1, 40)),
+                                   horizon_s=1e7 if trial % 7 else 20.0))
+    idx = list(range(len(cfgs)))
+    ctx.set_digests(False)
+    try:
+        a, ha = ctx.simulate(traces, cfgs, lat, MEMORIES["rule"](), cfg_index=idx)
+    finally:
+        ctx.set_digests(True)
+    b, hb = orc.simulate(traces, cfgs, lat, MEMORIES["rule"](), cfg_index=idx)
+    for t in range(len(traces)):
+        for f in FIELDS:
+            if not f.startswith("h_"):
+                assert getattr(a[t], f) == getattr(b[t], f), (t, cfgs[t].policy, f)
+    assert np.array_equal(ha, hb)
