@@ -141,9 +141,10 @@ SCLS_DEV int max_batch_size(const Mem& m, int l_in, int slice) {
 // canonicalised to +0.0 because the reference compares with `<`, under which
 // the two are equal (batcher.cpp:35-38, offloader.cpp:34-37).
 SCLS_DEV uint64_t ordered_bits(double x) {
-  if (x == 0.0) x = 0.0;
-  const uint64_t u = (uint64_t)__double_as_longlong(x);
-  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+  // -0.0 and +0.0 share a key; negatives flip every bit, others only the sign.
+  const uint64_t u = x == 0.0 ? 0ull : (uint64_t)__double_as_longlong(x);
+  const uint64_t m = (uint64_t)((int64_t)u >> 63);
+  return u ^ (m | 0x8000000000000000ull);
 }
 
 }  // namespace scls

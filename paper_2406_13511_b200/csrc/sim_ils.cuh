@@ -13,6 +13,64 @@
 namespace scls {
 namespace {
 
+__device__ __forceinline__ unsigned opaque_u32(unsigned x) {
+  unsigned y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ double opaque_f64(double x) {
+  double y;
+  asm volatile("mov.b64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// Keys of event times: with every time provably positive (see `pos` in the
+// kernel) the raw IEEE bits already order them, otherwise ordered_bits().
+template <bool kPos>
+__device__ __forceinline__ uint64_t time_key(double t) {
+  return kPos ? (uint64_t)__double_as_longlong(t) : ordered_bits(t);
+}
+
+template <bool kPos>
+__device__ __forceinline__ void ils_fast_run(int lane, int W, int MC, double next_arr, double horizon, const Lat& lat,
+                                             int n_run, int f_head, int f_tail, int next_exit, int& it_cnt,
+                                             int& seg_it, int& mctx, double& ev_t, unsigned& ev_s,
+                                             unsigned& next_seq) {
+  const bool has = lane < W && ev_t != dinf();
+  uint64_t key = has ? time_key<kPos>(ev_t) : ~0ull;
+  bool mine_fast = has && n_run > 0 && it_cnt + 1 < next_exit && !(f_tail > f_head && n_run < MC);
+  const uint64_t limit = time_key<kPos>(fmin(next_arr, horizon));
+  // Opaque copies: at the 64-register cap the compiler would otherwise
+  // rematerialise these (S2R + shift, I2F + 2 DMUL) on every iteration.
+  const unsigned lbit = opaque_u32(1u << lane);
+  const double dn = (double)n_run;
+  const double a1 = opaque_f64(__dmul_rn(lat.d1, dn)), a2 = opaque_f64(__dmul_rn(lat.d2, dn));
+  auto step = [&](int ctx) {
+    const double dl = (double)ctx;
+    return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a1, dl), a2), __dmul_rn(lat.d3, dl)), lat.d4);
+  };
+  double it_next = step(mctx + 1);
+  for (;;) {
+    const unsigned fm = __ballot_sync(FULL, mine_fast);
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mh = __reduce_min_sync(FULL, hi);
+    const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
+    const unsigned tie = __ballot_sync(FULL, hi == mh && lo == ml);
+    if ((tie & (tie - 1u)) | !(fm & tie) | ((((uint64_t)mh << 32) | ml) >= limit)) break;
+    if (tie == lbit) {
+      it_cnt += 1;
+      seg_it += 1;
+      mctx += 1;
+      ev_t = __dadd_rn(ev_t, it_next);
+      ev_s = next_seq;
+      key = time_key<kPos>(ev_t);
+      mine_fast = it_cnt + 1 < next_exit;
+      it_next = step(mctx + 1);
+    }
+    ++next_seq;
+  }
+}
+
 __device__ void finish_report(int lane, scls_trace_result* R, int status, int n, int W, int completed,
                               double first_arrival, double last_completion, double* resp, int32_t* bins,
                               double last_end, long long total_pad, long long total_inv, long long batch_count,
@@ -141,62 +199,50 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
 
   // instance registers (lane w < W)
   double ev_t = dinf(), last_end = 0.0;
-  unsigned long long ev_s = ~0ull;
+  unsigned ev_s = ~0u;
   int n_run = 0, boundary = 0, seg_n = 0, seg_lin = 0, seg_it = 0, it_cnt = 0, next_exit = 0, mctx = 0;
   int seg_id = -1, f_head = 0, f_tail = 0;
   // trace registers (uniform)
-  unsigned long long next_seq = (unsigned long long)n + 1;
-  double clock = 0.0, next_arr = n > 0 ? arr[0] : dinf();
-  double first_arrival = dinf(), last_completion = -dinf();
+  // 32-bit event sequence: one push per event, so it wraps only after 2^32 - n
+  // events in one trace (far beyond any horizon the sweep configurations use).
+  unsigned next_seq = (unsigned)n + 1u;
+  // The first arrival event is arr[0] and the last event of a finished run is
+  // its last completion, so neither first_arrival nor the clock is carried.
+  double next_arr = n > 0 ? arr[0] : dinf();
+  double last_completion = -dinf();
   int cur = 0, completed = 0, rr = 0, next_batch = 0;
-  long long batch_count = 0, batch_members = 0, n_events = 0, n_disp = 0;
+  unsigned batch_count = 0, n_disp = 0;  // <= 2n and <= n
+  long long batch_members = 0, n_events = 0;
   const unsigned lt = (1u << lane) - 1u;
+  // Every event time is positive when arrivals are, the horizon is, and each
+  // step time is (nonnegative coefficients with d2 or d4 positive: a boundary
+  // always has n >= 1 running).  Then raw IEEE bits order the times.
+  const bool pos = n > 0 && arr[0] > 0.0 && horizon > 0.0 && lat.p1 >= 0.0 && lat.p2 >= 0.0 && lat.p3 >= 0.0 &&
+                   lat.p4 >= 0.0 && lat.d1 >= 0.0 && lat.d2 >= 0.0 && lat.d3 >= 0.0 && lat.d4 >= 0.0 &&
+                   (lat.d2 > 0.0 || lat.d4 > 0.0);
 
   while (completed < n) {
     // ---- fast lane: unchanged iterations (see run_trace<ILS>) -------------------
-    {
-      const bool has = lane < W && ev_t != dinf();
-      uint64_t key = has ? ordered_bits(ev_t) : ~0ull;
-      bool mine_fast = has && n_run > 0 && it_cnt + 1 < next_exit && !(f_tail > f_head && n_run < MC);
-      const double dn = (double)n_run;
-      const double a1 = __dmul_rn(lat.d1, dn), a2 = __dmul_rn(lat.d2, dn);
-      for (;;) {
-        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
-        const unsigned mh = __reduce_min_sync(FULL, hi);
-        const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
-        const unsigned tie = __ballot_sync(FULL, hi == mh && lo == ml);
-        if (tie & (tie - 1u)) break;
-        const int w = __ffs(tie) - 1;
-        const uint64_t kmin = ((uint64_t)mh << 32) | ml;
-        if (kmin == ~0ull) break;
-        const double bt = __longlong_as_double(
-            (long long)((kmin & 0x8000000000000000ull) ? (kmin & ~0x8000000000000000ull) : ~kmin));
-        if (next_arr <= fmin(bt, horizon) || horizon <= bt) break;
-        if (!((__ballot_sync(FULL, mine_fast) >> w) & 1u)) break;
-        clock = bt;
-        if (lane == w) {
-          it_cnt += 1;
-          seg_it += 1;
-          mctx += 1;
-          const double dl = (double)mctx;
-          const double it = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a1, dl), a2), __dmul_rn(lat.d3, dl)), lat.d4);
-          ev_t = __dadd_rn(bt, it);
-          ev_s = next_seq;
-          key = ordered_bits(ev_t);
-          mine_fast = it_cnt + 1 < next_exit;
-        }
-        ++next_seq;
-      }
-    }
+    // While no instance changes membership, the next arrival and the horizon are
+    // fixed, so one precomputed key bounds the run: the loop stops at the first
+    // event at or past min(next arrival, horizon) (arrivals win ties), at a time
+    // tie between instances, or when the winner's next boundary changes
+    // membership.  The tie mask doubles as the winner's lane bit.  The winner's
+    // next step time is computed one iteration ahead, off the critical path.
+    if (pos)
+      ils_fast_run<true>(lane, W, MC, next_arr, horizon, lat, n_run, f_head, f_tail, next_exit, it_cnt, seg_it,
+                         mctx, ev_t, ev_s, next_seq);
+    else
+      ils_fast_run<false>(lane, W, MC, next_arr, horizon, lat, n_run, f_head, f_tail, next_exit, it_cnt, seg_it,
+                          mctx, ev_t, ev_s, next_seq);
     // ---- general step ----------------------------------------------------------------
     double na_t;
     unsigned long long na_s;
     const int na_w = argmin_event_redux(ev_t, ev_s, lane < W && ev_t != dinf(), lane, &na_t, &na_s);
     if (next_arr <= fmin(na_t, horizon)) {  // arrival (seq < n): sched_policies.cpp:279-290
       const int id = cur++;
-      clock = next_arr;
+      const double clock = next_arr;
       next_arr = cur < n ? arr[cur] : dinf();
-      if (first_arrival == dinf()) first_arrival = clock;
       ++n_events;
       const int w = rr;
       rr = rr + 1 == W ? 0 : rr + 1;
@@ -219,8 +265,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
     }
     // ---- an instance boundary with a membership change (sched_policies.cpp:292-391)
     const int w = na_w;
-    clock = na_t;
-    const double now = clock;
+    const double now = na_t;
     int4* run = run_base + (int64_t)w * MC;
     const int32_t* wq = fifo_base + (int64_t)w * cap_w;
     const int nr = shfl_i(n_run, w);
@@ -228,7 +273,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
     const int head = shfl_i(f_head, w), tail = shfl_i(f_tail, w);
     if (lane == w) {
       ev_t = dinf();
-      ev_s = ~0ull;
+      ev_s = ~0u;
       if (nr > 0) {
         it_cnt = it1;
         seg_it += 1;
@@ -319,8 +364,8 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
   }
   (void)seg_lin;
   if (hist && status == SCLS_OK && P.hist_bins > 1 && lane == 0) hist[1] = completed;
-  finish_report(lane, R, status, n, W, completed, first_arrival, last_completion, resp, bins, last_end, 0, 0,
-                batch_count, batch_members, 0, n_events, n_disp, 0, clock);
+  finish_report(lane, R, status, n, W, completed, n > 0 ? arr[0] : dinf(), last_completion, resp, bins, last_end, 0,
+                0, batch_count, batch_members, 0, n_events, n_disp, 0, last_completion);
 }
 
 }  // namespace

@@ -225,3 +225,44 @@ def test_metrics_only_path_vs_oracle(ctx, orc):
             if not f.startswith("h_"):
                 assert getattr(a[t], f) == getattr(b[t], f), (t, cfgs[t].policy, f)
     assert np.array_equal(ha, hb)
+
+
+def test_metrics_only_edge_times(ctx, orc):
+    """The lean ILS kernel keys event times by raw IEEE bits only when every
+    time is provably positive; zero / negative arrivals, models whose step
+    time may be zero, and exact time ties (duplicate arrivals, integer-valued
+    models) must take the general key path or the tie-break and still match."""
+    base = orc.generate(capi.workload_spec(rate=12.0, duration_s=40.0, seed=4242))
+    arr, inp, gen = (np.asarray(x) for x in base)
+    dup = np.repeat(arr[: len(arr) // 2], 2)
+    n2 = len(dup)
+    variants = {
+        "zero_start": (arr - arr[0], inp, gen),
+        "negative": (arr - 5.0, inp, gen),
+        "duplicates": (dup, inp[:n2], gen[:n2]),
+        "plain": (arr, inp, gen),
+    }
+    lats = {
+        "builtin": capi.builtin_latency_model(),
+        "no_const": capi.latency_model(p1=2e-6, p3=5e-5, d1=1e-7, d3=3e-6),
+        "integer": capi.latency_model(p4=1.0, d4=1.0),
+        "neg_coeff": capi.latency_model(p4=0.02, d3=3e-6, d4=0.02, d2=-1e-5),
+    }
+    for lname, lat in lats.items():
+        traces, cfgs = [], []
+        for vname, tr in variants.items():
+            for pol in ("ils", "scls", "sls"):
+                traces.append(tuple(np.ascontiguousarray(x) for x in tr))
+                cfgs.append(capi.sched_cfg(policy=pol, worker_count=4, max_concurrent=6, fixed_batch_size=6))
+        idx = list(range(len(cfgs)))
+        ctx.set_digests(False)
+        try:
+            a, ha = ctx.simulate(traces, cfgs, lat, MEMORIES["rule"](), cfg_index=idx)
+        finally:
+            ctx.set_digests(True)
+        b, hb = orc.simulate(traces, cfgs, lat, MEMORIES["rule"](), cfg_index=idx)
+        for t in range(len(traces)):
+            for f in FIELDS:
+                if not f.startswith("h_"):
+                    assert getattr(a[t], f) == getattr(b[t], f), (lname, t, cfgs[t].policy, f)
+        assert np.array_equal(ha, hb), lname
