@@ -31,44 +31,94 @@ __device__ __forceinline__ uint64_t time_key(double t) {
   return kPos ? (uint64_t)__double_as_longlong(t) : ordered_bits(t);
 }
 
+// Push order of pending events.  The reference orders simultaneous events by
+// a global sequence number taken at push time (sim_engine.cpp:101-168).  The
+// lean kernel processes several independent boundaries per step ("rounds",
+// below), so it records the push order as (round, key of the pushing event):
+// rounds are processed in order, one push per lane per round, and within a
+// round the pushing events have distinct times processed in time order --
+// the same total order as the reference's counter.
+struct PushOrder {
+  unsigned round;
+  uint64_t pkey;
+};
+
+// Fast rounds: membership of every instance is fixed until the next arrival
+// (or the horizon), so each instance's boundaries follow from its own state.
+// With bound = min(limit, every fast instance's SECOND boundary, every other
+// instance's pending event), all fast pending events before `bound` are the
+// next events in the reference's global order (each push lands at or after
+// `bound`), and they are processed together.  A round stops the run when it
+// is empty (the next event is an arrival, the horizon, a membership change
+// or needs the tie-break) or when two of its events share a time.
 template <bool kPos>
-__device__ __forceinline__ void ils_fast_run(int lane, int W, int MC, double next_arr, double horizon, const Lat& lat,
-                                             int n_run, int f_head, int f_tail, int next_exit, int& it_cnt,
-                                             int& seg_it, int& mctx, double& ev_t, unsigned& ev_s,
-                                             unsigned& next_seq) {
+__device__ __forceinline__ void ils_fast_rounds(int lane, int W, int MC, double next_arr, double horizon,
+                                                const Lat& lat, int n_run, int f_head, int f_tail, int next_exit,
+                                                int& it_cnt, int& seg_it, int& mctx, double& ev_t, PushOrder& po,
+                                                unsigned& round_ctr) {
   const bool has = lane < W && ev_t != dinf();
-  uint64_t key = has ? time_key<kPos>(ev_t) : ~0ull;
-  bool mine_fast = has && n_run > 0 && it_cnt + 1 < next_exit && !(f_tail > f_head && n_run < MC);
+  bool fast = has && n_run > 0 && it_cnt + 1 < next_exit && !(f_tail > f_head && n_run < MC);
   const uint64_t limit = time_key<kPos>(fmin(next_arr, horizon));
   // Opaque copies: at the 64-register cap the compiler would otherwise
-  // rematerialise these (S2R + shift, I2F + 2 DMUL) on every iteration.
-  const unsigned lbit = opaque_u32(1u << lane);
+  // rematerialise these (I2F + 2 DMUL) on every round.
   const double dn = (double)n_run;
   const double a1 = opaque_f64(__dmul_rn(lat.d1, dn)), a2 = opaque_f64(__dmul_rn(lat.d2, dn));
   auto step = [&](int ctx) {
     const double dl = (double)ctx;
     return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a1, dl), a2), __dmul_rn(lat.d3, dl)), lat.d4);
   };
-  double it_next = step(mctx + 1);
+  uint64_t key = has ? time_key<kPos>(ev_t) : ~0ull;
+  double tnext = __dadd_rn(ev_t, step(mctx + 1));
   for (;;) {
-    const unsigned fm = __ballot_sync(FULL, mine_fast);
-    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
-    const unsigned mh = __reduce_min_sync(FULL, hi);
-    const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
-    const unsigned tie = __ballot_sync(FULL, hi == mh && lo == ml);
-    if ((tie & (tie - 1u)) | !(fm & tie) | ((((uint64_t)mh << 32) | ml) >= limit)) break;
-    if (tie == lbit) {
+    const uint64_t cand = fast ? time_key<kPos>(tnext) : key;
+    const unsigned ch = (unsigned)(cand >> 32), cl = (unsigned)cand;
+    const unsigned mh = __reduce_min_sync(FULL, ch);
+    const unsigned ml = __reduce_min_sync(FULL, ch == mh ? cl : 0xffffffffu);
+    const uint64_t m = ((uint64_t)mh << 32) | ml;
+    const uint64_t bound = m < limit ? m : limit;
+    const bool in = fast && key < bound;
+    const unsigned S = __ballot_sync(FULL, in);
+    if (!S) break;
+    if (S & (S - 1u)) {  // distinct sentinels: keys in the round are < limit < ~lane
+      const unsigned same = __match_any_sync(FULL, in ? key : ~(uint64_t)lane);
+      if (__any_sync(FULL, same & (same - 1u))) break;
+    }
+    if (in) {
       it_cnt += 1;
       seg_it += 1;
       mctx += 1;
-      ev_t = __dadd_rn(ev_t, it_next);
-      ev_s = next_seq;
+      po.round = round_ctr;
+      po.pkey = key;
+      ev_t = tnext;
       key = time_key<kPos>(ev_t);
-      mine_fast = it_cnt + 1 < next_exit;
-      it_next = step(mctx + 1);
+      fast = it_cnt + 1 < next_exit;
+      tnext = __dadd_rn(ev_t, step(mctx + 1));
     }
-    ++next_seq;
+    ++round_ctr;
   }
+}
+
+// Earliest pending instance event by (time, push order); the reference's
+// queue order (sim_engine.cpp:101-168).  Returns the lane, -1 if none.
+__device__ __forceinline__ int argmin_pending(double ev_t, const PushOrder& po, bool has, int lane, double* bt) {
+  const uint64_t key = has ? ordered_bits(ev_t) : ~0ull;
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mh = __reduce_min_sync(FULL, hi);
+  const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xffffffffu);
+  unsigned tie = __ballot_sync(FULL, hi == mh && lo == ml);
+  if (tie & (tie - 1u)) {
+    bool in = (tie >> lane) & 1u;
+    const unsigned r = __reduce_min_sync(FULL, in ? po.round : 0xffffffffu);
+    in = in && po.round == r;
+    const unsigned ph = (unsigned)(po.pkey >> 32), pl = (unsigned)po.pkey;
+    const unsigned mph = __reduce_min_sync(FULL, in ? ph : 0xffffffffu);
+    in = in && ph == mph;
+    const unsigned mpl = __reduce_min_sync(FULL, in ? pl : 0xffffffffu);
+    tie = __ballot_sync(FULL, in && pl == mpl);
+  }
+  const int w = __ffs(tie) - 1;
+  *bt = shfl_d(has ? ev_t : dinf(), w);
+  return w;
 }
 
 __device__ void finish_report(int lane, scls_trace_result* R, int status, int n, int W, int completed,
@@ -199,13 +249,13 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
 
   // instance registers (lane w < W)
   double ev_t = dinf(), last_end = 0.0;
-  unsigned ev_s = ~0u;
+  PushOrder po = {~0u, ~0ull};
   int n_run = 0, boundary = 0, seg_n = 0, seg_lin = 0, seg_it = 0, it_cnt = 0, next_exit = 0, mctx = 0;
   int seg_id = -1, f_head = 0, f_tail = 0;
   // trace registers (uniform)
-  // 32-bit event sequence: one push per event, so it wraps only after 2^32 - n
-  // events in one trace (far beyond any horizon the sweep configurations use).
-  unsigned next_seq = (unsigned)n + 1u;
+  // Round counter of PushOrder: one round per processed step, so it wraps only
+  // after 2^32 steps of one trace (far beyond any horizon the sweeps use).
+  unsigned round_ctr = 0;
   // The first arrival event is arr[0] and the last event of a finished run is
   // its last completion, so neither first_arrival nor the clock is carried.
   double next_arr = n > 0 ? arr[0] : dinf();
@@ -230,15 +280,14 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
     // membership.  The tie mask doubles as the winner's lane bit.  The winner's
     // next step time is computed one iteration ahead, off the critical path.
     if (pos)
-      ils_fast_run<true>(lane, W, MC, next_arr, horizon, lat, n_run, f_head, f_tail, next_exit, it_cnt, seg_it,
-                         mctx, ev_t, ev_s, next_seq);
+      ils_fast_rounds<true>(lane, W, MC, next_arr, horizon, lat, n_run, f_head, f_tail, next_exit, it_cnt, seg_it,
+                            mctx, ev_t, po, round_ctr);
     else
-      ils_fast_run<false>(lane, W, MC, next_arr, horizon, lat, n_run, f_head, f_tail, next_exit, it_cnt, seg_it,
-                          mctx, ev_t, ev_s, next_seq);
+      ils_fast_rounds<false>(lane, W, MC, next_arr, horizon, lat, n_run, f_head, f_tail, next_exit, it_cnt, seg_it,
+                             mctx, ev_t, po, round_ctr);
     // ---- general step ----------------------------------------------------------------
     double na_t;
-    unsigned long long na_s;
-    const int na_w = argmin_event_redux(ev_t, ev_s, lane < W && ev_t != dinf(), lane, &na_t, &na_s);
+    const int na_w = argmin_pending(ev_t, po, lane < W && ev_t != dinf(), lane, &na_t);
     if (next_arr <= fmin(na_t, horizon)) {  // arrival (seq < n): sched_policies.cpp:279-290
       const int id = cur++;
       const double clock = next_arr;
@@ -252,11 +301,12 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
         ++f_tail;
         if (wake) {
           ev_t = clock;
-          ev_s = next_seq;
+          po.round = round_ctr;
+          po.pkey = 0;
           boundary = 1;
         }
       }
-      if (wake) ++next_seq;
+      if (wake) ++round_ctr;
       continue;
     }
     if (horizon <= na_t) {  // EndOfRun precedes every later event
@@ -273,7 +323,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
     const int head = shfl_i(f_head, w), tail = shfl_i(f_tail, w);
     if (lane == w) {
       ev_t = dinf();
-      ev_s = ~0u;
+      po.round = ~0u;
       if (nr > 0) {
         it_cnt = it1;
         seg_it += 1;
@@ -357,10 +407,11 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
       mctx = mc;
       next_exit = nx;
       ev_t = __dadd_rn(now, it);
-      ev_s = next_seq;
+      po.round = round_ctr;
+      po.pkey = 0;
       boundary = 1;
     }
-    ++next_seq;
+    ++round_ctr;
   }
   (void)seg_lin;
   if (hist && status == SCLS_OK && P.hist_bins > 1 && lane == 0) hist[1] = completed;
