@@ -79,9 +79,20 @@ __device__ __forceinline__ void ils_fast_rounds(int lane, int W, int MC, double 
     const bool in = fast && key < bound;
     const unsigned S = __ballot_sync(FULL, in);
     if (!S) break;
-    if (S & (S - 1u)) {  // distinct sentinels: keys in the round are < limit < ~lane
-      const unsigned same = __match_any_sync(FULL, in ? key : ~(uint64_t)lane);
-      if (__any_sync(FULL, same & (same - 1u))) break;
+    if (S & (S - 1u)) {
+      // Distinct keys are certified by a bucket mask over low key bits with
+      // one bucket per member (cheap REDUX.OR); only an inconclusive mask
+      // pays for the exact MATCH (distinct sentinels: keys in the round are
+      // < limit < ~lane).
+      const unsigned lo = (unsigned)key, ns = __popc(S);
+      const unsigned b1 = __reduce_or_sync(FULL, in ? 1u << (lo & 31u) : 0u);
+      if (__popc(b1) != ns) {
+        const unsigned b2 = __reduce_or_sync(FULL, in ? 1u << ((lo >> 5) & 31u) : 0u);
+        if (__popc(b2) != ns) {
+          const unsigned same = __match_any_sync(FULL, in ? key : ~(uint64_t)lane);
+          if (__any_sync(FULL, same & (same - 1u))) break;
+        }
+      }
     }
     if (in) {
       it_cnt += 1;
