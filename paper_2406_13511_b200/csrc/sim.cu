@@ -35,7 +35,13 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kSimWarps = 4;  // traces per CTA
-constexpr int kSplitSmem = 2048;
+#ifndef SCLS_SPLIT_SMEM
+#define SCLS_SPLIT_SMEM 256
+#endif
+#ifndef SCLS_SIM_MINB
+#define SCLS_SIM_MINB 7
+#endif
+constexpr int kSplitSmem = SCLS_SPLIT_SMEM;
 
 struct SimCfg {
   int32_t policy, S, G, B, MC, W;
@@ -275,7 +281,7 @@ __device__ __forceinline__ int bits_of(uint32_t x) { return x ? 32 - __clz(x) : 
 // ---- the per-trace simulation -------------------------------------------------------
 
 template <int POL, bool kHash, bool kLog>
-__device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, int32_t* ssplit) {
+__device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, int32_t* ssplit, double* sT) {
   const int64_t r0 = P.req_off[t];
   const int n = (int)(P.req_off[t + 1] - r0);
   const double* __restrict__ arr = P.arr + r0;
@@ -496,10 +502,15 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         err_req = tlog[tl_pos + bad];
         return SCLS_ERR_INFEASIBLE_REQUEST;
       }
-      // 3. the DP (batcher.cpp:48-67): tiles of 32 rows, far+mid then the chain
-      int32_t* split = P_ <= kSplitSmem ? ssplit : split_g;
+      // 3. the DP (batcher.cpp:48-67): tiles of 32 rows, far+mid then the chain.
+      //    T and split live in this warp's shared memory when the pool fits.
+      //    Cost loads are issued ahead of the dependent adds (4-wide batches
+      //    in the far part, a 2-deep pipeline along the chain).
+      const bool small = P_ <= kSplitSmem;
+      int32_t* split = small ? ssplit : split_g;
+      double* T = small ? sT : Tg;
       if (lane == 0) {
-        Tg[0] = 0.0;
+        T[0] = 0.0;
         split[0] = 0;
       }
       __syncwarp();
@@ -508,40 +519,66 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         const int r = tb + 1 + lane;
         const bool valid = r <= P_;
         const int L = valid ? sv[r - 1] : 0;
-        const int Wr = valid ? min(Kt[L], r) : 0;
-        const int cb = valid ? coff[L] - 1 : 0;
+        const int Wr = valid ? min(__ldg(Kt + L), r) : 0;
+        const double* crow = cost + (valid ? __ldg(coff + L) - 1 : 0);
         double acc = kInf;
         int kb = 0;
         const int wmax = __reduce_max_sync(FULL, Wr);
         // candidates with j <= tb, ascending j (k descending)
-        for (int j = max(0, tb + 1 - wmax); j <= tb; ++j) {
-          const double Tj = Tg[j];
+        int j = max(0, tb + 1 - wmax);
+        for (; j + 3 <= tb; j += 4) {
+          double tv[4], cv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = r - (j + u);
+            tv[u] = T[j + u];
+            cv[u] = k <= Wr ? __ldg(crow + k) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = r - (j + u);
+            if (k <= Wr) {
+              const double cand = __dadd_rn(tv[u], cv[u]);
+              if (cand <= acc) {
+                acc = cand;
+                kb = k;
+              }
+            }
+          }
+        }
+        for (; j <= tb; ++j) {
+          const double Tj = T[j];
           const int k = r - j;
           if (k <= Wr) {
-            const double cand = __dadd_rn(Tj, cost[cb + k]);
+            const double cand = __dadd_rn(Tj, __ldg(crow + k));
             if (cand <= acc) {
               acc = cand;
               kb = k;
             }
           }
         }
-        // the in-tile chain
-        double Tj = Tg[tb];
+        // the in-tile chain: row tb+s finalises at step s-1 (lane s-1) after
+        // T[tb+s-1] arrives; step s offers k = lane + 2 - s to this lane
+        double Tj = T[tb];
         const int rows = min(32, P_ - tb);
+        auto kval = [&](int s) { return s >= 2 && s <= rows && lane + 2 - s >= 1 && lane + 2 - s <= Wr; };
+        double c1 = 0.0;                                   // step s (never valid at s = 1)
+        double c2 = kval(2) ? __ldg(crow + lane) : 0.0;    // step s + 1
         for (int s = 1; s <= rows; ++s) {
-          // row tb+s finalises at step s-1 (lane s-1) after T[tb+s-1] arrives
-          const int k = r - (tb + s - 1);
-          if (s - 1 > 0 && k >= 1 && k <= Wr) {
-            const double cand = __dadd_rn(Tj, cost[cb + k]);
+          const double c0 = c1;
+          c1 = c2;
+          c2 = kval(s + 2) ? __ldg(crow + lane - s) : 0.0;  // k = lane + 2 - (s + 2)
+          if (kval(s)) {
+            const double cand = __dadd_rn(Tj, c0);
             if (cand <= acc) {
               acc = cand;
-              kb = k;
+              kb = lane + 2 - s;
             }
           }
           Tj = shfl_d(acc, s - 1);
         }
         if (valid) {
-          Tg[r] = acc;
+          T[r] = acc;
           split[r] = r - kb;
         }
         __syncwarp();
@@ -1145,14 +1182,16 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
 }
 
 template <int POL, bool kHash, bool kLog>
-__global__ void __launch_bounds__(kSimWarps * 32, POL == SCLS_POLICY_SCLS ? 4 : 8) sim_kernel(SimParams p, const int32_t* __restrict__ list,
+__global__ void __launch_bounds__(kSimWarps * 32, POL == SCLS_POLICY_SCLS ? SCLS_SIM_MINB : 8) sim_kernel(SimParams p, const int32_t* __restrict__ list,
                                                               int32_t count) {
   __shared__ int32_t bins[kSimWarps][256];
   __shared__ int32_t ssplit[POL == SCLS_POLICY_SCLS ? kSimWarps : 1][POL == SCLS_POLICY_SCLS ? kSplitSmem + 1 : 1];
+  __shared__ double sT[POL == SCLS_POLICY_SCLS ? kSimWarps : 1][POL == SCLS_POLICY_SCLS ? kSplitSmem + 1 : 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * kSimWarps + warp;
   if (g >= count) return;
-  run_trace<POL, kHash, kLog>(p, list[g], lane, bins[warp], ssplit[POL == SCLS_POLICY_SCLS ? warp : 0]);
+  run_trace<POL, kHash, kLog>(p, list[g], lane, bins[warp], ssplit[POL == SCLS_POLICY_SCLS ? warp : 0],
+                              sT[POL == SCLS_POLICY_SCLS ? warp : 0]);
 }
 
 }  // namespace
