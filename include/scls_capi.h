@@ -132,11 +132,13 @@ int64_t scls_last_launch_count(const scls_ctx* ctx);
 /* Context options.  SCLS_OPT_SIM_DIGESTS (default 1): scls_simulate fills
  * the h_* log digests of scls_trace_result; 0 skips them (the metrics are
  * computed either way, and the digests are zero). */
-enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2 };
+enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT = 3 };
 /* SCLS_OPT_DP_KERNEL: 0 (default) picks the monotone decision kernel when the
  * model allows it and some window exceeds 32 rows, else the serial-chain
  * kernel; 1 forces the chain kernel; 2 forces the decision kernel when the
- * model allows it. */
+ * model allows it.  SCLS_OPT_SIM_CONCURRENT (default 1): the simulator's
+ * per-policy launches run concurrently on forked streams (0: in sequence on
+ * the context stream); results are identical either way. */
 scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value);
 /* Diagnostics: enable/disable clock64 phase counters in the DP chain kernel
  * and read-and-reset them (cycles: main chain, main barrier wait, helper
@@ -294,6 +296,20 @@ scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int64_t* req_of
                           const scls_latency* lat, const scls_memory* memm,
                           scls_trace_result* results, int32_t hist_bins,
                           int64_t* slice_hist, scls_event_log* log, int32_t mem);
+
+/* The sweep grid (experiment.h:60 sweep; experiment.cpp runs every policy /
+ * slice / worker configuration on the same generated trace): every config in
+ * `cfgs` on every trace, each trace's requests staged once.  Job j =
+ * c * n_traces + t simulates trace t under cfgs[c]; results / slice_hist /
+ * log are indexed by job (n_cfgs * n_traces entries).  Same statuses and
+ * per-job results as scls_simulate with the traces repeated per config. */
+scls_status scls_simulate_grid(scls_ctx* ctx, int32_t n_traces, const int64_t* req_offset,
+                               const double* arrival, const int32_t* input_len,
+                               const int32_t* gen_len, int32_t n_cfgs,
+                               const scls_sched_cfg* cfgs, const scls_latency* lat,
+                               const scls_memory* memm, scls_trace_result* results,
+                               int32_t hist_bins, int64_t* slice_hist, scls_event_log* log,
+                               int32_t mem);
 
 /* ---- workload: workload.h:78 generate ------------------------------------
  * Host-side Poisson trace generation (mt19937_64 + glibc log, the reference's

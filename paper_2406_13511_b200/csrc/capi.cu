@@ -190,6 +190,8 @@ void scls_ctx_destroy(scls_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
+  for (auto& st : ctx->side)
+    if (st) cudaStreamDestroy(st);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -220,6 +222,10 @@ scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value) {
   }
   if (option == SCLS_OPT_DP_KERNEL) {
     ctx->dp_mode = (int)value;
+    return SCLS_OK;
+  }
+  if (option == SCLS_OPT_SIM_CONCURRENT) {
+    ctx->sim_concurrent = value != 0;
     return SCLS_OK;
   }
   return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "unknown option");

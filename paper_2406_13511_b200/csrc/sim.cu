@@ -50,8 +50,9 @@ struct SimCfg {
 };
 
 struct SimParams {
-  int32_t n_traces;
-  const int64_t* req_off;
+  int32_t n_traces;  // jobs
+  const int64_t* req_off;  // per source trace
+  const int32_t* src;      // job -> source trace (null: identity)
   const double* arr;
   const int32_t* inp;
   const int32_t* tg;
@@ -282,8 +283,9 @@ __device__ __forceinline__ int bits_of(uint32_t x) { return x ? 32 - __clz(x) : 
 
 template <int POL, bool kHash, bool kLog>
 __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, int32_t* ssplit, double* sT) {
-  const int64_t r0 = P.req_off[t];
-  const int n = (int)(P.req_off[t + 1] - r0);
+  const int ts = P.src ? P.src[t] : t;  // source trace of job t
+  const int64_t r0 = P.req_off[ts];
+  const int n = (int)(P.req_off[ts + 1] - r0);
   const double* __restrict__ arr = P.arr + r0;
   const int32_t* __restrict__ inp = P.inp + r0;
   const int32_t* __restrict__ tg = P.tg + r0;
@@ -1205,14 +1207,14 @@ namespace {
 // Σ_i ceil(min(gen_i, G) / S): the exact number of (request, slice) pairs a
 // SCLS run serves, i.e. the tick-log and batch capacity of the trace.
 __global__ void slice_caps_kernel(int32_t n_traces, const int64_t* __restrict__ req_off,
-                                  const int32_t* __restrict__ tg, const SimCfg* __restrict__ cfgs,
+                                  const int32_t* __restrict__ src, const int32_t* __restrict__ tg, const SimCfg* __restrict__ cfgs,
                                   const int32_t* __restrict__ cfg_index, int64_t* __restrict__ caps) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n_traces) return;
   const SimCfg c = cfgs[cfg_index ? cfg_index[warp] : 0];
   long long s = 0;
   if (c.policy == SCLS_POLICY_SCLS && c.S > 0)
-    for (int64_t i = req_off[warp] + lane; i < req_off[warp + 1]; i += 32) {
+    for (int64_t i = req_off[src ? src[warp] : warp] + lane; i < req_off[(src ? src[warp] : warp) + 1]; i += 32) {
       const int g = min(tg[i], c.G);
       s += (g + c.S - 1) / c.S;
     }
@@ -1278,49 +1280,34 @@ using namespace scls;
 extern "C" scls_status scls_validate_latency(const scls_latency* m);
 extern "C" scls_status scls_validate_memory(const scls_memory* m);
 
-extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int64_t* req_offset,
-                                     const double* arrival, const int32_t* input_len,
-                                     const int32_t* gen_len, int32_t n_cfgs, const scls_sched_cfg* cfgs,
-                                     const int32_t* cfg_index, const scls_latency* lat,
-                                     const scls_memory* memm, scls_trace_result* results,
-                                     int32_t hist_bins, int64_t* slice_hist, scls_event_log* log,
-                                     int32_t mem) {
-  if (!ctx) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null context");
-  ctx->err.clear();
-  ctx->err_request = -1;
-  ctx->launches = 0;
-  std::fill(ctx->timings, ctx->timings + 8, 0.f);
-  SCLS_CUDA(cudaSetDevice(ctx->device));
-  if (n_traces < 0 || n_cfgs < 1 || !cfgs || !lat || !memm || !results || !req_offset || hist_bins < 0 ||
-      (hist_bins > 0 && !slice_hist))
-    return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad arguments");
-  if (n_traces == 0) return SCLS_OK;
+// The simulator entry (shared by scls_simulate and scls_simulate_grid): job j
+// runs source trace src[j] (identity when null) under config job_cfg[j].
+static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* req_offset, const double* arrival,
+                                 const int32_t* input_len, const int32_t* gen_len, int32_t n_cfgs,
+                                 const scls_sched_cfg* cfgs, int32_t n_traces, const std::vector<int32_t>& h_src,
+                                 const std::vector<int32_t>& h_idx, const scls_latency* lat,
+                                 const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
+                                 int64_t* slice_hist, scls_event_log* log, int32_t mem) {
+  // n_traces counts jobs below; h_off / inputs are per source trace.
+  const bool has_src = !h_src.empty();
+  const bool cfg_index = !h_idx.empty();
   cudaStream_t s = ctx->stream;
   // Host-side copies of the small arguments.
-  std::vector<int64_t> h_off(n_traces + 1);
+  std::vector<int64_t> h_off(n_src + 1);
   if (mem == SCLS_MEM_DEVICE) {
-    SCLS_CUDA(cudaMemcpy(h_off.data(), req_offset, sizeof(int64_t) * (n_traces + 1), cudaMemcpyDeviceToHost));
+    SCLS_CUDA(cudaMemcpy(h_off.data(), req_offset, sizeof(int64_t) * (n_src + 1), cudaMemcpyDeviceToHost));
   } else {
-    std::memcpy(h_off.data(), req_offset, sizeof(int64_t) * (n_traces + 1));
+    std::memcpy(h_off.data(), req_offset, sizeof(int64_t) * (n_src + 1));
   }
-  std::vector<int32_t> h_idx;
-  if (cfg_index) {
-    h_idx.resize(n_traces);
-    if (mem == SCLS_MEM_DEVICE)
-      SCLS_CUDA(cudaMemcpy(h_idx.data(), cfg_index, sizeof(int32_t) * n_traces, cudaMemcpyDeviceToHost));
-    else
-      std::memcpy(h_idx.data(), cfg_index, sizeof(int32_t) * n_traces);
-    for (int32_t v : h_idx)
-      if (v < 0 || v >= n_cfgs) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "cfg_index out of range");
-  }
-  const int64_t total = h_off[n_traces] - h_off[0];
+  const int64_t total = h_off[n_src] - h_off[0];
   if (h_off[0] != 0 || total < 0) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "req_offset must start at 0");
   int64_t nmax = 0;
-  for (int t = 0; t < n_traces; ++t) {
+  for (int t = 0; t < n_src; ++t) {
     const int64_t nt = h_off[t + 1] - h_off[t];
     if (nt < 0 || nt >= (1ll << 30)) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad trace size");
     nmax = std::max(nmax, nt);
   }
+  auto src_of = [&](int j) { return has_src ? h_src[j] : j; };
   // Configs: validate (Simulator::Simulator, sim_engine.cpp:32-35), limits.
   const bool model_ok = scls_validate_latency(lat) == SCLS_OK && scls_validate_memory(memm) == SCLS_OK;
   std::vector<SimCfg> hc(n_cfgs);
@@ -1342,7 +1329,9 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
   const double* d_arr = arrival;
   const int32_t* d_inp = input_len;
   const int32_t* d_tg = gen_len;
-  int64_t* d_off = (int64_t*)ctx->buf(kSlotSim + 0, sizeof(int64_t) * (n_traces + 1));
+  int64_t* d_off = (int64_t*)ctx->buf(kSlotSim + 0, sizeof(int64_t) * (n_src + 1));
+  int32_t* d_src = has_src ? (int32_t*)ctx->buf(kSlotSim + 23, sizeof(int32_t) * n_traces) : nullptr;
+  if (has_src && !d_src) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
   SimCfg* d_cfg = (SimCfg*)ctx->buf(kSlotSim + 1, sizeof(SimCfg) * n_cfgs);
   uint8_t* d_ok = (uint8_t*)ctx->buf(kSlotSim + 2, n_cfgs);
   int32_t* d_idx = cfg_index ? (int32_t*)ctx->buf(kSlotSim + 3, sizeof(int32_t) * n_traces) : nullptr;
@@ -1360,7 +1349,8 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
     d_inp = b;
     d_tg = g;
   }
-  SCLS_CUDA(cudaMemcpyAsync(d_off, h_off.data(), sizeof(int64_t) * (n_traces + 1), cudaMemcpyHostToDevice, s));
+  SCLS_CUDA(cudaMemcpyAsync(d_off, h_off.data(), sizeof(int64_t) * (n_src + 1), cudaMemcpyHostToDevice, s));
+  if (d_src) SCLS_CUDA(cudaMemcpyAsync(d_src, h_src.data(), sizeof(int32_t) * n_traces, cudaMemcpyHostToDevice, s));
   SCLS_CUDA(cudaMemcpyAsync(d_cfg, hc.data(), sizeof(SimCfg) * n_cfgs, cudaMemcpyHostToDevice, s));
   SCLS_CUDA(cudaMemcpyAsync(d_ok, hok.data(), n_cfgs, cudaMemcpyHostToDevice, s));
   if (d_idx) SCLS_CUDA(cudaMemcpyAsync(d_idx, h_idx.data(), sizeof(int32_t) * n_traces, cudaMemcpyHostToDevice, s));
@@ -1378,7 +1368,7 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
   }
   int64_t* d_caps = (int64_t*)ctx->buf(kSlotSim + 7, sizeof(int64_t) * n_traces);
   if (!d_caps) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
-  slice_caps_kernel<<<div_up((int64_t)n_traces * 32, 256), 256, 0, s>>>(n_traces, d_off, d_tg, d_cfg, d_idx, d_caps);
+  slice_caps_kernel<<<div_up((int64_t)n_traces * 32, 256), 256, 0, s>>>(n_traces, d_off, d_src, d_tg, d_cfg, d_idx, d_caps);
   SCLS_LAUNCHED();
   std::vector<int64_t> caps(n_traces);
   SCLS_CUDA(cudaMemcpyAsync(caps.data(), d_caps, sizeof(int64_t) * n_traces, cudaMemcpyDeviceToHost, s));
@@ -1437,7 +1427,7 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
   std::vector<int64_t> tbase(n_traces + 1, 0);
   for (int t = 0; t < n_traces; ++t) {
     const SimCfg& c = hc[cfg_index ? h_idx[t] : 0];
-    const int64_t nt = h_off[t + 1] - h_off[t];
+    const int64_t nt = h_off[src_of(t) + 1] - h_off[src_of(t)];
     tbase[t + 1] = tbase[t] + sim_layout(nt, std::max(c.W, 1), c.policy, caps[t], std::max(c.MC, 1)).total;
   }
   int64_t* d_tbase = (int64_t*)ctx->buf(kSlotSim + 13, sizeof(int64_t) * (n_traces + 1));
@@ -1457,6 +1447,7 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
   SimParams p{};
   p.n_traces = n_traces;
   p.req_off = d_off;
+  p.src = d_src;
   p.arr = d_arr;
   p.inp = d_inp;
   p.tg = d_tg;
@@ -1511,24 +1502,48 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
     SCLS_CUDA(cudaMemcpyAsync(d_lists, flat.data(), sizeof(int32_t) * n_traces, cudaMemcpyHostToDevice, s));
   }
   const bool hash = ctx->sim_digests;
+  // Per-policy launches; with more than one policy they run concurrently on
+  // forked streams so one kernel's tail overlaps the others' work.
+  int n_pol = 0;
+  for (auto& l : lists) n_pol += !l.empty();
+  const bool fork = ctx->sim_concurrent && n_pol > 1;
+  if (fork) {
+    for (auto& st : ctx->side)
+      if (!st) SCLS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    SCLS_CUDA(cudaEventRecord(ctx->ev[8], s));
+  }
   int64_t at = 0;
-  for (int pol = 0; pol < 3; ++pol) {
+  int k = 0;
+  for (int pol : {SCLS_POLICY_ILS, SCLS_POLICY_SCLS, SCLS_POLICY_SLS}) {  // longest first
     const int32_t cnt = (int32_t)lists[pol].size();
+    int64_t off = 0;
+    for (int q = 0; q < pol; ++q) off += (int64_t)lists[q].size();
     if (cnt == 0) continue;
+    cudaStream_t ls = s;
+    if (fork) {
+      ls = ctx->side[k];
+      SCLS_CUDA(cudaStreamWaitEvent(ls, ctx->ev[8], 0));
+    }
     const int grid = div_up(cnt, kSimWarps);
-    const int32_t* l = d_lists + at;
+    const int32_t* l = d_lists + off;
     at += cnt;
-#define SCLS_SIM_LAUNCH(POLV)                                                                     \
-  if (want_log) sim_kernel<POLV, true, true><<<grid, kSimWarps * 32, 0, s>>>(p, l, cnt);          \
-  else if (hash) sim_kernel<POLV, true, false><<<grid, kSimWarps * 32, 0, s>>>(p, l, cnt);        \
-  else sim_kernel<POLV, false, false><<<grid, kSimWarps * 32, 0, s>>>(p, l, cnt);
+#define SCLS_SIM_LAUNCH(POLV)                                                                      \
+  if (want_log) sim_kernel<POLV, true, true><<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);          \
+  else if (hash) sim_kernel<POLV, true, false><<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);        \
+  else sim_kernel<POLV, false, false><<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);
     if (pol == SCLS_POLICY_SCLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SCLS) }
     else if (pol == SCLS_POLICY_SLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SLS) }
-    else if (!want_log && !hash) sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, s>>>(p, l, cnt);
+    else if (!want_log && !hash) sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);
     else { SCLS_SIM_LAUNCH(SCLS_POLICY_ILS) }
 #undef SCLS_SIM_LAUNCH
     SCLS_LAUNCHED();
+    if (fork) {
+      SCLS_CUDA(cudaEventRecord(ctx->ev[9 + k], ls));
+      SCLS_CUDA(cudaStreamWaitEvent(s, ctx->ev[9 + k], 0));
+    }
+    ++k;
   }
+  (void)at;
   SCLS_CUDA(cudaEventRecord(ctx->ev[2], s));
   if (mem == SCLS_MEM_HOST) {
     SCLS_CUDA(cudaMemcpyAsync(results, d_res, sizeof(scls_trace_result) * n_traces, cudaMemcpyDeviceToHost, s));
@@ -1549,4 +1564,61 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
   cudaEventElapsedTime(&ctx->timings[6], ctx->ev[1], ctx->ev[2]);
   cudaEventElapsedTime(&ctx->timings[2], ctx->ev[0], ctx->ev[1]);
   return SCLS_OK;
+}
+
+extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int64_t* req_offset,
+                                     const double* arrival, const int32_t* input_len,
+                                     const int32_t* gen_len, int32_t n_cfgs, const scls_sched_cfg* cfgs,
+                                     const int32_t* cfg_index, const scls_latency* lat,
+                                     const scls_memory* memm, scls_trace_result* results,
+                                     int32_t hist_bins, int64_t* slice_hist, scls_event_log* log,
+                                     int32_t mem) {
+  if (!ctx) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null context");
+  ctx->err.clear();
+  ctx->err_request = -1;
+  ctx->launches = 0;
+  std::fill(ctx->timings, ctx->timings + 8, 0.f);
+  SCLS_CUDA(cudaSetDevice(ctx->device));
+  if (n_traces < 0 || n_cfgs < 1 || !cfgs || !lat || !memm || !results || !req_offset || hist_bins < 0 ||
+      (hist_bins > 0 && !slice_hist))
+    return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (n_traces == 0) return SCLS_OK;
+  std::vector<int32_t> h_idx;
+  if (cfg_index) {
+    h_idx.resize(n_traces);
+    if (mem == SCLS_MEM_DEVICE)
+      SCLS_CUDA(cudaMemcpy(h_idx.data(), cfg_index, sizeof(int32_t) * n_traces, cudaMemcpyDeviceToHost));
+    else
+      std::memcpy(h_idx.data(), cfg_index, sizeof(int32_t) * n_traces);
+    for (int32_t v : h_idx)
+      if (v < 0 || v >= n_cfgs) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "cfg_index out of range");
+  }
+  return simulate_core(ctx, n_traces, req_offset, arrival, input_len, gen_len, n_cfgs, cfgs, n_traces, {}, h_idx,
+                       lat, memm, results, hist_bins, slice_hist, log, mem);
+}
+
+extern "C" scls_status scls_simulate_grid(scls_ctx* ctx, int32_t n_traces, const int64_t* req_offset,
+                                          const double* arrival, const int32_t* input_len,
+                                          const int32_t* gen_len, int32_t n_cfgs, const scls_sched_cfg* cfgs,
+                                          const scls_latency* lat, const scls_memory* memm,
+                                          scls_trace_result* results, int32_t hist_bins, int64_t* slice_hist,
+                                          scls_event_log* log, int32_t mem) {
+  if (!ctx) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null context");
+  ctx->err.clear();
+  ctx->err_request = -1;
+  ctx->launches = 0;
+  std::fill(ctx->timings, ctx->timings + 8, 0.f);
+  SCLS_CUDA(cudaSetDevice(ctx->device));
+  if (n_traces < 0 || n_cfgs < 1 || !cfgs || !lat || !memm || !results || !req_offset || hist_bins < 0 ||
+      (hist_bins > 0 && !slice_hist) || (int64_t)n_traces * n_cfgs > INT32_MAX)
+    return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (n_traces == 0) return SCLS_OK;
+  const int32_t n_jobs = n_traces * n_cfgs;
+  std::vector<int32_t> h_src(n_jobs), h_idx(n_jobs);
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    h_src[j] = j % n_traces;
+    h_idx[j] = j / n_traces;
+  }
+  return simulate_core(ctx, n_traces, req_offset, arrival, input_len, gen_len, n_cfgs, cfgs, n_jobs, h_src, h_idx,
+                       lat, memm, results, hist_bins, slice_hist, log, mem);
 }

@@ -226,8 +226,9 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
   if (g >= count) return;
   const int t = list[g];
   int32_t* bins = sbins[warp];
-  const int64_t r0 = P.req_off[t];
-  const int n = (int)(P.req_off[t + 1] - r0);
+  const int ts = P.src ? P.src[t] : t;  // source trace of job t
+  const int64_t r0 = P.req_off[ts];
+  const int n = (int)(P.req_off[ts + 1] - r0);
   const double* __restrict__ arr = P.arr + r0;
   const int32_t* __restrict__ inp = P.inp + r0;
   const int32_t* __restrict__ tg = P.tg + r0;

@@ -30,7 +30,7 @@ EXPORTS = [
     "scls_validate_latency", "scls_validate_memory", "scls_validate_sched",
     "scls_batch_serve_time", "scls_would_oom", "scls_max_batch_size",
     "scls_batch_requests", "scls_offload", "scls_schedule", "scls_simulate",
-    "scls_generate", "scls_make_pool", "scls_debug_dp_profile", "scls_set_option",
+    "scls_simulate_grid", "scls_generate", "scls_make_pool", "scls_debug_dp_profile", "scls_set_option",
 ]
 
 
@@ -78,6 +78,8 @@ def load():
                                 P(capi.Batches), vp, vp, i32]),
         "scls_simulate": (i32, [vp, i32, vp, vp, vp, vp, i32, S, vp, L, M,
                                 P(capi.TraceResult), i32, vp, P(capi.EventLog), i32]),
+        "scls_simulate_grid": (i32, [vp, i32, vp, vp, vp, vp, i32, S, L, M,
+                                     P(capi.TraceResult), i32, vp, P(capi.EventLog), i32]),
         "scls_generate": (i32, [P(capi.WorkloadSpec), i64, P(i64), vp, vp, vp]),
         "scls_make_pool": (i32, [i64, C.c_uint64, vp, vp, vp, vp]),
         "scls_debug_dp_profile": (i32, [vp, i32, vp]),
@@ -152,6 +154,10 @@ class Context:
     def set_digests(self, on):
         """SCLS_OPT_SIM_DIGESTS: compute the per-trace log digests (default on)."""
         self._check(self.lib.scls_set_option(self.h, 1, 1 if on else 0))
+
+    def set_concurrent(self, on):
+        """SCLS_OPT_SIM_CONCURRENT: run the per-policy simulator launches concurrently."""
+        self._check(self.lib.scls_set_option(self.h, 3, 1 if on else 0))
 
     def set_dp_kernel(self, mode):
         """SCLS_OPT_DP_KERNEL: 0 auto (monotone decision kernel when allowed), 1 chain."""
@@ -275,17 +281,7 @@ class Context:
                  rec_cap=0, mem_cap=0):
         """Simulator::run + compute for every trace (list of (arrival, input_len,
         gen_len)).  Returns (results, hist[, log])."""
-        offs = np.zeros(len(traces) + 1, np.int64)
-        for i, t in enumerate(traces):
-            offs[i + 1] = offs[i] + len(t[0])
-        tot = max(int(offs[-1]), 1)
-        arr = np.zeros(tot, np.float64)
-        inp = np.zeros(tot, np.int32)
-        gen = np.zeros(tot, np.int32)
-        for i, (a, b, g) in enumerate(traces):
-            arr[offs[i]:offs[i + 1]] = a
-            inp[offs[i]:offs[i + 1]] = b
-            gen[offs[i]:offs[i + 1]] = g
+        offs, arr, inp, gen = _flatten(traces)
         return self.simulate_flat(offs, arr, inp, gen, cfgs, lat, mem, cfg_index, hist_bins,
                                   n_logged, rec_cap, mem_cap)
 
@@ -318,6 +314,44 @@ class Context:
         if log is not None:
             return res, hist, log
         return res, hist
+
+    def simulate_grid(self, traces, cfgs, lat, mem, hist_bins=64):
+        """scls_simulate_grid: every config on every trace, each trace staged
+        once.  Returns (results, hist) with results[c][t] and hist[c, t]."""
+        if isinstance(cfgs, capi.SchedCfg):
+            cfgs = [cfgs]
+        offs, arr, inp, gen = _flatten(traces)
+        res, hist = self.simulate_grid_flat(offs, arr, inp, gen, cfgs, lat, mem, hist_bins)
+        ntr = len(traces)
+        return [[res[c * ntr + t] for t in range(ntr)] for c in range(len(cfgs))], hist
+
+    def simulate_grid_flat(self, offs, arr, inp, gen, cfgs, lat, mem, hist_bins=64):
+        ntr, nc = len(offs) - 1, len(cfgs)
+        cfg_arr = (capi.SchedCfg * nc)(*cfgs)
+        res = (capi.TraceResult * max(ntr * nc, 1))()
+        hist = np.zeros(max(ntr * nc * hist_bins, 1), np.int64)
+        self._check(self.lib.scls_simulate_grid(self.h, ntr, _ptr(np.ascontiguousarray(offs, np.int64)),
+                                                _ptr(arr), _ptr(inp), _ptr(gen), nc, cfg_arr,
+                                                C.byref(lat), C.byref(mem), res, hist_bins, _ptr(hist), None,
+                                                capi.MEM_HOST))
+        # flat job order: res[c * ntr + t]
+        return res, hist[:ntr * nc * hist_bins].reshape(nc, ntr, hist_bins)
+
+
+def _flatten(traces):
+    """List of (arrival, input_len, gen_len) -> (req_offset, arrival, input_len, gen_len)."""
+    offs = np.zeros(len(traces) + 1, np.int64)
+    for i, t in enumerate(traces):
+        offs[i + 1] = offs[i] + len(t[0])
+    tot = max(int(offs[-1]), 1)
+    arr = np.zeros(tot, np.float64)
+    inp = np.zeros(tot, np.int32)
+    gen = np.zeros(tot, np.int32)
+    for i, (a, b, g) in enumerate(traces):
+        arr[offs[i]:offs[i + 1]] = a
+        inp[offs[i]:offs[i + 1]] = b
+        gen[offs[i]:offs[i + 1]] = g
+    return offs, arr, inp, gen
 
 
 def generate(spec):

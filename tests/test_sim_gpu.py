@@ -266,3 +266,33 @@ def test_metrics_only_edge_times(ctx, orc):
                 if not f.startswith("h_"):
                     assert getattr(a[t], f) == getattr(b[t], f), (lname, t, cfgs[t].policy, f)
         assert np.array_equal(ha, hb), lname
+
+
+@pytest.mark.parametrize("digests", [False, True])
+@pytest.mark.parametrize("concurrent", [True, False])
+def test_simulate_grid_matches_per_trace_runs(ctx, orc, digests, concurrent):
+    """scls_simulate_grid (each trace staged once, every config on every
+    trace, per-policy launches on forked streams) must equal the oracle run
+    on the repeated traces, job by job."""
+    lat = capi.builtin_latency_model()
+    traces = [orc.generate(capi.workload_spec(rate=r, duration_s=45.0, seed=900 + i))
+              for i, r in enumerate((6.0, 11.0, 17.0, 23.0, 29.0))]
+    cfgs = [capi.sched_cfg(policy=p, worker_count=w, slice_len=sl)
+            for p, w, sl in (("scls", 4, 64), ("sls", 3, 128), ("ils", 5, 128), ("scls", 8, 128), ("ils", 2, 64))]
+    ctx.set_digests(digests)
+    ctx.set_concurrent(concurrent)
+    try:
+        got, gh = ctx.simulate_grid(traces, cfgs, lat, MEMORIES["rule"](), hist_bins=16)
+    finally:
+        ctx.set_digests(True)
+        ctx.set_concurrent(True)
+    rep = [t for _ in cfgs for t in traces]
+    idx = [c for c in range(len(cfgs)) for _ in traces]
+    want, wh = orc.simulate(rep, cfgs, lat, MEMORIES["rule"](), cfg_index=idx, hist_bins=16)
+    for c in range(len(cfgs)):
+        for t in range(len(traces)):
+            a, b = got[c][t], want[c * len(traces) + t]
+            for f in FIELDS:
+                if digests or not f.startswith("h_"):
+                    assert getattr(a, f) == getattr(b, f), (c, t, f)
+    assert np.array_equal(gh.reshape(-1, 16), np.asarray(wh).reshape(-1, 16))
