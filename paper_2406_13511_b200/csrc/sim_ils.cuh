@@ -13,6 +13,8 @@
 namespace scls {
 namespace {
 
+constexpr int kIlsRunSmem = 128;  // running slots per warp kept in shared memory (W * MC)
+
 __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
   unsigned y;
   asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
@@ -221,6 +223,7 @@ __device__ void finish_report(int lane, scls_trace_result* R, int status, int n,
 __global__ void __launch_bounds__(kSimWarps * 32, 8)
     sim_ils_lean_kernel(SimParams P, const int32_t* __restrict__ list, int32_t count) {
   __shared__ int32_t sbins[kSimWarps][256];
+  __shared__ int4 srun[kSimWarps][kIlsRunSmem];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * kSimWarps + warp;
   if (g >= count) return;
@@ -254,10 +257,11 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
   char* base = P.arena + P.trace_base[t];
   const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_ILS, P.trace_cap[t], MC);
   double* resp = (double*)(base + Lay.resp);
-  const int cap_w = (n + W - 1) / W;
-  int32_t* fifo_base = (int32_t*)(base + Lay.fifo);
-  int4* run_base = (int4*)(base + Lay.run);
-  int32_t* ex_base = (int32_t*)(base + Lay.ex);
+  // Running slots in this warp's shared memory when W * MC fits (global
+  // arena otherwise).  Waiting FIFOs need no storage: arrivals go round-robin
+  // in id order (sched_policies.cpp:280), so instance w's k-th arrival is
+  // request w + k * W and a FIFO is just its (head, tail) counters.
+  int4* run_base = W * MC <= kIlsRunSmem ? srun[warp] : (int4*)(base + Lay.run);
 
   // instance registers (lane w < W)
   double ev_t = dinf(), last_end = 0.0;
@@ -305,11 +309,11 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
       const double clock = next_arr;
       next_arr = cur < n ? arr[cur] : dinf();
       ++n_events;
-      const int w = rr;
+      const int w = rr;  // == id % W
       rr = rr + 1 == W ? 0 : rr + 1;
       const bool wake = shfl_i(n_run == 0 && !boundary, w);  // idle instance: boundary at `clock`
+      (void)id;
       if (lane == w) {
-        fifo_base[(int64_t)w * cap_w + f_tail] = id;
         ++f_tail;
         if (wake) {
           ev_t = clock;
@@ -329,7 +333,6 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
     const int w = na_w;
     const double now = na_t;
     int4* run = run_base + (int64_t)w * MC;
-    const int32_t* wq = fifo_base + (int64_t)w * cap_w;
     const int nr = shfl_i(n_run, w);
     const int it1 = shfl_i(it_cnt, w) + (nr > 0 ? 1 : 0);
     const int head = shfl_i(f_head, w), tail = shfl_i(f_tail, w);
@@ -341,6 +344,8 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
         seg_it += 1;
       }
     }
+    // retire (survivors compacted in order; exits complete in member order,
+    // their responses written straight to resp) and admit FCFS
     int nexit = 0, keep = 0;
     for (int b0 = 0; b0 < nr; b0 += 32) {
       const int i = b0 + lane;
@@ -354,7 +359,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
       const unsigned em = __ballot_sync(FULL, ok && ex);
       const unsigned km = __ballot_sync(FULL, ok && !ex);
       __syncwarp();
-      if (ok && ex) ex_base[nexit + __popc(em & lt)] = v.x;
+      if (ok && ex) resp[completed + nexit + __popc(em & lt)] = now - arr[v.x];
       if (ok && !ex) run[keep + __popc(km & lt)] = v;
       nexit += __popc(em);
       keep += __popc(km);
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
     }
     const int njoin = min(MC - keep, tail - head);
     for (int j = lane; j < njoin; j += 32) {
-      const int id = wq[head + j];
+      const int id = w + (head + j) * W;
       run[keep + j] = make_int4(id, it1, min(tg[id], G), inp[id]);
     }
     __syncwarp();
@@ -381,11 +386,9 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
         last_end = fmax(last_end, now);
       }
     }
-    for (int c0 = 0; c0 < nexit; c0 += 32) {  // completions, member order
-      const int cnt = min(32, nexit - c0);
-      if (lane < cnt) resp[completed + lane] = now - arr[ex_base[c0 + lane]];
-      completed += cnt;
-      n_events += cnt;
+    if (nexit > 0) {  // completions (responses written above)
+      completed += nexit;
+      n_events += nexit;
       last_completion = now;
     }
     __syncwarp();
