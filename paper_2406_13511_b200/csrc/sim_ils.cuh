@@ -14,6 +14,7 @@ namespace scls {
 namespace {
 
 constexpr int kIlsRunSmem = 128;  // running slots per warp kept in shared memory (W * MC)
+constexpr int kOwnBuckets = 1024;  // owner table of the rounds' distinct-key certificate
 
 __device__ __forceinline__ unsigned opaque_u32(unsigned x) {
   unsigned y;
@@ -57,7 +58,7 @@ template <bool kPos>
 __device__ __forceinline__ void ils_fast_rounds(int lane, int W, int MC, double next_arr, double horizon,
                                                 const Lat& lat, int n_run, int f_head, int f_tail, int next_exit,
                                                 int& it_cnt, int& seg_it, int& mctx, double& ev_t, PushOrder& po,
-                                                unsigned& round_ctr) {
+                                                unsigned& round_ctr, uint8_t* own) {
   const bool has = lane < W && ev_t != dinf();
   bool fast = has && n_run > 0 && it_cnt + 1 < next_exit && !(f_tail > f_head && n_run < MC);
   const uint64_t limit = time_key<kPos>(fmin(next_arr, horizon));
@@ -86,14 +87,22 @@ __device__ __forceinline__ void ils_fast_rounds(int lane, int W, int MC, double 
       // one bucket per member (cheap REDUX.OR); only an inconclusive mask
       // pays for the exact MATCH (distinct sentinels: keys in the round are
       // < limit < ~lane).
-      const unsigned lo = (unsigned)key, ns = __popc(S);
-      const unsigned b1 = __reduce_or_sync(FULL, in ? 1u << (lo & 31u) : 0u);
-      if (__popc(b1) != ns) {
-        const unsigned b2 = __reduce_or_sync(FULL, in ? 1u << ((lo >> 5) & 31u) : 0u);
-        if (__popc(b2) != ns) {
-          const unsigned same = __match_any_sync(FULL, in ? key : ~(uint64_t)lane);
-          if (__any_sync(FULL, same & (same - 1u))) break;
-        }
+      // Distinct keys are certified by an owner table in shared memory: each
+      // member writes its lane id into bucket h(key) and reads it back; a
+      // member that finds another lane's id (a tie, or a bucket collision --
+      // ~2% of rounds with 1024 buckets) sends the round to the exact but slow
+      // MATCH (~450 cycles on B200 vs ~80 for the table).
+      bool clash = false;
+      if (in) {
+        const unsigned lo = (unsigned)key;
+        const unsigned h = (lo ^ (lo >> 10) ^ (unsigned)(key >> 32)) & (kOwnBuckets - 1);
+        own[h] = (uint8_t)lane;
+        __syncwarp(S);
+        clash = own[h] != (uint8_t)lane;
+      }
+      if (__any_sync(FULL, clash)) {
+        const unsigned same = __match_any_sync(FULL, in ? key : ~(uint64_t)lane);
+        if (__any_sync(FULL, same & (same - 1u))) break;
       }
     }
     if (in) {
@@ -220,10 +229,14 @@ __device__ void finish_report(int lane, scls_trace_result* R, int status, int n,
   }
 }
 
-__global__ void __launch_bounds__(kSimWarps * 32, 8)
+#ifndef SCLS_ILS_MINB
+#define SCLS_ILS_MINB 7  // 28 warps/SM: one wave for 4096 traces, 72 registers
+#endif
+__global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_MINB)
     sim_ils_lean_kernel(SimParams P, const int32_t* __restrict__ list, int32_t count) {
   __shared__ int32_t sbins[kSimWarps][256];
   __shared__ int4 srun[kSimWarps][kIlsRunSmem];
+  __shared__ uint8_t sown[kSimWarps][kOwnBuckets];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * kSimWarps + warp;
   if (g >= count) return;
@@ -287,7 +300,21 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
                    lat.p4 >= 0.0 && lat.d1 >= 0.0 && lat.d2 >= 0.0 && lat.d3 >= 0.0 && lat.d4 >= 0.0 &&
                    (lat.d2 > 0.0 || lat.d4 > 0.0);
 
+#ifdef SCLS_ILS_PROF  // debug build: per-phase clock64 totals into hist[4..15]
+  long long prof[10] = {0}, tp = clock64();
+#define ILS_PROF(i)                \
+  do {                             \
+    const long long tq = clock64(); \
+    prof[i] += tq - tp;            \
+    tp = tq;                       \
+  } while (0)
+#else
+#define ILS_PROF(i) \
+  do {              \
+  } while (0)
+#endif
   while (completed < n) {
+    ILS_PROF(9);
     // ---- fast lane: unchanged iterations (see run_trace<ILS>) -------------------
     // While no instance changes membership, the next arrival and the horizon are
     // fixed, so one precomputed key bounds the run: the loop stops at the first
@@ -297,13 +324,15 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
     // next step time is computed one iteration ahead, off the critical path.
     if (pos)
       ils_fast_rounds<true>(lane, W, MC, next_arr, horizon, lat, n_run, f_head, f_tail, next_exit, it_cnt, seg_it,
-                            mctx, ev_t, po, round_ctr);
+                            mctx, ev_t, po, round_ctr, sown[warp]);
     else
       ils_fast_rounds<false>(lane, W, MC, next_arr, horizon, lat, n_run, f_head, f_tail, next_exit, it_cnt, seg_it,
-                             mctx, ev_t, po, round_ctr);
+                             mctx, ev_t, po, round_ctr, sown[warp]);
+    ILS_PROF(0);
     // ---- general step ----------------------------------------------------------------
     double na_t;
     const int na_w = argmin_pending(ev_t, po, lane < W && ev_t != dinf(), lane, &na_t);
+    ILS_PROF(1);
     if (next_arr <= fmin(na_t, horizon)) {  // arrival (seq < n): sched_policies.cpp:279-290
       const int id = cur++;
       const double clock = next_arr;
@@ -323,6 +352,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
         }
       }
       if (wake) ++round_ctr;
+      ILS_PROF(2);
       continue;
     }
     if (horizon <= na_t) {  // EndOfRun precedes every later event
@@ -365,6 +395,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
       keep += __popc(km);
       __syncwarp();
     }
+    ILS_PROF(3);
     const int njoin = min(MC - keep, tail - head);
     for (int j = lane; j < njoin; j += 32) {
       const int id = w + (head + j) * W;
@@ -376,6 +407,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
       f_head = head + njoin;
       n_run = nr_new;
     }
+    ILS_PROF(4);
     const bool changed = nexit > 0 || njoin > 0;
     if (changed && shfl_i(seg_id, w) >= 0 && shfl_i(seg_it, w) > 0) {  // batch_end record
       ++batch_count;
@@ -396,6 +428,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
       if (lane == w) boundary = 0;
       continue;
     }
+    ILS_PROF(5);
     int mc = 0, nx = 0x7fffffff;
     for (int i = lane; i < nr_new; i += 32) {
       const int4 v = run[i];
@@ -427,8 +460,13 @@ __global__ void __launch_bounds__(kSimWarps * 32, 8)
       boundary = 1;
     }
     ++round_ctr;
+    ILS_PROF(6);
   }
   (void)seg_lin;
+#ifdef SCLS_ILS_PROF
+  if (hist && P.hist_bins >= 14 && lane == 0)
+    for (int i = 0; i < 10; ++i) hist[4 + i] = prof[i];
+#endif
   if (hist && status == SCLS_OK && P.hist_bins > 1 && lane == 0) hist[1] = completed;
   finish_report(lane, R, status, n, W, completed, n > 0 ? arr[0] : dinf(), last_completion, resp, bins, last_end, 0,
                 0, batch_count, batch_members, 0, n_events, n_disp, 0, last_completion);

@@ -1,0 +1,20 @@
+"""Per-phase clock64 breakdown of the lean ILS kernel (build with
+make -C paper_2406_13511_b200/csrc EXTRA=-DSCLS_ILS_PROF)."""
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+from paper_2406_13511_b200 import capi, lib
+ntr = int(sys.argv[1]) if len(sys.argv) > 1 else 148
+rate = float(sys.argv[2]) if len(sys.argv) > 2 else 25.0
+ctx = lib.Context(0)
+ctx.set_digests(False)
+lat = capi.builtin_latency_model(); mem = capi.builtin_memory_model()
+traces = [lib.generate(capi.workload_spec(rate=rate, duration_s=600.0, seed=1000 + i)) for i in range(ntr)]
+res, hist = ctx.simulate(traces, capi.sched_cfg(policy="ils"), lat, mem, hist_bins=16)
+print("sim %.1f ms" % ctx.timings()["simulate"])
+p = hist[:, 4:14].astype(np.float64).mean(axis=0)
+names = ["rounds", "argmin", "arrival", "compact", "join", "records+compl", "mc/nx+push", "-", "-", "loop top"]
+tot = p.sum()
+for n, v in zip(names, p):
+    print("%-14s %12.0f cycles/trace  %5.1f%%" % (n, v, 100 * v / tot))
+print("total %.0f cycles/trace = %.1f ms at 1.965 GHz" % (tot, tot / 1.965e6))
