@@ -369,6 +369,11 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   int32_t* split_g = (int32_t*)(base + Lay.split);
   int32_t* segs = (int32_t*)(base + Lay.segs);
   int32_t* tlog = (int32_t*)(base + Lay.tlog);
+  int32_t* tl_g = (int32_t*)(base + Lay.tl_g);
+  int32_t* tl_t = (int32_t*)(base + Lay.tl_t);
+  int32_t* tl_e = (int32_t*)(base + Lay.tl_e);
+  int32_t* tl_s = (int32_t*)(base + Lay.tl_s);
+  double* tl_a = (double*)(base + Lay.tl_a);
   int32_t* b_start = (int32_t*)(base + Lay.b_start);
   int32_t* b_n = (int32_t*)(base + Lay.b_n);
   int32_t* b_lin = (int32_t*)(base + Lay.b_lin);
@@ -388,6 +393,21 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   const double* cost = P.cost;
   const Lat& lat = P.lat;  // stays in the kernel parameter (constant) bank: frees 16 registers
 
+#ifdef SCLS_SIM_PROF  // debug build: SCLS per-phase clock64 totals into hist[4..15]
+  long long prof[12] = {0}, tp = clock64();
+#define SIM_PROF(i)                                 \
+  do {                                              \
+    if (POL == SCLS_POLICY_SCLS) {                  \
+      const long long tq = clock64();               \
+      prof[i] += tq - tp;                           \
+      tp = tq;                                      \
+    }                                               \
+  } while (0)
+#else
+#define SIM_PROF(i) \
+  do {              \
+  } while (0)
+#endif
   if (POL == SCLS_POLICY_SCLS) {  // sched_policies.cpp:84: first tick at 0
     tick_t = 0.0;
     tick_s = next_seq++;
@@ -485,8 +505,10 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       }
       emax = __reduce_max_sync(FULL, emax);
       __syncwarp();
+      SIM_PROF(2);
       const bool sw = warp_radix_sort(P_, sk, nullptr, sk2, nullptr, idb + bits_of(emax), lane, bins);
       const uint64_t* keys = sw ? sk2 : sk;
+      SIM_PROF(3);
       const uint64_t idmask = (1ull << idb) - 1ull;
       // 2. rows: L, singleton feasibility (batcher.cpp:40-46)
       int bad = 0x7fffffff;
@@ -494,7 +516,13 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         const uint64_t key = keys[i];
         const int id = (int)(key & idmask);
         const int L = (int)(key >> idb);
-        tlog[tl_pos + i] = id;
+        const int64_t q = tl_pos + i;
+        tlog[q] = id;
+        tl_g[q] = gen[id];
+        tl_t[q] = tg[id];
+        tl_e[q] = L;
+        tl_s[q] = sl[id];
+        tl_a[q] = arr[id];
         sv[i] = L;
         if (L > P.Lmax || Kt[L] == 0) bad = min(bad, i);
       }
@@ -504,6 +532,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         err_req = tlog[tl_pos + bad];
         return SCLS_ERR_INFEASIBLE_REQUEST;
       }
+      SIM_PROF(4);
       // 3. the DP (batcher.cpp:48-67): tiles of 32 rows, far+mid then the chain.
       //    T and split live in this warp's shared memory when the pool fits.
       //    Cost loads are issued ahead of the dependent adds (4-wide batches
@@ -585,6 +614,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         }
         __syncwarp();
       }
+      SIM_PROF(5);
       // 4. backtrack (batcher.cpp:69-73): segment ends, reversed
       int cnt = 0;
       for (int i = P_; i > 0; i = split[i]) {
@@ -605,12 +635,17 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           b_n[bi] = end - beg;
           b_lin[bi] = L;
           b_est[bi] = cost[coff[L] - 1 + (end - beg)];
+          // slice_served_l_out (sched_policies.cpp:72-80): max over members
+          int served = 0;
+          for (int q = tl_pos + beg; q < tl_pos + end; ++q) served = max(served, min(tl_t[q] - tl_g[q], C.S));
+          b_served[bi] = served;
         }
       }
       tl_pos += P_;
       pool_len = 0;
       __syncwarp();
     }
+    SIM_PROF(6);
     const int first = (int)next_batch;
     next_batch += nb;
     // 6. offload (offloader.cpp:25-54): stable est-descending order, then the
@@ -642,21 +677,13 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       const double e = b_est[b];
       double bt;
       unsigned long long bs;
-      const int w = argmin_event(lane < W ? load : dinf(), (unsigned long long)lane, lane, rounds, &bt, &bs);
+      // min (load, worker id): loads are >= 0, so (load, lane) keys order exactly
+      const int w = argmin_event_redux(load, (unsigned long long)lane, lane < W, lane, &bt, &bs);
       if (lane == w) load = __dadd_rn(load, e);
-      // dispatch record, slice_served_l_out (sched_policies.cpp:72-80), enqueue
-      const int bn = b_n[b], bst = b_start[b];
-      int served = 0;
-      for (int i = lane; i < bn; i += 32) {
-        const int id = tlog[bst + i];
-        served = max(served, min(tg[id] - gen[id], C.S));
-      }
-      served = __reduce_max_sync(FULL, served);
+      // dispatch record (served l_out computed at emit), enqueue
+      const int bn = b_n[b];
       sink.record(lane, 2, clock, -1, w, b, bn, b_lin[b], C.S, 0, e, 0, 0, 0.0, 0, 0.0, 0);
-      if (lane == 0) {
-        b_served[b] = served;
-        b_next[b] = -1;
-      }
+      if (lane == 0) b_next[b] = -1;
       const int tail = shfl_i(q_tail, w);
       if (lane == 0 && tail >= 0) b_next[tail] = b;
       if (lane == w) {
@@ -666,6 +693,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       __syncwarp();
       start_next_scls(w);
     }
+    SIM_PROF(7);
     // sched_policies.cpp:134-146: adaptive interval from the post-offload loads
     double ml = lane < W ? load : dinf();
     for (int o = 16; o; o >>= 1) ml = fmin(ml, __shfl_xor_sync(FULL, ml, o));
@@ -686,23 +714,24 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     early += served < C.S;
     const unsigned lt = (1u << lane) - 1u;
     int nfin = 0;
-    int32_t* fin = sv;  // finished ids, member order (reused scratch)
+    int32_t* fin = sv;  // finished members' slots, member order (reused scratch)
     for (int b0 = 0; b0 < bn; b0 += 32) {
       const int i = b0 + lane;
       const bool ok = i < bn;
       int id = 0, eff = 0, g = 0, pad = 0, inv = 0;
       bool done = false;
       if (ok) {
-        id = tlog[bst + i];
-        const int gsf = gen[id];
-        eff = inp[id] + gsf;
-        g = min(tg[id] - gsf, served);
+        const int q = bst + i;
+        id = tlog[q];
+        const int gsf = tl_g[q], tgv = tl_t[q];
+        eff = tl_e[q];
+        g = min(tgv - gsf, served);
         pad = lin - eff;
         inv = served - g;
         const int ng = gsf + g;
         gen[id] = ng;
-        sl[id] += 1;
-        done = ng >= tg[id] || ng >= C.G;
+        sl[id] = tl_s[q] + 1;
+        done = ng >= tgv || ng >= C.G;
       }
       const int cnt = min(32, bn - b0);
       sink.members(lane, cnt, id, eff, pad, g, inv);
@@ -710,16 +739,26 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       total_inv += __reduce_add_sync(FULL, ok ? inv : 0);
       const unsigned fm = __ballot_sync(FULL, ok && done);
       const unsigned pm = __ballot_sync(FULL, ok && !done);
-      if (ok && done) fin[nfin + __popc(fm & lt)] = id;
+      if (ok && done) fin[nfin + __popc(fm & lt)] = bst + i;
       if (ok && !done) pool[pool_len + __popc(pm & lt)] = id;
       nfin += __popc(fm);
       pool_len += __popc(pm);
     }
     __syncwarp();
-    for (int c0 = 0; c0 < nfin; c0 += 32) {
+    for (int c0 = 0; c0 < nfin; c0 += 32) {  // completions from the slot state
       const int cnt = min(32, nfin - c0);
-      const int id = lane < cnt ? fin[c0 + lane] : 0;
-      complete_chunk(cnt, id, w);
+      const int q = lane < cnt ? fin[c0 + lane] : 0;
+      const int id = lane < cnt ? tlog[q] : 0;
+      const double r = lane < cnt ? clock - tl_a[q] : 0.0;
+      const int s = lane < cnt ? tl_s[q] + 1 : 0;
+      if (lane < cnt) {
+        resp[completed + lane] = r;
+        if (hist && s < P.hist_bins) atomicAdd((unsigned long long*)&hist[s], 1ull);
+      }
+      for (int i = 0; i < cnt; ++i)
+        sink.record(lane, 5, clock, shfl_i(id, i), w, -1, 0, 0, 0, 0, 0.0, 0, 0, shfl_d(r, i), shfl_i(s, i), 0.0, 0);
+      completed += cnt;
+      if (cnt > 0) last_completion = clock;
     }
     if (lane == w) {
       last_end = fmax(last_end, clock);
@@ -967,6 +1006,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       }
       dirty = false;
     }
+    SIM_PROF(0);
     const double bound = fmin(na_t, C.horizon);
     if (next_arr <= bound) {  // next_arr = arr[cur], +INF once all arrived
       // Arrival(s): seq < n, so they precede any non-arrival event at the same time.
@@ -999,6 +1039,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         cur += cnt;
         next_arr = cur < n ? arr[cur] : dinf();
         __syncwarp();
+        SIM_PROF(1);
         continue;
       }
       const int id = cur++;
@@ -1044,7 +1085,9 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       if (POL == SCLS_POLICY_SCLS) {
         tick_t = dinf();
         tick_s = ~0ull;
+        SIM_PROF(8);
         status = scls_tick();
+        SIM_PROF(9);
         if (status != SCLS_OK) break;
       } else {  // SLS deferred dispatch check
         const int w = pf_w[pf_head];
@@ -1063,8 +1106,10 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           busy = 0;
           infl = -1;
         }
+        SIM_PROF(8);
         scls_done(w, b);
         start_next_scls(w);
+        SIM_PROF(10);
       } else if (POL == SCLS_POLICY_SLS) {
         sls_done(w);
       } else {
@@ -1074,6 +1119,11 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     __syncwarp();
   }
 
+  SIM_PROF(8);
+#ifdef SCLS_SIM_PROF
+  if (POL == SCLS_POLICY_SCLS && hist && P.hist_bins >= 16 && lane == 0)
+    for (int i = 0; i < 12; ++i) hist[4 + i] = prof[i];
+#endif
   // ---- report (metrics.cpp:30-117) ------------------------------------------------------
   if (status == SCLS_OK && (sink.n_events == 0 || completed == 0)) status = SCLS_ERR_EMPTY_LOG;
   double thr = 0.0, avg = 0.0, p95 = 0.0, ctstd = 0.0;

@@ -11,6 +11,7 @@ struct SimLayout {
   int64_t gen, sl, resp;                                  // per request
   int64_t pool, sk, sk2, sv, T, split, segs, tlog;        // SCLS tick
   int64_t b_start, b_n, b_lin, b_served, b_next, b_est;   // SCLS batches
+  int64_t tl_g, tl_t, tl_e, tl_s, tl_a;                   // SCLS slot state
   int64_t fifo, pf_t, pf_seq, pf_w, run, ex;              // SLS / ILS
   int64_t total;
 };
@@ -42,6 +43,15 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
     L.split = take(4 * (n1 + 1));
     L.segs = take(4 * (n1 + 1));
     L.tlog = take(4 * (cap + 1));
+    // per-slot request state captured when the slot is batched (the request's
+    // generated count, true gen, effective input, slices so far, arrival), so
+    // offload and batch completion read slot-contiguous memory instead of
+    // chasing request ids
+    L.tl_g = take(4 * (cap + 1));
+    L.tl_t = take(4 * (cap + 1));
+    L.tl_e = take(4 * (cap + 1));
+    L.tl_s = take(4 * (cap + 1));
+    L.tl_a = take(8 * (cap + 1));
     L.b_start = take(4 * (cap + 1));
     L.b_n = take(4 * (cap + 1));
     L.b_lin = take(4 * (cap + 1));
