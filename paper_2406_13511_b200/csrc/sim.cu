@@ -708,6 +708,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   // SCLS on_batch_done (sched_policies.cpp:149-188) for worker w, batch b.
   auto scls_done = [&](int w, int b) {
     const int bn = b_n[b], bst = b_start[b], lin = b_lin[b], served = b_served[b];
+    const double best = b_est[b];
     sink.record(lane, 4, clock, -1, w, b, bn, lin, C.S, served, 0.0, 0, 0, 0.0, 0, 0.0, bn);
     ++batch_count;
     batch_members += bn;
@@ -715,22 +716,28 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     const unsigned lt = (1u << lane) - 1u;
     int nfin = 0;
     int32_t* fin = sv;  // finished members' slots, member order (reused scratch)
+    // One chunk (bn <= 32, the common case): the completions come straight
+    // from the member registers, still after this chunk's member records.
+    const bool one = bn <= 32;
     for (int b0 = 0; b0 < bn; b0 += 32) {
       const int i = b0 + lane;
       const bool ok = i < bn;
-      int id = 0, eff = 0, g = 0, pad = 0, inv = 0;
+      int id = 0, eff = 0, g = 0, pad = 0, inv = 0, s1 = 0;
+      double ta = 0.0;
       bool done = false;
       if (ok) {
         const int q = bst + i;
         id = tlog[q];
         const int gsf = tl_g[q], tgv = tl_t[q];
         eff = tl_e[q];
+        s1 = tl_s[q] + 1;
+        if (one) ta = tl_a[q];
         g = min(tgv - gsf, served);
         pad = lin - eff;
         inv = served - g;
         const int ng = gsf + g;
         gen[id] = ng;
-        sl[id] = tl_s[q] + 1;
+        sl[id] = s1;
         done = ng >= tgv || ng >= C.G;
       }
       const int cnt = min(32, bn - b0);
@@ -739,10 +746,30 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       total_inv += __reduce_add_sync(FULL, ok ? inv : 0);
       const unsigned fm = __ballot_sync(FULL, ok && done);
       const unsigned pm = __ballot_sync(FULL, ok && !done);
-      if (ok && done) fin[nfin + __popc(fm & lt)] = bst + i;
       if (ok && !done) pool[pool_len + __popc(pm & lt)] = id;
-      nfin += __popc(fm);
       pool_len += __popc(pm);
+      if (one) {
+        const int cnt = __popc(fm);
+        const int pos = __popc(fm & lt);
+        const double r = clock - ta;
+        if (ok && done) {
+          resp[completed + pos] = r;
+          if (hist && s1 < P.hist_bins) atomicAdd((unsigned long long*)&hist[s1], 1ull);
+        }
+        if (kHash || kLog)
+          for (unsigned m = fm; m; m &= m - 1) {
+            const int src = __ffs(m) - 1;
+            sink.record(lane, 5, clock, shfl_i(id, src), w, -1, 0, 0, 0, 0, 0.0, 0, 0, shfl_d(r, src),
+                        shfl_i(s1, src), 0.0, 0);
+          }
+        else
+          sink.n_events += cnt;
+        completed += cnt;
+        if (cnt > 0) last_completion = clock;
+        break;
+      }
+      if (ok && done) fin[nfin + __popc(fm & lt)] = bst + i;
+      nfin += __popc(fm);
     }
     __syncwarp();
     for (int c0 = 0; c0 < nfin; c0 += 32) {  // completions from the slot state
@@ -762,7 +789,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     }
     if (lane == w) {
       last_end = fmax(last_end, clock);
-      load = load - b_est[b];  // offloader.cpp:56-59 complete_batch
+      load = load - best;  // offloader.cpp:56-59 complete_batch
       if (load < 0.0) load = 0.0;
     }
   };
