@@ -136,9 +136,11 @@ enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT
 /* SCLS_OPT_DP_KERNEL: 0 (default) picks the monotone decision kernel when the
  * model allows it and some window exceeds 32 rows, else the serial-chain
  * kernel; 1 forces the chain kernel; 2 forces the decision kernel when the
- * model allows it.  SCLS_OPT_SIM_CONCURRENT (default 1): the simulator's
- * per-policy launches run concurrently on forked streams (0: in sequence on
- * the context stream); results are identical either way. */
+ * model allows it.  SCLS_OPT_SIM_CONCURRENT (default 0): 1 runs the
+ * simulator's per-policy launches concurrently on forked streams instead of in
+ * sequence on the context stream (results are identical; on the C5 sweep the
+ * sequential order is faster: 124 vs 131 ms, the event-chain-bound ILS kernel
+ * loses more to shared SMs than the others gain). */
 scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value);
 /* Diagnostics: enable/disable clock64 phase counters in the DP chain kernel
  * and read-and-reset them (cycles: main chain, main barrier wait, helper
