@@ -4,11 +4,14 @@ Headline (BASELINE.json metric, configs[4]): simulated traces/s of the
 Monte Carlo sweep — 4096 traces (1024 seeds x arrival rates 10/15/20/25 req/s,
 600 s, 8 instances, S = 128, codefuse-like lengths, builtin latency model and
 rule-table memory) x the three policies {SCLS, SLS, ILS}: 12,288 simulations
-per step.  The trace dimension is sharded across ranks (contiguous ranges,
-strong scaling: the sweep is fixed as N grows); each rank simulates its
-shard on its GPU and the per-trace result records are all-gathered over NCCL
-(the only collective).  Device time, CUDA events on the launching stream,
-max over ranks.
+per step.  One step is the reference's sweep() (experiment.cpp:62-85:
+generate -> Simulator::run -> compute per run) through scls_run_sweep: the
+traces are generated on the device from their WorkloadSpecs (bit-exact with
+generate()), then every policy runs on every trace.  The trace dimension is
+sharded across ranks (contiguous ranges, strong scaling: the sweep is fixed as
+N grows); each rank generates and simulates its shard on its GPU and the
+per-trace result records are all-gathered over NCCL (the only collective).
+Device time, CUDA events on the launching stream, max over ranks.
 
 The same JSON line carries the scheduling-core number (configs[2]): requests
 scheduled/s for batch_requests + offload of the 1M-request pool
@@ -16,7 +19,8 @@ scheduled/s for batch_requests + offload of the 1M-request pool
 with its phase breakdown.
 
 Inputs are synthetic (the reference's own generators, exact); parity of the
-measured shard is checked against the C oracle outside the timed region.
+measured shard is checked against the C oracle and the host generator
+outside the timed region.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -166,12 +170,13 @@ def run_reference(args, rank, world):
     cores = os.cpu_count() or 1
     per = args.cpu_sample or max(8, min(64, cores * 4))
     ids = list(range(per))
-    traces = gen_traces(ids, args.duration, lib.generate)
     lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
     cfgs = [capi.sched_cfg(policy=p) for p in POLICIES]
 
     def step():
+        # experiment.cpp sweep on the host: generate each trace, run every policy
         t0 = time.perf_counter()
+        traces = gen_traces(ids, args.duration, lib.generate)
         for c in cfgs:
             lib.simulate(traces, c, lat, mem, threads=cores)
         return time.perf_counter() - t0
@@ -188,7 +193,7 @@ def run_reference(args, rank, world):
             "config": {"workload": f"C5 sweep sample: {per} traces x 3 policies (600 s, 8 instances, "
                                    "S=128, rates 10/15/20/25)", "host_threads": cores},
             "cpu_baseline": {"value": value, "unit": "traces/s", "cores": cores, "kind": kind,
-                             "sample": f"{per} traces x 3 policies per step"},
+                             "sample": f"{per} traces per step: generate once + 3 policies"},
             "e2e": {"value": value, "unit": "traces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -279,6 +284,16 @@ def run_ours(args, rank, world, dist):
     ctx.set_digests(False)  # the reference's sweep reports metrics only
     cfg_arr = (capi.SchedCfg * 3)(*cfgs)
 
+    spec_arr = (capi.WorkloadSpec * ntr)(*[trace_spec(i, args.duration) for i in ids])
+
+    def sweep_step():
+        # experiment.cpp sweep: generate every trace on the device
+        # (workload.cpp:163-181, bit-exact) and run every policy on it
+        st = ctx.lib.scls_run_sweep(ctx.h, ntr, spec_arr, 3, cfg_arr, C.byref(lat), C.byref(mem),
+                                    C.cast(C.c_void_p(d_res_all.data_ptr()), C.POINTER(capi.TraceResult)),
+                                    hist_bins, C.c_void_p(d_hist.data_ptr()), None, capi.MEM_DEVICE)
+        ctx._check(st)
+
     def sim_grid():
         # every policy on every trace (experiment.cpp sweep), inputs staged once
         st = ctx.lib.scls_simulate_grid(ctx.h, ntr, C.c_void_p(d_offs.data_ptr()), C.c_void_p(d_arr.data_ptr()),
@@ -305,7 +320,7 @@ def run_ours(args, rank, world, dist):
         return [sweep.gather_records(d_res[k].view(ntr, nfields), T, world, dist) for k in range(3)]
 
     def step():
-        sim_grid()
+        sweep_step()
         gather()
 
     for _ in range(args.warmup):
@@ -317,9 +332,11 @@ def run_ours(args, rank, world, dist):
     with ClockSampler(local) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        gen_ms = []
         for _ in range(args.steps):
-            sim_grid()
+            sweep_step()
             launches += ctx.launches()
+            gen_ms.append(ctx.timings()["generate"])
             gather()
         e1.record(stream)
         torch.cuda.synchronize()
@@ -340,25 +357,42 @@ def run_ours(args, rank, world, dist):
             sim_policy(k)
             kernel_ms[POLICIES[k]].append(ctx.timings()["simulate"])
 
-    # e2e through the public C-ABI with host buffers (H2D inputs, D2H results):
-    # inputs staged once in pinned host memory and copied to the device inside
-    # every call (scls_simulate_grid with SCLS_MEM_HOST: each trace once, all
-    # three policies on it)
-    p_offs = torch.from_numpy(offs).pin_memory().numpy()
-    p_arr = torch.from_numpy(arr).pin_memory().numpy()
-    p_inp = torch.from_numpy(inp).pin_memory().numpy()
-    p_gen = torch.from_numpy(gen).pin_memory().numpy()
+    # e2e through the public C-ABI with host buffers: scls_run_sweep takes the
+    # WorkloadSpecs from host memory (H2D inside the call), generates and
+    # simulates on the device, and returns the result records and histograms
+    # to host memory (D2H inside the call) — the reference's sweep() call shape
+    specs_host = [trace_spec(i, args.duration) for i in ids]
     e2e_t = []
     for _ in range(max(2, args.steps // 2)):
         t0 = time.perf_counter()
-        ctx.simulate_grid_flat(p_offs, p_arr, p_inp, p_gen, cfgs, lat, mem, hist_bins=hist_bins)
+        ctx.run_sweep(specs_host, cfgs, lat, mem, hist_bins=hist_bins)
         e2e_t.append(time.perf_counter() - t0)
     e2e_local = statistics.median(e2e_t)
     t_e2e = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    h2d = nreq * 16 + (ntr + 1) * 8
+    h2d = ntr * C.sizeof(capi.WorkloadSpec)
     d2h = 3 * ntr * (C.sizeof(capi.TraceResult) + 8 * hist_bins)
+
+    # the simulator alone on pre-generated traces: device-resident inputs, and
+    # e2e with the 16 B/request inputs copied from pinned host memory per call
+    sim_only = []
+    for _ in range(max(2, args.steps // 2)):
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        sim_grid()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        sim_only.append(s0.elapsed_time(s1))
+    p_offs = torch.from_numpy(offs).pin_memory().numpy()
+    p_arr = torch.from_numpy(arr).pin_memory().numpy()
+    p_inp = torch.from_numpy(inp).pin_memory().numpy()
+    p_gen = torch.from_numpy(gen).pin_memory().numpy()
+    sim_e2e = []
+    for _ in range(max(2, args.steps // 2)):
+        t0 = time.perf_counter()
+        ctx.simulate_grid_flat(p_offs, p_arr, p_inp, p_gen, cfgs, lat, mem, hist_bins=hist_bins)
+        sim_e2e.append(time.perf_counter() - t0)
 
     # parity of this rank's first traces vs the C oracle (outside the timed region)
     ctx.set_digests(True)
@@ -373,6 +407,12 @@ def run_ours(args, rank, world, dist):
             for f, _ in capi.TraceResult._fields_:
                 if f != "sim_clock" and getattr(a[i], f) != getattr(b[i], f):
                     bad += 1
+    # device generation parity on the whole shard: run_sweep == simulate_grid on
+    # the host-generated traces, every result word of every job
+    sweep_step()
+    r_sweep = d_res_all.clone()
+    sim_grid()
+    gen_mismatch = int((r_sweep.view(3 * ntr, nfields) != d_res_all.view(3 * ntr, nfields)).any(dim=1).sum().item())
     statuses = set()
     for kk in range(3):
         r = d_res[kk].view(ntr, nfields).cpu().numpy()
@@ -390,12 +430,13 @@ def run_ours(args, rank, world, dist):
         "metric": METRIC, "value": value, "unit": "traces/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generators: mt19937_64 Poisson arrivals, codefuse-like lengths)",
-        "config": {"workload": f"C5 Monte Carlo sweep: {T} traces (seeds x rates 10/15/20/25 req/s), "
-                               f"{args.duration:.0f} s, 8 instances, S=128, max_gen 1024, x {{SCLS,SLS,ILS}} "
-                               f"= {3 * T} simulations per step",
+        "data": "synthetic: every step generates its traces on the device from WorkloadSpecs (the reference "
+                "sampler: mt19937_64, glibc log gaps, codefuse-like lengths; bit-exact with generate())",
+        "config": {"workload": f"C5 Monte Carlo sweep (experiment.cpp sweep: generate + simulate + metrics): "
+                               f"{T} traces (seeds x rates 10/15/20/25 req/s), {args.duration:.0f} s, 8 instances, "
+                               f"S=128, max_gen 1024, x {{SCLS,SLS,ILS}} = {3 * T} simulations per step",
                    "traces": T, "requests_per_rank": nreq, "parallelism": f"trace-sharded dp{world}",
-                   "l2": "inputs (%.0f MB) > L2 per rank" % (nreq * 16 / 1e6)},
+                   "l2": "generated traces (%.0f MB per rank) > L2, rewritten every step" % (nreq * 16 / 1e6)},
         "e2e": {"value": 3 * T / float(t_e2e.item()), "unit": "traces/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
@@ -406,8 +447,14 @@ def run_ours(args, rank, world, dist):
                      "note": "event-chain latency/issue bound (ncu: profiles/ncu_summary.json); algorithmic "
                              "bytes = 16 B/request in + result records out"},
         "kernel_ms_per_policy": pol_ms,
-        "parity": {"checked": f"{k} traces x 3 policies vs C oracle, all TraceResult fields bit-exact",
-                   "mismatches": bad, "statuses": sorted(statuses)},
+        "generate_ms_per_step": statistics.median(gen_ms),
+        "simulate_only": {"value": 3 * ntr / (statistics.median(sim_only) / 1e3),
+                          "e2e_value": 3 * ntr / statistics.median(sim_e2e), "unit": "traces/s",
+                          "note": "scls_simulate_grid on host-generated traces (this rank); e2e copies "
+                                  "16 B/request from pinned host memory per call"},
+        "parity": {"checked": f"{k} traces x 3 policies vs C oracle, all TraceResult fields bit-exact; "
+                              f"device-generated sweep vs host-generated traces, all {3 * ntr} jobs of this rank",
+                   "mismatches": bad, "generate_mismatches": gen_mismatch, "statuses": sorted(statuses)},
         "clocks": clk.summary(),
     }
     if not args.no_c3:
@@ -428,14 +475,14 @@ def cpu_baseline(args):
         lib, kind = OracleLib(ORACLE_SO), "port"
     cores = os.cpu_count() or 1
     per = args.cpu_sample or max(8, min(64, cores * 4))
-    traces = gen_traces(list(range(per)), args.duration, lib.generate)
     lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
     t0 = time.perf_counter()
+    traces = gen_traces(list(range(per)), args.duration, lib.generate)
     for p in POLICIES:
         lib.simulate(traces, capi.sched_cfg(policy=p), lat, mem, threads=cores)
     sec = time.perf_counter() - t0
     out = {"value": 3 * per / sec, "unit": "traces/s", "cores": cores, "kind": kind,
-           "sample": f"{per} traces x 3 policies of the C5 sweep, {cores} host threads"}
+           "sample": f"{per} traces of the C5 sweep: generate once + 3 policies, {cores} host threads"}
     # C3 single-thread (the reference API is one serial call)
     eff, arr, ids, _ = (OracleLib(ORACLE_SO)).make_pool(1 << 20, 7)
     t0 = time.perf_counter()

@@ -125,7 +125,9 @@ size_t scls_last_error(const scls_ctx* ctx, char* buf, size_t cap);
 int64_t scls_last_request_id(const scls_ctx* ctx);
 /* Device time (ms, CUDA events on the context stream) of the phases of the
  * last call: [0]=total, [1]=sort, [2]=estimate/window tables, [3]=DP chain,
- * [4]=backtrack+emit, [5]=offload, [6]=simulate. */
+ * [4]=backtrack+emit, [5]=offload, [6]=simulate, [7]=device trace generation
+ * (scls_run_sweep / scls_generate_batch) or, after a batcher call, 1.0 when
+ * the monotone DP kernel ran. */
 void scls_last_timings(const scls_ctx* ctx, float out_ms[8]);
 /* Number of CUDA kernel launches issued by the last call. */
 int64_t scls_last_launch_count(const scls_ctx* ctx);
@@ -312,6 +314,32 @@ scls_status scls_simulate_grid(scls_ctx* ctx, int32_t n_traces, const int64_t* r
                                const scls_memory* memm, scls_trace_result* results,
                                int32_t hist_bins, int64_t* slice_hist, scls_event_log* log,
                                int32_t mem);
+
+/* The sweep entry point with generation on the device: experiment.h:37,52-53
+ * run_experiment / sweep (experiment.cpp:39-85 = generate -> Simulator::run ->
+ * compute per run).  Trace t is generated from specs[t] on the device
+ * (workload.cpp:163-181, bit-exact: mt19937_64, top-53-bit uniforms, glibc
+ * 2.39's log for the gaps; uniform and histogram lengths — log-normal specs
+ * fail with SCLS_ERR_ERROR), then every config runs on every trace exactly as
+ * scls_simulate_grid (job j = c * n_traces + t).  specs / cfgs are host
+ * structs; `mem` places results / slice_hist / log.  Timings: [7] = generation. */
+scls_status scls_run_sweep(scls_ctx* ctx, int32_t n_traces, const scls_workload_spec* specs,
+                           int32_t n_cfgs, const scls_sched_cfg* cfgs, const scls_latency* lat,
+                           const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
+                           int64_t* slice_hist, scls_event_log* log, int32_t mem);
+
+/* workload.h:78 generate for n_specs traces at once, on the device (same
+ * sampler and restrictions as scls_run_sweep).  Trace t's requests are
+ * [req_offset[t], req_offset[t+1]) of the concatenated outputs (ids = arrival
+ * ranks); req_offset has n_specs + 1 entries.  SCLS_ERR_CAPACITY (req_offset
+ * still filled) when the total exceeds `cap`.  `mem` places the outputs. */
+scls_status scls_generate_batch(scls_ctx* ctx, int32_t n_specs, const scls_workload_spec* specs,
+                                int64_t cap, int64_t* req_offset, double* arrival,
+                                int32_t* input_len, int32_t* gen_len, int32_t mem);
+
+/* Diagnostics: the device port of glibc's log (csrc/glibc_log.cuh) on n
+ * inputs, for the bit-exactness check against the host libm. */
+scls_status scls_debug_log(scls_ctx* ctx, int64_t n, const double* x, double* y, int32_t mem);
 
 /* ---- workload: workload.h:78 generate ------------------------------------
  * Host-side Poisson trace generation (mt19937_64 + glibc log, the reference's

@@ -52,8 +52,9 @@ enum ScratchSlot : int {
   kSlotRadixOffs = 31,
   kSlotScan = 40,     // 40..55: two per recursion level
   kSlotStage = 60,    // 60..79: host<->device staging of entry-point arguments
-  kSlotSim = 80,      // 80..99: simulator
-  kNumSlots = 100,
+  kSlotSim = 80,      // 80..109: simulator
+  kSlotGen = 110,     // 110..119: device trace generation
+  kNumSlots = 120,
 };
 
 // Status plumbing shared by the C-ABI entry points.

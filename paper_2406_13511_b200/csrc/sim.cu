@@ -1359,19 +1359,23 @@ extern "C" scls_status scls_validate_memory(const scls_memory* m);
 
 // The simulator entry (shared by scls_simulate and scls_simulate_grid): job j
 // runs source trace src[j] (identity when null) under config job_cfg[j].
+// in_mem: where arrival/input_len/gen_len and req_offset live (SCLS_MEM_HOST,
+// SCLS_MEM_DEVICE, or kMemDeviceArrays: arrays on the device, req_offset on
+// the host); mem: where results / slice_hist / log live.
+constexpr int32_t kMemDeviceArrays = 2;
 static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* req_offset, const double* arrival,
                                  const int32_t* input_len, const int32_t* gen_len, int32_t n_cfgs,
                                  const scls_sched_cfg* cfgs, int32_t n_traces, const std::vector<int32_t>& h_src,
                                  const std::vector<int32_t>& h_idx, const scls_latency* lat,
                                  const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
-                                 int64_t* slice_hist, scls_event_log* log, int32_t mem) {
+                                 int64_t* slice_hist, scls_event_log* log, int32_t mem, int32_t in_mem) {
   // n_traces counts jobs below; h_off / inputs are per source trace.
   const bool has_src = !h_src.empty();
   const bool cfg_index = !h_idx.empty();
   cudaStream_t s = ctx->stream;
   // Host-side copies of the small arguments.
   std::vector<int64_t> h_off(n_src + 1);
-  if (mem == SCLS_MEM_DEVICE) {
+  if (in_mem == SCLS_MEM_DEVICE) {
     SCLS_CUDA(cudaMemcpy(h_off.data(), req_offset, sizeof(int64_t) * (n_src + 1), cudaMemcpyDeviceToHost));
   } else {
     std::memcpy(h_off.data(), req_offset, sizeof(int64_t) * (n_src + 1));
@@ -1414,7 +1418,7 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   int32_t* d_idx = cfg_index ? (int32_t*)ctx->buf(kSlotSim + 3, sizeof(int32_t) * n_traces) : nullptr;
   if (!d_off || !d_cfg || !d_ok || (cfg_index && !d_idx)) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
   SCLS_CUDA(cudaEventRecord(ctx->ev[0], s));
-  if (mem == SCLS_MEM_HOST && total > 0) {
+  if (in_mem == SCLS_MEM_HOST && total > 0) {
     double* a = (double*)ctx->buf(kSlotSim + 4, sizeof(double) * total);
     int32_t* b = (int32_t*)ctx->buf(kSlotSim + 5, sizeof(int32_t) * total);
     int32_t* g = (int32_t*)ctx->buf(kSlotSim + 6, sizeof(int32_t) * total);
@@ -1671,7 +1675,7 @@ extern "C" scls_status scls_simulate(scls_ctx* ctx, int32_t n_traces, const int6
       if (v < 0 || v >= n_cfgs) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "cfg_index out of range");
   }
   return simulate_core(ctx, n_traces, req_offset, arrival, input_len, gen_len, n_cfgs, cfgs, n_traces, {}, h_idx,
-                       lat, memm, results, hist_bins, slice_hist, log, mem);
+                       lat, memm, results, hist_bins, slice_hist, log, mem, mem);
 }
 
 extern "C" scls_status scls_simulate_grid(scls_ctx* ctx, int32_t n_traces, const int64_t* req_offset,
@@ -1697,5 +1701,51 @@ extern "C" scls_status scls_simulate_grid(scls_ctx* ctx, int32_t n_traces, const
     h_idx[j] = j / n_traces;
   }
   return simulate_core(ctx, n_traces, req_offset, arrival, input_len, gen_len, n_cfgs, cfgs, n_jobs, h_src, h_idx,
-                       lat, memm, results, hist_bins, slice_hist, log, mem);
+                       lat, memm, results, hist_bins, slice_hist, log, mem, mem);
+}
+
+namespace scls {
+scls_status generate_device(scls_ctx* ctx, int32_t n_specs, const scls_workload_spec* specs,
+                            std::vector<int64_t>& h_off, double** arr, int32_t** inp, int32_t** gen);
+}
+
+extern "C" scls_status scls_run_sweep(scls_ctx* ctx, int32_t n_traces, const scls_workload_spec* specs,
+                                      int32_t n_cfgs, const scls_sched_cfg* cfgs, const scls_latency* lat,
+                                      const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
+                                      int64_t* slice_hist, scls_event_log* log, int32_t mem) {
+  if (!ctx) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null context");
+  ctx->err.clear();
+  ctx->err_request = -1;
+  ctx->launches = 0;
+  std::fill(ctx->timings, ctx->timings + 8, 0.f);
+  SCLS_CUDA(cudaSetDevice(ctx->device));
+  if (n_traces < 0 || n_cfgs < 1 || !cfgs || !lat || !memm || !results || (n_traces > 0 && !specs) ||
+      hist_bins < 0 || (hist_bins > 0 && !slice_hist) || (int64_t)n_traces * n_cfgs > INT32_MAX)
+    return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (n_traces == 0) return SCLS_OK;
+  cudaStream_t s = ctx->stream;
+  SCLS_CUDA(cudaEventRecord(ctx->ev[14], s));
+  std::vector<int64_t> h_off;
+  double* d_arr = nullptr;
+  int32_t* d_inp = nullptr;
+  int32_t* d_gen = nullptr;
+  scls_status st = generate_device(ctx, n_traces, specs, h_off, &d_arr, &d_inp, &d_gen);
+  if (st) return st;
+  SCLS_CUDA(cudaEventRecord(ctx->ev[15], s));
+  const int32_t n_jobs = n_traces * n_cfgs;
+  std::vector<int32_t> h_src(n_jobs), h_idx(n_jobs);
+  for (int32_t j = 0; j < n_jobs; ++j) {
+    h_src[j] = j % n_traces;
+    h_idx[j] = j / n_traces;
+  }
+  // offsets on the host, request arrays on the device
+  st = simulate_core(ctx, n_traces, h_off.data(), d_arr, d_inp, d_gen, n_cfgs, cfgs, n_jobs, h_src, h_idx, lat,
+                     memm, results, hist_bins, slice_hist, log, mem, kMemDeviceArrays);
+  if (st) return st;
+  float gen_ms = 0.f, all_ms = 0.f;
+  cudaEventElapsedTime(&gen_ms, ctx->ev[14], ctx->ev[15]);
+  cudaEventElapsedTime(&all_ms, ctx->ev[14], ctx->ev[3]);
+  ctx->timings[7] = gen_ms;
+  ctx->timings[0] = all_ms;
+  return SCLS_OK;
 }

@@ -49,29 +49,42 @@ int draw_length(const scls_length_dist& d, int limit, std::mt19937_64& g) {
   return truncate_len(draw_int(d.edges[bucket], d.edges[bucket + 1], g), limit);
 }
 
-scls_status check_dist(const scls_length_dist& d) {
+scls_status check_dist(scls_ctx* ctx, const scls_length_dist& d) {
   using scls::set_error;
   if (d.kind == SCLS_DIST_UNIFORM) {
-    if (d.lo < 1 || d.hi < d.lo) return set_error(nullptr, SCLS_ERR_ERROR, "uniform length distribution requires 1 <= lo <= hi");
+    if (d.lo < 1 || d.hi < d.lo) return set_error(ctx, SCLS_ERR_ERROR, "uniform length distribution requires 1 <= lo <= hi");
   } else if (d.kind == SCLS_DIST_LOGNORMAL) {
-    if (!(d.sigma > 0.0) || d.cap < 1) return set_error(nullptr, SCLS_ERR_ERROR, "log-normal length distribution requires sigma > 0 and cap >= 1");
+    if (!(d.sigma > 0.0) || d.cap < 1) return set_error(ctx, SCLS_ERR_ERROR, "log-normal length distribution requires sigma > 0 and cap >= 1");
   } else if (d.kind == SCLS_DIST_HISTOGRAM) {
-    if (d.n_buckets < 1 || d.n_buckets > SCLS_MAX_BUCKETS) return set_error(nullptr, SCLS_ERR_ERROR, "histogram needs k weights and k+1 edges, k >= 1");
+    if (d.n_buckets < 1 || d.n_buckets > SCLS_MAX_BUCKETS) return set_error(ctx, SCLS_ERR_ERROR, "histogram needs k weights and k+1 edges, k >= 1");
     for (int i = 0; i < d.n_buckets; ++i)
-      if (d.edges[i] < 1 || d.edges[i] > d.edges[i + 1]) return set_error(nullptr, SCLS_ERR_ERROR, "histogram edges must be >= 1 and non-decreasing");
+      if (d.edges[i] < 1 || d.edges[i] > d.edges[i + 1]) return set_error(ctx, SCLS_ERR_ERROR, "histogram edges must be >= 1 and non-decreasing");
     double total = 0.0;
     for (int i = 0; i < d.n_buckets; ++i) {
-      if (d.weights[i] < 0.0) return set_error(nullptr, SCLS_ERR_ERROR, "histogram weights must be non-negative");
+      if (d.weights[i] < 0.0) return set_error(ctx, SCLS_ERR_ERROR, "histogram weights must be non-negative");
       total += d.weights[i];
     }
-    if (std::abs(total - 1.0) > 1e-9) return set_error(nullptr, SCLS_ERR_ERROR, "histogram weights must sum to 1 within 1e-9");
+    if (std::abs(total - 1.0) > 1e-9) return set_error(ctx, SCLS_ERR_ERROR, "histogram weights must sum to 1 within 1e-9");
   } else {
-    return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "unknown length distribution kind");
+    return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "unknown length distribution kind");
   }
   return SCLS_OK;
 }
 
 }  // namespace
+
+namespace scls {
+// validate(const WorkloadSpec&) (workload.cpp:84-98), shared with the device
+// generator (workload_gen.cu).
+scls_status validate_workload_spec(scls_ctx* ctx, const scls_workload_spec& spec) {
+  if (!(spec.rate > 0.0)) return set_error(ctx, SCLS_ERR_ERROR, "workload rate must be > 0");
+  if (spec.duration_s < 0.0) return set_error(ctx, SCLS_ERR_ERROR, "workload duration must be >= 0");
+  if (spec.max_input_limit < 1 || spec.max_gen_limit < 1) return set_error(ctx, SCLS_ERR_ERROR, "length limits must be >= 1");
+  scls_status st = check_dist(ctx, spec.input_len_dist);
+  if (st) return st;
+  return check_dist(ctx, spec.gen_len_dist);
+}
+}  // namespace scls
 
 extern "C" scls_status scls_generate(const scls_workload_spec* spec, int64_t cap, int64_t* n, double* arrival,
                                      int32_t* input_len, int32_t* gen_len) {
@@ -79,12 +92,8 @@ extern "C" scls_status scls_generate(const scls_workload_spec* spec, int64_t cap
   if (!spec || !n || (cap > 0 && (!arrival || !input_len || !gen_len)))
     return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "bad arguments");
   *n = 0;
-  if (!(spec->rate > 0.0)) return set_error(nullptr, SCLS_ERR_ERROR, "workload rate must be > 0");
-  if (spec->duration_s < 0.0) return set_error(nullptr, SCLS_ERR_ERROR, "workload duration must be >= 0");
-  if (spec->max_input_limit < 1 || spec->max_gen_limit < 1) return set_error(nullptr, SCLS_ERR_ERROR, "length limits must be >= 1");
-  scls_status st = check_dist(spec->input_len_dist);
+  scls_status st = scls::validate_workload_spec(nullptr, *spec);
   if (st) return st;
-  if ((st = check_dist(spec->gen_len_dist))) return st;
   std::mt19937_64 g(spec->seed);
   double clock = 0.0;
   int64_t k = 0;

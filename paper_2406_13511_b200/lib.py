@@ -31,6 +31,7 @@ EXPORTS = [
     "scls_batch_serve_time", "scls_would_oom", "scls_max_batch_size",
     "scls_batch_requests", "scls_offload", "scls_schedule", "scls_simulate",
     "scls_simulate_grid", "scls_generate", "scls_make_pool", "scls_debug_dp_profile", "scls_set_option",
+    "scls_run_sweep", "scls_generate_batch", "scls_debug_log",
 ]
 
 
@@ -84,6 +85,10 @@ def load():
         "scls_make_pool": (i32, [i64, C.c_uint64, vp, vp, vp, vp]),
         "scls_debug_dp_profile": (i32, [vp, i32, vp]),
         "scls_set_option": (i32, [vp, i32, i64]),
+        "scls_run_sweep": (i32, [vp, i32, P(capi.WorkloadSpec), i32, S, L, M,
+                                 P(capi.TraceResult), i32, vp, P(capi.EventLog), i32]),
+        "scls_generate_batch": (i32, [vp, i32, P(capi.WorkloadSpec), i64, vp, vp, vp, vp, i32]),
+        "scls_debug_log": (i32, [vp, i64, vp, vp, i32]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -145,11 +150,13 @@ class Context:
 
     def timings(self):
         """Device ms of the last call: total, sort, estimate, dp, backtrack+emit,
-        offload, simulate."""
+        offload, simulate, generate."""
         out = (C.c_float * 8)()
         self.lib.scls_last_timings(self.h, out)
-        return dict(zip(["total", "sort", "estimate", "dp", "backtrack", "offload", "simulate", "dp_mono"],
-                        list(out)))
+        d = dict(zip(["total", "sort", "estimate", "dp", "backtrack", "offload", "simulate", "generate"],
+                     list(out)))
+        d["dp_mono"] = d["generate"]  # slot 7 of a batcher call: 1.0 when the monotone DP kernel ran
+        return d
 
     def set_digests(self, on):
         """SCLS_OPT_SIM_DIGESTS: compute the per-trace log digests (default on)."""
@@ -336,6 +343,61 @@ class Context:
                                                 capi.MEM_HOST))
         # flat job order: res[c * ntr + t]
         return res, hist[:ntr * nc * hist_bins].reshape(nc, ntr, hist_bins)
+
+    # -- device trace generation (workload.h:78) and the sweep (experiment.h:37,52-53) --
+    def generate_batch(self, specs):
+        """generate() for every spec on the device -> (req_offset, arrival, input_len, gen_len)."""
+        specs = list(specs)
+        n = len(specs)
+        sp = (capi.WorkloadSpec * max(n, 1))(*specs)
+        offs = np.zeros(n + 1, np.int64)
+        st = self.lib.scls_generate_batch(self.h, n, sp, 0, _ptr(offs), None, None, None, capi.MEM_HOST)
+        if st not in (0, capi.ERR_CAPACITY):
+            self._check(st)
+        tot = int(offs[-1])
+        arr = np.zeros(max(tot, 1), np.float64)
+        inp = np.zeros(max(tot, 1), np.int32)
+        gen = np.zeros(max(tot, 1), np.int32)
+        self._check(self.lib.scls_generate_batch(self.h, n, sp, tot, _ptr(offs), _ptr(arr), _ptr(inp), _ptr(gen),
+                                                 capi.MEM_HOST))
+        return offs, arr[:tot], inp[:tot], gen[:tot]
+
+    def run_sweep(self, specs, cfgs, lat, mem, hist_bins=64, n_logged=0, rec_cap=0, mem_cap=0):
+        """scls_run_sweep: generate every trace on the device, then every config
+        on every trace.  Returns (results, hist[, log]); results[c * ntr + t]."""
+        if isinstance(cfgs, capi.SchedCfg):
+            cfgs = [cfgs]
+        specs = list(specs)
+        ntr, nc = len(specs), len(cfgs)
+        sp = (capi.WorkloadSpec * max(ntr, 1))(*specs)
+        cfg_arr = (capi.SchedCfg * nc)(*cfgs)
+        res = (capi.TraceResult * max(ntr * nc, 1))()
+        hist = np.zeros(max(ntr * nc * hist_bins, 1), np.int64)
+        log = None
+        if n_logged:
+            recs = (capi.EventRecord * (n_logged * rec_cap))()
+            mems = (capi.Member * max(n_logged * mem_cap, 1))()
+            rc = np.zeros(n_logged, np.int64)
+            mc = np.zeros(n_logged, np.int64)
+            st = capi.EventLog(n_logged, rec_cap, mem_cap, recs, mems,
+                               rc.ctypes.data_as(C.POINTER(C.c_int64)),
+                               mc.ctypes.data_as(C.POINTER(C.c_int64)))
+            log = dict(struct=st, records=recs, members=mems, rec_count=rc, mem_count=mc,
+                       rec_cap=rec_cap, mem_cap=mem_cap)
+        self._check(self.lib.scls_run_sweep(self.h, ntr, sp, nc, cfg_arr, C.byref(lat), C.byref(mem), res,
+                                            hist_bins, _ptr(hist), C.byref(log["struct"]) if log else None,
+                                            capi.MEM_HOST))
+        hist = hist[:ntr * nc * hist_bins].reshape(nc, ntr, hist_bins)
+        if log is not None:
+            return res, hist, log
+        return res, hist
+
+    def debug_log(self, x):
+        """The device port of glibc log on x (float64 array)."""
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros_like(x)
+        self._check(self.lib.scls_debug_log(self.h, len(x), _ptr(x), _ptr(y), capi.MEM_HOST))
+        return y
 
 
 def _flatten(traces):

@@ -1,0 +1,192 @@
+"""Device trace generation: generate() on the B200,
+bit-exact with the reference's sampler (workload.cpp:100-181).
+
+CPU tests pin the ingredient the device cannot take from the reference: the
+port of glibc 2.39's FMA-variant `log` (csrc/glibc_log.cuh, constants from
+tools/extract_glibc_log.py), compiled for the host and compared bit for bit
+with this image's libm over 30M inputs.  GPU tests compare the device port
+with libm, scls_generate_batch with the host generator and the compiled
+reference, and scls_run_sweep with scls_simulate_grid on host-generated
+traces (every TraceResult field)."""
+import ctypes as C
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+from paper_2406_13511_b200 import capi
+from tests.conftest import ROOT
+from tests.helpers import MEMORIES
+
+CSRC = os.path.join(ROOT, "paper_2406_13511_b200", "csrc")
+
+CHECK_SRC = r"""
+#include "glibc_log.cuh"
+#include <cmath>
+#include <cstdio>
+#include <random>
+int main() {
+  std::mt19937_64 g(1);
+  long bad = 0, n = 0;
+  auto chk = [&](double x) {
+    const double a = std::log(x), b = scls_glibc::log_fma(x);
+    ++n;
+    if (scls_glibc::f_bits(a) != scls_glibc::f_bits(b) && !(std::isnan(a) && std::isnan(b))) {
+      if (bad < 5) std::printf("x=%a libm=%a port=%a\n", x, a, b);
+      ++bad;
+    }
+  };
+  for (int i = 0; i < 20000000; ++i) chk(1.0 - (double)(g() >> 11) * 0x1p-53);   // the sampler's domain
+  for (int i = 0; i < 5000000; ++i) chk(0.93 + (double)(g() >> 11) * 0x1p-53 * 0.15);  // near-1 path
+  for (int i = 0; i < 5000000; ++i) chk(scls_glibc::f_dbl(g()));                 // every bit pattern
+  for (double x : {0.0, -0.0, 1.0, (double)INFINITY, -1.0, (double)NAN, 0x1p-1074, 0x1p-1060, 0x1p-53, 0x1.fffffffffffffp-1})
+    chk(x);
+  std::printf("n=%ld bad=%ld\n", n, bad);
+  return bad != 0;
+}
+"""
+
+LIBM_SRC = r"""
+#include <math.h>
+#include <stdint.h>
+void libm_log(int64_t n, const double* x, double* y) { for (int64_t i = 0; i < n; ++i) y[i] = log(x[i]); }
+"""
+
+
+def _build(src, name, shared=False):
+    d = tempfile.mkdtemp(prefix="scls_glog_")
+    path = os.path.join(d, name + (".cpp" if not shared else ".c"))
+    with open(path, "w") as f:
+        f.write(src)
+    out = os.path.join(d, name + (".so" if shared else ""))
+    cmd = (["gcc", "-O2", "-shared", "-fPIC", path, "-o", out, "-lm"] if shared else
+           ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-I", CSRC, path, "-o", out])
+    subprocess.run(cmd, check=True, capture_output=True)
+    return out
+
+
+def test_glibc_log_port_matches_libm_on_host():
+    exe = _build(CHECK_SRC, "glog_check")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout
+    assert "bad=0" in r.stdout
+
+
+def test_log_table_matches_this_libm(tmp_path):
+    """The committed constants are the ones this image's libm carries."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("extract", os.path.join(ROOT, "tools", "extract_glibc_log.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.OUT = str(tmp_path / "glibc_log_data.h")
+    mod.main()
+    want = open(os.path.join(CSRC, "glibc_log_data.h")).read().split("\n", 1)[1]
+    got = open(mod.OUT).read().split("\n", 1)[1]
+    assert got == want
+
+
+# ------------------------------------------------------------------------------------------
+def _specs():
+    """A spread of WorkloadSpecs: histogram (codefuse-like, long-gen) and
+    uniform lengths, tight limits, tiny and empty traces, many seeds/rates."""
+    out = []
+    for i in range(48):
+        out.append(capi.workload_spec(rate=float(1 + i % 25), duration_s=float(20 + 13 * (i % 7)), seed=7000 + i))
+    out.append(capi.workload_spec(rate=20.0, duration_s=600.0, seed=42))
+    out.append(capi.workload_spec(rate=2.0, duration_s=500.0, seed=42))
+    out.append(capi.workload_spec(rate=5.0, duration_s=0.0, seed=1))           # empty trace
+    out.append(capi.workload_spec(rate=0.01, duration_s=3.0, seed=3))          # almost surely empty
+    out.append(capi.workload_spec(rate=50.0, duration_s=100.0, gen_dist=capi.long_gen_dist(), seed=9))
+    u = capi.uniform_dist(1, 2000)
+    out.append(capi.workload_spec(rate=30.0, duration_s=100.0, input_dist=u, gen_dist=capi.uniform_dist(5, 700),
+                                  max_input_limit=1500, max_gen_limit=300, seed=11))
+    out.append(capi.workload_spec(rate=8.0, duration_s=200.0, input_dist=u, seed=2 ** 63 + 5))
+    out.append(capi.workload_spec(rate=1000.0, duration_s=30.0, max_input_limit=100, max_gen_limit=50, seed=0))
+    return out
+
+
+@pytest.mark.gpu
+def test_device_log_matches_libm(ctx):
+    so = _build(LIBM_SRC, "libm_log", shared=True)
+    libm = C.CDLL(so)
+    libm.libm_log.argtypes = [C.c_int64, C.c_void_p, C.c_void_p]
+    rng = np.random.default_rng(5)
+    u = (rng.integers(0, 2 ** 53, 4_000_000, dtype=np.int64).astype(np.float64)) * 2.0 ** -53
+    x = np.concatenate([1.0 - u, 0.93 + 0.15 * u[:1_000_000],
+                        rng.integers(0, 2 ** 63, 1_000_000, dtype=np.int64).view(np.float64),
+                        np.array([0.0, -0.0, 1.0, np.inf, -1.0, np.nan, 5e-324, 2.0 ** -1060, 2.0 ** -53])])
+    want = np.zeros_like(x)
+    libm.libm_log(len(x), x.ctypes.data, want.ctypes.data)
+    got = ctx.debug_log(x)
+    nan = np.isnan(want) & np.isnan(got)
+    bad = (got.view(np.int64) != want.view(np.int64)) & ~nan
+    assert not bad.any(), (x[bad][:5], got[bad][:5], want[bad][:5])
+
+
+@pytest.mark.gpu
+def test_generate_batch_matches_host_and_reference(ctx, orc):
+    from oracle import pyoracle
+    from paper_2406_13511_b200 import lib
+    ref = pyoracle.ref_lib()
+    specs = _specs()
+    offs, arr, inp, gen = ctx.generate_batch(specs)
+    for t, sp in enumerate(specs):
+        a, b, g = lib.generate(sp)  # host generator (std::log)
+        lo, hi = offs[t], offs[t + 1]
+        assert hi - lo == len(a), t
+        assert np.array_equal(arr[lo:hi].view(np.int64), np.asarray(a).view(np.int64)), t
+        assert np.array_equal(inp[lo:hi], b) and np.array_equal(gen[lo:hi], g), t
+        want = (ref or orc).generate(sp)
+        assert np.array_equal(arr[lo:hi].view(np.int64), np.asarray(want[0], np.float64).view(np.int64)), t
+        assert np.array_equal(inp[lo:hi], want[1]) and np.array_equal(gen[lo:hi], want[2]), t
+
+
+@pytest.mark.gpu
+def test_generate_batch_large_sweep_fingerprint(ctx):
+    """The bench's C5 traces (1024 seeds x 4 rates, 600 s): device == host, all 4096."""
+    from paper_2406_13511_b200 import lib
+    specs = [capi.workload_spec(rate=(10.0, 15.0, 20.0, 25.0)[i % 4], duration_s=600.0, seed=1000 + i // 4)
+             for i in range(4096)]
+    offs, arr, inp, gen = ctx.generate_batch(specs)
+    rng = np.random.default_rng(0)
+    for t in sorted(set(rng.integers(0, 4096, 64).tolist()) | {0, 4095}):
+        a, b, g = lib.generate(specs[t])
+        lo, hi = offs[t], offs[t + 1]
+        assert hi - lo == len(a)
+        assert np.array_equal(arr[lo:hi].view(np.int64), np.asarray(a).view(np.int64))
+        assert np.array_equal(inp[lo:hi], b) and np.array_equal(gen[lo:hi], g)
+    assert ctx.timings()["generate"] > 0
+
+
+@pytest.mark.gpu
+def test_run_sweep_equals_simulate_grid(ctx):
+    from paper_2406_13511_b200 import lib
+    lat, mem = capi.builtin_latency_model(), MEMORIES["rule"]()
+    specs = _specs()
+    cfgs = [capi.sched_cfg(policy=p) for p in ("scls", "sls", "ils")] + \
+           [capi.sched_cfg(policy="scls", slice_len=64, worker_count=3, max_gen_limit=512)]
+    a, ha = ctx.run_sweep(specs, cfgs, lat, mem, hist_bins=16)
+    traces = [lib.generate(s) for s in specs]
+    b, hb = ctx.simulate_grid(traces, cfgs, lat, mem, hist_bins=16)
+    n = len(specs)
+    for c in range(len(cfgs)):
+        for t in range(n):
+            for f, _ in capi.TraceResult._fields_:
+                assert getattr(a[c * n + t], f) == getattr(b[c][t], f), (c, t, f)
+    assert np.array_equal(ha, hb)
+
+
+@pytest.mark.gpu
+def test_run_sweep_errors(ctx):
+    lat, mem = capi.builtin_latency_model(), MEMORIES["rule"]()
+    from paper_2406_13511_b200.lib import SclsError
+    bad = capi.workload_spec(rate=-1.0)
+    with pytest.raises(SclsError) as e:
+        ctx.run_sweep([bad], [capi.sched_cfg(policy="scls")], lat, mem)
+    assert e.value.name == "Error" and "rate" in str(e.value)
+    ln = capi.workload_spec(rate=5.0, duration_s=10.0, gen_dist=capi.lognormal_dist(5.0, 1.0, 1024))
+    with pytest.raises(SclsError) as e:
+        ctx.run_sweep([ln], [capi.sched_cfg(policy="scls")], lat, mem)
+    assert "log-normal" in str(e.value)
