@@ -328,6 +328,15 @@ scls_status scls_run_sweep(scls_ctx* ctx, int32_t n_traces, const scls_workload_
                            const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
                            int64_t* slice_hist, scls_event_log* log, int32_t mem);
 
+/* experiment.h:37 run_experiment for n_runs independent runs (the body of the
+ * reference's sweep loop, experiment.cpp:67-83): run i generates specs[i] on
+ * the device and simulates it under cfgs[i].  Same generator, statuses and
+ * per-run results as scls_run_sweep (results indexed by run). */
+scls_status scls_run_experiments(scls_ctx* ctx, int32_t n_runs, const scls_workload_spec* specs,
+                                 const scls_sched_cfg* cfgs, const scls_latency* lat,
+                                 const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
+                                 int64_t* slice_hist, scls_event_log* log, int32_t mem);
+
 /* workload.h:78 generate for n_specs traces at once, on the device (same
  * sampler and restrictions as scls_run_sweep).  Trace t's requests are
  * [req_offset[t], req_offset[t+1]) of the concatenated outputs (ids = arrival

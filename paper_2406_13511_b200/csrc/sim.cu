@@ -1709,37 +1709,45 @@ scls_status generate_device(scls_ctx* ctx, int32_t n_specs, const scls_workload_
                             std::vector<int64_t>& h_off, double** arr, int32_t** inp, int32_t** gen);
 }
 
-extern "C" scls_status scls_run_sweep(scls_ctx* ctx, int32_t n_traces, const scls_workload_spec* specs,
-                                      int32_t n_cfgs, const scls_sched_cfg* cfgs, const scls_latency* lat,
-                                      const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
-                                      int64_t* slice_hist, scls_event_log* log, int32_t mem) {
+// Generate n_specs traces on the device, then run the jobs (h_src, h_idx) on
+// them; grid = true builds the every-config-on-every-trace job list.
+static scls_status run_generated(scls_ctx* ctx, int32_t n_specs, const scls_workload_spec* specs, int32_t n_cfgs,
+                                 const scls_sched_cfg* cfgs, bool grid, const scls_latency* lat,
+                                 const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
+                                 int64_t* slice_hist, scls_event_log* log, int32_t mem) {
   if (!ctx) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null context");
   ctx->err.clear();
   ctx->err_request = -1;
   ctx->launches = 0;
   std::fill(ctx->timings, ctx->timings + 8, 0.f);
   SCLS_CUDA(cudaSetDevice(ctx->device));
-  if (n_traces < 0 || n_cfgs < 1 || !cfgs || !lat || !memm || !results || (n_traces > 0 && !specs) ||
-      hist_bins < 0 || (hist_bins > 0 && !slice_hist) || (int64_t)n_traces * n_cfgs > INT32_MAX)
+  if (n_specs < 0 || n_cfgs < 1 || !cfgs || !lat || !memm || !results || (n_specs > 0 && !specs) ||
+      hist_bins < 0 || (hist_bins > 0 && !slice_hist) || (int64_t)n_specs * n_cfgs > INT32_MAX ||
+      (!grid && n_cfgs != n_specs))
     return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad arguments");
-  if (n_traces == 0) return SCLS_OK;
+  if (n_specs == 0) return SCLS_OK;
   cudaStream_t s = ctx->stream;
   SCLS_CUDA(cudaEventRecord(ctx->ev[14], s));
   std::vector<int64_t> h_off;
   double* d_arr = nullptr;
   int32_t* d_inp = nullptr;
   int32_t* d_gen = nullptr;
-  scls_status st = generate_device(ctx, n_traces, specs, h_off, &d_arr, &d_inp, &d_gen);
+  scls_status st = generate_device(ctx, n_specs, specs, h_off, &d_arr, &d_inp, &d_gen);
   if (st) return st;
   SCLS_CUDA(cudaEventRecord(ctx->ev[15], s));
-  const int32_t n_jobs = n_traces * n_cfgs;
-  std::vector<int32_t> h_src(n_jobs), h_idx(n_jobs);
-  for (int32_t j = 0; j < n_jobs; ++j) {
-    h_src[j] = j % n_traces;
-    h_idx[j] = j / n_traces;
+  const int32_t n_jobs = grid ? n_specs * n_cfgs : n_specs;
+  std::vector<int32_t> h_src, h_idx(n_jobs);
+  if (grid) {
+    h_src.resize(n_jobs);
+    for (int32_t j = 0; j < n_jobs; ++j) {
+      h_src[j] = j % n_specs;
+      h_idx[j] = j / n_specs;
+    }
+  } else {
+    for (int32_t j = 0; j < n_jobs; ++j) h_idx[j] = j;
   }
   // offsets on the host, request arrays on the device
-  st = simulate_core(ctx, n_traces, h_off.data(), d_arr, d_inp, d_gen, n_cfgs, cfgs, n_jobs, h_src, h_idx, lat,
+  st = simulate_core(ctx, n_specs, h_off.data(), d_arr, d_inp, d_gen, n_cfgs, cfgs, n_jobs, h_src, h_idx, lat,
                      memm, results, hist_bins, slice_hist, log, mem, kMemDeviceArrays);
   if (st) return st;
   float gen_ms = 0.f, all_ms = 0.f;
@@ -1748,4 +1756,20 @@ extern "C" scls_status scls_run_sweep(scls_ctx* ctx, int32_t n_traces, const scl
   ctx->timings[7] = gen_ms;
   ctx->timings[0] = all_ms;
   return SCLS_OK;
+}
+
+extern "C" scls_status scls_run_sweep(scls_ctx* ctx, int32_t n_traces, const scls_workload_spec* specs,
+                                      int32_t n_cfgs, const scls_sched_cfg* cfgs, const scls_latency* lat,
+                                      const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
+                                      int64_t* slice_hist, scls_event_log* log, int32_t mem) {
+  return run_generated(ctx, n_traces, specs, n_cfgs, cfgs, true, lat, memm, results, hist_bins, slice_hist, log,
+                       mem);
+}
+
+extern "C" scls_status scls_run_experiments(scls_ctx* ctx, int32_t n_runs, const scls_workload_spec* specs,
+                                            const scls_sched_cfg* cfgs, const scls_latency* lat,
+                                            const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
+                                            int64_t* slice_hist, scls_event_log* log, int32_t mem) {
+  return run_generated(ctx, n_runs, specs, n_runs, cfgs, false, lat, memm, results, hist_bins, slice_hist, log,
+                       mem);
 }

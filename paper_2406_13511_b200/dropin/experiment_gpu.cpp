@@ -3,9 +3,12 @@
 // workload → Simulator::run, now on the B200 → compute).  sweep
 // (experiment.h:52-53) is the data-parallel entry point: instead of one run
 // after another it builds every run of the sweep and simulates all of them
-// in ONE scls_simulate call (one warp per trace), reading the reports the
-// device computes online (metrics.cpp:30-117, bit for bit).  Errors surface
-// in value order, as the sequential reference would raise them.
+// in ONE call (one warp per trace), reading the reports the device computes
+// online (metrics.cpp:30-117, bit for bit).  Generated workloads with uniform
+// or histogram lengths are generated on the device too (scls_run_experiments,
+// bit-exact with generate()); trace files and log-normal lengths are loaded /
+// generated on the host and simulated with scls_simulate.  Errors surface in
+// value order, as the sequential reference would raise them.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -50,6 +53,43 @@ RunConfig with_value(const RunConfig& base, const std::string& param, double val
   return cfg;
 }
 
+// Whether generate(cfg.workload) can run on the device (scls_run_experiments).
+bool device_generated(const RunConfig& cfg) {
+  const WorkloadSpec& w = cfg.workload;
+  auto ok = [](const LengthDist& d) {
+    return d.kind == LengthDist::Kind::kUniform ||
+           (d.kind == LengthDist::Kind::kHistogram && d.weights.size() <= SCLS_MAX_BUCKETS);
+  };
+  return !cfg.workload_from_trace && ok(w.input_len_dist) && ok(w.gen_len_dist);
+}
+
+scls_length_dist to_c(const LengthDist& d) {
+  scls_length_dist c{};
+  c.kind = d.kind == LengthDist::Kind::kUniform ? SCLS_DIST_UNIFORM
+           : d.kind == LengthDist::Kind::kLogNormal ? SCLS_DIST_LOGNORMAL : SCLS_DIST_HISTOGRAM;
+  c.lo = d.lo;
+  c.hi = d.hi;
+  c.mu = d.mu;
+  c.sigma = d.sigma;
+  c.cap = d.cap;
+  c.n_buckets = static_cast<int32_t>(d.weights.size());
+  for (std::size_t i = 0; i < d.edges.size() && i <= SCLS_MAX_BUCKETS; ++i) c.edges[i] = d.edges[i];
+  for (std::size_t i = 0; i < d.weights.size() && i < SCLS_MAX_BUCKETS; ++i) c.weights[i] = d.weights[i];
+  return c;
+}
+
+scls_workload_spec to_c(const WorkloadSpec& w) {
+  scls_workload_spec c{};
+  c.rate = w.rate;
+  c.duration_s = w.duration_s;
+  c.input_len_dist = to_c(w.input_len_dist);
+  c.gen_len_dist = to_c(w.gen_len_dist);
+  c.max_input_limit = w.max_input_limit;
+  c.max_gen_limit = w.max_gen_limit;
+  c.seed = w.seed;
+  return c;
+}
+
 }  // namespace
 
 RunResult run_experiment(const RunConfig& cfg) {
@@ -71,6 +111,8 @@ std::vector<SweepRow> sweep(const RunConfig& base, const std::string& param,
   // Host preparation per value; failures are deferred so they surface in value order.
   std::vector<std::exception_ptr> early(nv);
   std::vector<std::vector<Request>> work(nv);
+  std::vector<char> on_dev(nv, 0);
+  std::vector<scls_workload_spec> specs(nv);
   std::vector<scls_sched_cfg> cfgs(nv);
   std::vector<scls_latency> lats(nv);
   std::vector<scls_memory> mems(nv);
@@ -79,7 +121,13 @@ std::vector<SweepRow> sweep(const RunConfig& base, const std::string& param,
       const RunConfig cfg = with_value(base, param, values[v]);
       const LatencyModel lat = resolve_latency_model(cfg.latency_model_path);
       const MemoryModel mem = resolve_memory_model(cfg.memory_model_path);
-      work[v] = load_workload(cfg);
+      if (device_generated(cfg)) {
+        validate(cfg.workload);  // generate()'s own check, same exception
+        specs[v] = to_c(cfg.workload);
+        on_dev[v] = 1;
+      } else {
+        work[v] = load_workload(cfg);
+      }
       Simulator check(cfg.sched, lat, mem, cfg.horizon_s);  // constructor validation
       cfgs[v] = b200::to_c(cfg.sched, cfg.horizon_s);
       lats[v] = b200::to_c(lat);
@@ -102,7 +150,8 @@ std::vector<SweepRow> sweep(const RunConfig& base, const std::string& param,
     if (early[v0] || done[v0]) continue;
     std::vector<std::size_t> group;
     for (std::size_t v = v0; v < nv; ++v)
-      if (!early[v] && !done[v] && std::memcmp(&lats[v], &lats[v0], sizeof(scls_latency)) == 0 &&
+      if (!early[v] && !done[v] && on_dev[v] == on_dev[v0] &&
+          std::memcmp(&lats[v], &lats[v0], sizeof(scls_latency)) == 0 &&
           std::memcmp(&mems[v], &mems[v0], sizeof(scls_memory)) == 0)
         group.push_back(v);
     std::vector<int64_t> offs(1, 0);
@@ -121,9 +170,16 @@ std::vector<SweepRow> sweep(const RunConfig& base, const std::string& param,
     }
     std::vector<scls_trace_result> gr(group.size());
     std::vector<int64_t> gh(group.size() * hist_bins);
-    b200::check(ctx, scls_simulate(ctx, static_cast<int32_t>(group.size()), offs.data(), arr.data(), inp.data(),
-                                   gen.data(), static_cast<int32_t>(gc.size()), gc.data(), idx.data(), &lats[v0],
-                                   &mems[v0], gr.data(), hist_bins, gh.data(), nullptr, SCLS_MEM_HOST));
+    if (on_dev[v0]) {
+      std::vector<scls_workload_spec> gs;
+      for (std::size_t v : group) gs.push_back(specs[v]);
+      b200::check(ctx, scls_run_experiments(ctx, static_cast<int32_t>(group.size()), gs.data(), gc.data(), &lats[v0],
+                                            &mems[v0], gr.data(), hist_bins, gh.data(), nullptr, SCLS_MEM_HOST));
+    } else {
+      b200::check(ctx, scls_simulate(ctx, static_cast<int32_t>(group.size()), offs.data(), arr.data(), inp.data(),
+                                     gen.data(), static_cast<int32_t>(gc.size()), gc.data(), idx.data(), &lats[v0],
+                                     &mems[v0], gr.data(), hist_bins, gh.data(), nullptr, SCLS_MEM_HOST));
+    }
     for (std::size_t g = 0; g < group.size(); ++g) {
       res[group[g]] = gr[g];
       std::copy(gh.begin() + g * hist_bins, gh.begin() + (g + 1) * hist_bins, hist.begin() + group[g] * hist_bins);

@@ -31,7 +31,7 @@ EXPORTS = [
     "scls_batch_serve_time", "scls_would_oom", "scls_max_batch_size",
     "scls_batch_requests", "scls_offload", "scls_schedule", "scls_simulate",
     "scls_simulate_grid", "scls_generate", "scls_make_pool", "scls_debug_dp_profile", "scls_set_option",
-    "scls_run_sweep", "scls_generate_batch", "scls_debug_log",
+    "scls_run_sweep", "scls_run_experiments", "scls_generate_batch", "scls_debug_log",
 ]
 
 
@@ -87,6 +87,8 @@ def load():
         "scls_set_option": (i32, [vp, i32, i64]),
         "scls_run_sweep": (i32, [vp, i32, P(capi.WorkloadSpec), i32, S, L, M,
                                  P(capi.TraceResult), i32, vp, P(capi.EventLog), i32]),
+        "scls_run_experiments": (i32, [vp, i32, P(capi.WorkloadSpec), S, L, M,
+                                       P(capi.TraceResult), i32, vp, P(capi.EventLog), i32]),
         "scls_generate_batch": (i32, [vp, i32, P(capi.WorkloadSpec), i64, vp, vp, vp, vp, i32]),
         "scls_debug_log": (i32, [vp, i64, vp, vp, i32]),
     }
@@ -391,6 +393,19 @@ class Context:
         if log is not None:
             return res, hist, log
         return res, hist
+
+    def run_experiments(self, specs, cfgs, lat, mem, hist_bins=64):
+        """scls_run_experiments: run i = generate(specs[i]) simulated under cfgs[i]."""
+        specs, cfgs = list(specs), list(cfgs)
+        n = len(specs)
+        assert len(cfgs) == n
+        sp = (capi.WorkloadSpec * max(n, 1))(*specs)
+        cfg_arr = (capi.SchedCfg * max(n, 1))(*cfgs)
+        res = (capi.TraceResult * max(n, 1))()
+        hist = np.zeros(max(n * hist_bins, 1), np.int64)
+        self._check(self.lib.scls_run_experiments(self.h, n, sp, cfg_arr, C.byref(lat), C.byref(mem), res,
+                                                  hist_bins, _ptr(hist), None, capi.MEM_HOST))
+        return res, hist[:n * hist_bins].reshape(n, hist_bins)
 
     def debug_log(self, x):
         """The device port of glibc log on x (float64 array)."""

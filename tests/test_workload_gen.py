@@ -190,3 +190,22 @@ def test_run_sweep_errors(ctx):
     with pytest.raises(SclsError) as e:
         ctx.run_sweep([ln], [capi.sched_cfg(policy="scls")], lat, mem)
     assert "log-normal" in str(e.value)
+
+
+@pytest.mark.gpu
+def test_run_experiments_equals_simulate(ctx):
+    """experiment.cpp sweep body: run i = generate(specs[i]) under cfgs[i]."""
+    from paper_2406_13511_b200 import lib
+    lat, mem = capi.builtin_latency_model(), MEMORIES["rule"]()
+    specs = _specs()
+    pols = ("scls", "sls", "ils")
+    cfgs = [capi.sched_cfg(policy=pols[i % 3], slice_len=(32, 64, 128, 256)[i % 4],
+                           worker_count=1 + i % 8, max_gen_limit=512 if i % 4 < 3 else 1024)
+            for i in range(len(specs))]
+    a, ha = ctx.run_experiments(specs, cfgs, lat, mem, hist_bins=40)
+    traces = [lib.generate(s) for s in specs]
+    b, hb = ctx.simulate(traces, cfgs, lat, mem, cfg_index=list(range(len(specs))), hist_bins=40)
+    for t in range(len(specs)):
+        for f, _ in capi.TraceResult._fields_:
+            assert getattr(a[t], f) == getattr(b[t], f), (t, f)
+    assert np.array_equal(ha, hb)

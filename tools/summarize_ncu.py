@@ -63,7 +63,8 @@ def report(path, names):
     rows = list(csv.reader(io.StringIO(raw)))
     h = rows[0]
     units = rows[1]
-    scale = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "byte": 1.0, "Kbyte": 1e3,
+    scale = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1.0, "us": 1e3, "ms": 1e6,
+             "s": 1e9, "byte": 1.0, "Kbyte": 1e3,
              "Mbyte": 1e6, "Gbyte": 1e9}
 
     def val(r, m):
