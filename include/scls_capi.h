@@ -134,7 +134,7 @@ int64_t scls_last_launch_count(const scls_ctx* ctx);
 /* Context options.  SCLS_OPT_SIM_DIGESTS (default 1): scls_simulate fills
  * the h_* log digests of scls_trace_result; 0 skips them (the metrics are
  * computed either way, and the digests are zero). */
-enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT = 3 };
+enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT = 3, SCLS_OPT_ILS_KERNEL = 4 };
 /* SCLS_OPT_DP_KERNEL: 0 (default) picks the monotone decision kernel when the
  * model allows it and some window exceeds 32 rows, else the serial-chain
  * kernel; 1 forces the chain kernel; 2 forces the decision kernel when the
@@ -142,7 +142,10 @@ enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT
  * simulator's per-policy launches concurrently on forked streams instead of in
  * sequence on the context stream (results are identical; on the C5 sweep the
  * sequential order is faster: 124 vs 131 ms, the event-chain-bound ILS kernel
- * loses more to shared SMs than the others gain). */
+ * loses more to shared SMs than the others gain).  SCLS_OPT_ILS_KERNEL
+ * (default 0): metrics-only ILS runs every instance in its own lane and
+ * merges the completions (csrc/sim_ils_indep.cuh); 1 forces the lock-step
+ * kernel that processes the global event order directly (results identical). */
 scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value);
 /* Diagnostics: enable/disable clock64 phase counters in the DP chain kernel
  * and read-and-reset them (cycles: main chain, main barrier wait, helper

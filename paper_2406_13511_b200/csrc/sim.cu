@@ -1277,6 +1277,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, POL == SCLS_POLICY_SCLS ? SCLS
 }  // namespace scls
 
 #include "sim_ils.cuh"
+#include "sim_ils_indep.cuh"
 
 namespace scls {
 namespace {
@@ -1583,6 +1584,8 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
     SCLS_CUDA(cudaMemcpyAsync(d_lists, flat.data(), sizeof(int32_t) * n_traces, cudaMemcpyHostToDevice, s));
   }
   const bool hash = ctx->sim_digests;
+  int32_t* d_fb = (int32_t*)ctx->buf(kSlotSim + 24, sizeof(int32_t) * (n_traces + 1));  // ILS fallback list
+  if (!d_fb) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
   // Per-policy launches; with more than one policy they run concurrently on
   // forked streams so one kernel's tail overlaps the others' work.
   int n_pol = 0;
@@ -1614,7 +1617,15 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   else sim_kernel<POLV, false, false><<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);
     if (pol == SCLS_POLICY_SCLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SCLS) }
     else if (pol == SCLS_POLICY_SLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SLS) }
-    else if (!want_log && !hash) sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);
+    else if (!want_log && !hash && ctx->ils_lockstep) sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, nullptr);
+    else if (!want_log && !hash) {
+      // independent instance lanes; jobs with an exact cross-instance time tie
+      // are re-run by the lock-step kernel from a device-side list
+      SCLS_CUDA(cudaMemsetAsync(d_fb, 0, sizeof(int32_t), ls));
+      sim_ils_indep_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, d_fb, d_fb + 1);
+      SCLS_LAUNCHED();
+      sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, d_fb + 1, cnt, d_fb);
+    }
     else { SCLS_SIM_LAUNCH(SCLS_POLICY_ILS) }
 #undef SCLS_SIM_LAUNCH
     SCLS_LAUNCHED();

@@ -13,6 +13,7 @@ struct SimLayout {
   int64_t b_start, b_n, b_lin, b_served, b_next, b_est;   // SCLS batches
   int64_t tl_g, tl_t, tl_e, tl_s, tl_a;                   // SCLS slot state
   int64_t fifo, pf_t, pf_seq, pf_w, run, ex;              // SLS / ILS
+  int64_t ct, cp, cr, ra;                                 // ILS completion records, slot arrivals
   int64_t total;
 };
 
@@ -67,6 +68,10 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
     L.fifo = take(4 * (W * cap_w + 1));
     L.run = take(16 * ((int64_t)W * mc + 1));
     L.ex = take(4 * ((int64_t)mc + 1));
+    L.ct = take(8 * (W * cap_w + 1));
+    L.cp = take(8 * (W * cap_w + 1));
+    L.cr = take(8 * (W * cap_w + 1));
+    L.ra = take(8 * ((int64_t)W * mc + 1));
   }
   L.total = o;
   return L;

@@ -154,10 +154,14 @@ __device__ void finish_report(int lane, scls_trace_result* R, int status, int n,
     const double span = last_completion - first_arrival;
     const double comp = (double)completed;
     thr = span > 0.0 ? __ddiv_rn(comp, span) : 0.0;
+    // sequential sum in completion order (metrics.cpp:83-85): coalesced loads,
+    // then 32 dependent DADDs per chunk on broadcast values (every lane holds it)
     double sum = 0.0;
-    if (lane == 0)
-      for (int i = 0; i < completed; ++i) sum = __dadd_rn(sum, resp[i]);
-    sum = shfl_d(sum, 0);
+    for (int c = 0; c < completed; c += 32) {
+      const double v = c + lane < completed ? resp[c + lane] : 0.0;
+      const int m = min(32, completed - c);
+      for (int j = 0; j < m; ++j) sum = __dadd_rn(sum, shfl_d(v, j));
+    }
     avg = __ddiv_rn(sum, comp);
     const size_t rk = (size_t)ceil(__dmul_rn(0.95, comp));
     int want = (int)(rk > 1 ? rk : 1) - 1;
@@ -233,7 +237,9 @@ __device__ void finish_report(int lane, scls_trace_result* R, int status, int n,
 #define SCLS_ILS_MINB 7  // 28 warps/SM: one wave for 4096 traces, 72 registers
 #endif
 __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_MINB)
-    sim_ils_lean_kernel(SimParams P, const int32_t* __restrict__ list, int32_t count) {
+    sim_ils_lean_kernel(SimParams P, const int32_t* __restrict__ list, int32_t count,
+                        const int32_t* __restrict__ dcount) {
+  if (dcount) count = *dcount;  // fallback launches: the job count lives on the device
   __shared__ int32_t sbins[kSimWarps][256];
   __shared__ int4 srun[kSimWarps][kIlsRunSmem];
   __shared__ uint8_t sown[kSimWarps][kOwnBuckets];

@@ -1,0 +1,418 @@
+// sim_ils_indep.cuh — metrics-only ILS simulator with independent instance
+// lanes (included by sim.cu after sim_ils.cuh).
+//
+// ILS instances never interact.  Arrivals are assigned round-robin in id
+// order (sched_policies.cpp:279-281), so instance w sees exactly the requests
+// w, w + W, w + 2W, ...; its boundaries (sched_policies.cpp:292-391) read and
+// write only its own queue, running set and segment, and its wake-up fires
+// after the arrivals that share its instant (seq < n, sim_engine.cpp:116-119).
+// The reference's global (time, seq) order therefore matters for exactly one
+// report field: avg_response_s sums the responses in global completion order
+// (metrics.cpp:83-85).  Everything else is a count, a max, a per-worker value
+// or an order-free selection (p95).
+//
+// So lane w simulates instance w on its own, at its own pace — no warp
+// reduction per event, and an unchanged iteration costs one dependent DADD
+// (the step time depends only on the context length, so it is computed ahead)
+// — and records each completion as (t, push time of its boundary, response).
+// A W-way warp merge then replays the completions in the reference's order:
+// by time, then by the push order of the completing boundaries.  Two
+// boundaries of different instances at the same time were pushed by their
+// instances' previous boundaries, so the earlier push time wins; an exact tie
+// of both times would need the push order one level further back, and such a
+// job is handed to the exact lock-step kernel (sim_ils_lean_kernel) through a
+// device-side fallback list instead.
+//
+// NonTermination (sim_engine.cpp:160-164): EndOfRun (horizon, seq n) precedes
+// every boundary at or after the horizon and every arrival after it, so the
+// run fails iff some instance still has work when its next event reaches it.
+#pragma once
+
+namespace scls {
+namespace {
+
+struct IlsRec {
+  double* t;   // completion time
+  double* tp;  // push time of the completing boundary (its instance's previous boundary)
+  double* r;   // response (t - arrival)
+};
+
+constexpr int kMergeWin = 256;  // merge window entries per warp (time key + response), reused as p95 bins
+#ifndef SCLS_ILS_INDEP_MINB
+#define SCLS_ILS_INDEP_MINB 4
+#endif
+
+__global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
+    sim_ils_indep_kernel(SimParams P, const int32_t* __restrict__ list, int32_t count, int32_t* __restrict__ fb_count,
+                         int32_t* __restrict__ fb_list) {
+  __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
+  __shared__ double swin_r[kSimWarps][kMergeWin];
+  __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
+  __shared__ int4 srun[kSimWarps][2][kIlsRunSmem];   // running slots, ping-pong
+  __shared__ double sra[kSimWarps][2][kIlsRunSmem];  // their arrival times
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * kSimWarps + warp;
+  if (g >= count) return;
+  const int t = list[g];
+  int32_t* bins = (int32_t*)swin_t[warp];  // p95 bins (after the merge)
+  const int ts = P.src ? P.src[t] : t;
+  const int64_t r0 = P.req_off[ts];
+  const int n = (int)(P.req_off[ts + 1] - r0);
+  const double* __restrict__ arr = P.arr + r0;
+  const int32_t* __restrict__ inp = P.inp + r0;
+  const int32_t* __restrict__ tg = P.tg + r0;
+  const int ci = P.cfg_index ? P.cfg_index[t] : 0;
+  const int W = P.cfgs[ci].W, MC = P.cfgs[ci].MC, G = P.cfgs[ci].G;
+  const double horizon = P.cfgs[ci].horizon;
+  const Lat& lat = P.lat;
+  scls_trace_result* R = &P.res[t];
+  int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
+
+  int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
+  if (status == SCLS_OK) {
+    int bad = 0;
+    for (int i = 1 + lane; i < n; i += 32) bad |= arr[i] < arr[i - 1];
+    if (__any_sync(FULL, bad)) status = SCLS_ERR_ERROR;
+  }
+  if (hist)
+    for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
+  if (status != SCLS_OK) {
+    finish_report(lane, R, status, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0);
+    return;
+  }
+  if (W * MC > kIlsRunSmem) {  // running slots do not fit this warp's shared memory
+    if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
+    return;
+  }
+  char* base = P.arena + P.trace_base[t];
+  const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_ILS, P.trace_cap[t], MC);
+  double* resp = (double*)(base + Lay.resp);
+  const int64_t cap_w = (n + W - 1) / W;
+
+#ifdef SCLS_ILS_PROF  // debug build: per-phase clock64 totals into hist[4..7]
+  long long t_a = clock64();
+#endif
+  // ---- phase 1: lane w simulates instance w ------------------------------------------
+  int comp = 0, batch_count = 0, n_disp = 0, stuck = 0;
+  long long batch_members = 0, n_ev = 0;
+#ifdef SCLS_ILS_PROF
+  long long pc_fast = 0, pc_slow = 0, pc_arr = 0, pc_outer = 0, cy_fast = 0, cy_arr = 0, cy_slow = 0;
+  __shared__ unsigned long long s_trips[kSimWarps][2];
+  if (lane == 0) s_trips[warp][0] = s_trips[warp][1] = 0;
+  __syncwarp();
+#endif
+  double last_end = 0.0, last_comp = -dinf();
+  {
+    const int w = lane;
+    const bool active = lane < W;
+    // running slots {join iteration, min(gen, G), input, -} + their arrival
+    // times, in running order; a boundary compacts from one buffer to the other
+    int4* run = srun[warp][0] + w * MC;
+    double* ra = sra[warp][0] + w * MC;
+    int4* run2 = srun[warp][1] + w * MC;
+    double* ra2 = sra[warp][1] + w * MC;
+    IlsRec rec{(double*)(base + Lay.ct) + w * cap_w, (double*)(base + Lay.cp) + w * cap_w,
+               (double*)(base + Lay.cr) + w * cap_w};
+    const int n_mine = active && w < n ? (n - 1 - w) / W + 1 : 0;  // requests w, w + W, ...
+    int f_head = 0, f_tail = 0;  // joined / arrived (FIFO as counters)
+    int n_run = 0, it_cnt = 0, seg_it = 0, seg_n = 0, room = 0;
+    bool seg = false, boundary = false;
+    double ev_t = dinf(), t_push = 0.0;
+    double a1 = 0.0, a2 = 0.0, dl = 0.0;  // step-time terms of the current membership, next context
+    // request stream prefetch: the next two arrivals, and the next join's data
+    double next_arr = n_mine > 0 ? arr[w] : dinf();
+    double next_arr2 = n_mine > 1 ? arr[w + W] : dinf();
+    double j_a = n_mine > 0 ? arr[w] : 0.0;
+    int j_i = n_mine > 0 ? inp[w] : 0, j_g = n_mine > 0 ? tg[w] : 0;
+    bool live = n_mine > 0;
+    auto step = [&](double x) {
+      return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a1, x), a2), __dmul_rn(lat.d3, x)), lat.d4);
+    };
+    // Each outer trip: this lane's run of unchanged iterations (four per inner
+    // trip, branch-free), then its next arrival or membership-changing boundary.
+    for (;;) {
+      const double stop = fmin(next_arr, horizon);
+      if (live && boundary && n_run > 0 && !(f_tail > f_head && n_run < MC)) {
+        while (room > 0 && ev_t < stop) {
+          const double x1 = __dadd_rn(dl, 1.0), x2 = __dadd_rn(dl, 2.0), x3 = __dadd_rn(dl, 3.0),
+                       x4 = __dadd_rn(dl, 4.0);
+          const double s0 = step(dl), s1 = step(x1), s2 = step(x2), s3 = step(x3);
+          const double b1 = __dadd_rn(ev_t, s0), b2 = __dadd_rn(b1, s1), b3 = __dadd_rn(b2, s2),
+                       b4 = __dadd_rn(b3, s3);
+          const bool c1 = (room > 1) & (b1 < stop);
+          const bool c2 = c1 & (room > 2) & (b2 < stop);
+          const bool c3 = c2 & (room > 3) & (b3 < stop);
+          const int k = 1 + (int)c1 + (int)c2 + (int)c3;
+          t_push = c3 ? b3 : (c2 ? b2 : (c1 ? b1 : ev_t));
+          ev_t = c3 ? b4 : (c2 ? b3 : (c1 ? b2 : b1));
+          dl = c3 ? x4 : (c2 ? x3 : (c1 ? x2 : x1));
+          room -= k;
+          it_cnt += k;
+          seg_it += k;
+#ifdef SCLS_ILS_PROF
+          pc_fast += k;
+          if (lane == __ffs(__activemask()) - 1) ++s_trips[warp][0];
+#endif
+        }
+      }
+      const bool arrive = live && next_arr <= ev_t && next_arr <= horizon;
+      const bool slow = live && !arrive && boundary && ev_t < next_arr && ev_t < horizon;
+      if (!__any_sync(FULL, arrive || slow)) break;
+#ifdef SCLS_ILS_PROF
+      if (lane == 0) ++s_trips[warp][1];
+#endif
+      if (arrive) {
+        // on_arrival (sched_policies.cpp:279-290)
+        ++f_tail;
+        if (n_run == 0 && !boundary) {  // wake: boundary at this instant, after the arrivals
+          boundary = true;
+          ev_t = next_arr;
+          t_push = next_arr;
+        }
+        next_arr = next_arr2;
+        next_arr2 = f_tail + 1 < n_mine ? arr[w + (f_tail + 1) * W] : dinf();
+#ifdef SCLS_ILS_PROF
+        ++pc_arr;
+#endif
+      } else if (slow) {
+      // a boundary (sched_policies.cpp:292-391): retire, compact, admit FCFS,
+      // and the next step's context / first exit, in one pass over the slots
+      const double now = ev_t;
+      const int nr = n_run;
+      const int it1 = it_cnt + (nr > 0 ? 1 : 0);
+      if (nr > 0) {
+        it_cnt = it1;
+        ++seg_it;
+      }
+      int nexit = 0, keep = 0, mc = 0, nx = 0x7fffffff;
+      // four slots per trip, loads first (the compiler cannot prove the
+      // ping-pong buffers disjoint, so it would not hoist them itself)
+      for (int i = 0; i < nr; i += 4) {
+        int4 v[4];
+        double a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          v[u] = i + u < nr ? run[i + u] : make_int4(0, 0x7fffffff, 0, 0);
+          a[u] = i + u < nr ? ra[i + u] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (i + u >= nr) break;
+          if (it1 - v[u].x >= v[u].y) {
+            rec.t[comp + nexit] = now;
+            rec.tp[comp + nexit] = t_push;
+            rec.r[comp + nexit] = now - a[u];
+            ++nexit;
+          } else {
+            run2[keep] = v[u];
+            ra2[keep] = a[u];
+            ++keep;
+            mc = max(mc, v[u].z + (it1 - v[u].x));
+            nx = min(nx, v[u].x + v[u].y);
+          }
+        }
+      }
+      {  // the compacted buffer becomes the running set
+        int4* tr = run;
+        run = run2;
+        run2 = tr;
+        double* ta = ra;
+        ra = ra2;
+        ra2 = ta;
+      }
+      const int njoin = min(MC - keep, f_tail - f_head);
+      for (int j = 0; j < njoin; ++j) {
+        const int lim = min(j_g, G);
+        run[keep + j] = make_int4(it1, lim, j_i, 0);
+        ra[keep + j] = j_a;
+        mc = max(mc, j_i);
+        nx = min(nx, it1 + lim);
+        ++f_head;
+        if (f_head < n_mine) {
+          const int id = w + f_head * W;
+          j_a = arr[id];
+          j_i = inp[id];
+          j_g = tg[id];
+        }
+      }
+      const int nr_new = keep + njoin;
+      n_run = nr_new;
+      const bool changed = nexit > 0 || njoin > 0;
+      if (changed && seg && seg_it > 0) {  // batch_end record
+        ++batch_count;
+        batch_members += seg_n;
+        ++n_ev;
+        seg = false;
+        last_end = fmax(last_end, now);
+      }
+      if (nexit > 0) {
+        comp += nexit;
+        n_ev += nexit;
+        last_comp = now;
+      }
+      if (nr_new == 0) {
+        boundary = false;
+        ev_t = dinf();
+      } else {
+        if (changed) {  // batch_start record
+          ++n_ev;
+          seg = true;
+          seg_n = nr_new;
+          seg_it = 0;
+        }
+        double it = decode_step_time(lat, mc, nr_new);
+        for (int j = keep; j < nr_new; ++j) it = __dadd_rn(it, prefill_time(lat, 1, run[j].z));
+        n_disp += njoin;
+        n_ev += njoin;
+        const double dn = (double)nr_new;
+        a1 = __dmul_rn(lat.d1, dn);
+        a2 = __dmul_rn(lat.d2, dn);
+        dl = (double)(mc + 1);
+        room = nx - it_cnt - 1;
+        t_push = now;
+        ev_t = __dadd_rn(now, it);
+      }
+#ifdef SCLS_ILS_PROF
+        ++pc_slow;
+#endif
+      }
+      live = live && (comp < n_mine);
+    }
+    stuck = comp < n_mine;
+  }
+  if (__any_sync(FULL, stuck)) {
+    finish_report(lane, R, SCLS_ERR_NON_TERMINATION, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0,
+                  0.0);
+    return;
+  }
+  const int completed = __reduce_add_sync(FULL, comp);
+  const long long n_events = n + __reduce_add_sync(FULL, (unsigned)n_ev);
+  const int n_disp_all = __reduce_add_sync(FULL, n_disp);
+  const int batch_all = __reduce_add_sync(FULL, batch_count);
+  for (int o = 16; o; o >>= 1) batch_members += __shfl_xor_sync(FULL, batch_members, o);
+  double last_completion = last_comp;
+  for (int o = 16; o; o >>= 1) last_completion = fmax(last_completion, __shfl_xor_sync(FULL, last_completion, o));
+
+#ifdef SCLS_ILS_PROF
+  const long long t_b = clock64();
+#endif
+  // ---- phase 2: the completions in the reference's global order ----------------------
+  // W-way merge by (time, push time).  Each instance streams its records
+  // through a shared-memory window (kMergeWin / W entries, refilled by the
+  // whole warp).  A step selects by a 32-bit fixed-point image of the time
+  // (monotone, so its minimum holds the minimum time; one REDUX); only
+  // lanes sharing that image compare the exact 64-bit keys.
+  bool tie = false;
+  {
+    const int ws = kMergeWin / W;
+    uint64_t* wt = swin_t[warp];
+    double* wr = swin_r[warp];
+    uint32_t* wq = swin_q[warp];
+    const double* ct = (const double*)(base + Lay.ct);
+    const double* cp = (const double*)(base + Lay.cp);
+    const double* cr = (const double*)(base + Lay.cr);
+    const int mine = lane < W ? comp : 0;
+    double t_lo = mine > 0 ? ct[lane * cap_w] : dinf();
+    for (int o = 16; o; o >>= 1) t_lo = fmin(t_lo, __shfl_xor_sync(FULL, t_lo, o));
+    const double span = __dsub_rn(last_completion, t_lo);
+    const double scale = completed > 0 && span > 0.0 ? __ddiv_rn(4294967040.0, span) : 0.0;
+    int k = 0, h = 0;  // records consumed; head position in the window
+    unsigned need = __ballot_sync(FULL, mine > 0);
+    uint64_t kt = ~0ull;
+    uint32_t kq = 0xffffffffu;
+    for (int i = 0;; ++i) {
+      while (need) {  // refill the windows of the instances in `need`
+        const int q = __ffs(need) - 1;
+        need &= need - 1u;
+        const int kk = shfl_i(k, q), mq = shfl_i(mine, q);
+        for (int e = lane; e < ws; e += 32) {
+          const int64_t idx = kk + e;
+          if (idx < mq) {
+            const double tv = ct[q * cap_w + idx];
+            wt[q * ws + e] = ordered_bits(tv);
+            wq[q * ws + e] = (uint32_t)__dmul_rn(__dsub_rn(tv, t_lo), scale);
+            wr[q * ws + e] = cr[q * cap_w + idx];
+          }
+        }
+        __syncwarp();
+        if (lane == q) {
+          h = 0;
+          kt = wt[q * ws];
+          kq = wq[q * ws];
+        }
+      }
+      if (i == completed) break;
+      const unsigned mq = __reduce_min_sync(FULL, kq);
+      unsigned win = __ballot_sync(FULL, kq == mq);
+      if (win & (win - 1u)) {  // same fixed-point image: exact time, then push order
+        bool in = (win >> lane) & 1u;
+        const unsigned hi = (unsigned)(kt >> 32), lo = (unsigned)kt;
+        const unsigned mh = __reduce_min_sync(FULL, in ? hi : 0xffffffffu);
+        in = in && hi == mh;
+        const unsigned ml = __reduce_min_sync(FULL, in ? lo : 0xffffffffu);
+        in = in && lo == ml;
+        win = __ballot_sync(FULL, in);
+        if (win & (win - 1u)) {
+          const uint64_t kp = in ? ordered_bits(cp[lane * cap_w + k]) : ~0ull;
+          const unsigned ph = (unsigned)(kp >> 32), pl = (unsigned)kp;
+          const unsigned mph = __reduce_min_sync(FULL, ph);
+          const unsigned mpl = __reduce_min_sync(FULL, ph == mph ? pl : 0xffffffffu);
+          win = __ballot_sync(FULL, in && ph == mph && pl == mpl);
+          if (win & (win - 1u)) {
+            tie = true;
+            break;
+          }
+        }
+      }
+      bool refill = false;
+      if ((win >> lane) & 1u) {
+        resp[i] = wr[lane * ws + h];
+        ++k;
+        ++h;
+        if (k == mine) {
+          kt = ~0ull;
+          kq = 0xffffffffu;
+        } else if (h == ws) {
+          refill = true;
+        } else {
+          kt = wt[lane * ws + h];
+          kq = wq[lane * ws + h];
+        }
+      }
+      need = __ballot_sync(FULL, refill);
+    }
+  }
+  if (tie) {  // the exact lock-step kernel re-runs this job
+    if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
+    return;
+  }
+#ifdef SCLS_ILS_PROF
+  const long long t_c = clock64();
+#endif
+  __syncwarp();
+  if (hist && P.hist_bins > 1 && lane == 0) hist[1] = completed;
+  finish_report(lane, R, SCLS_OK, n, W, completed, n > 0 ? arr[0] : dinf(), last_completion, resp, bins, last_end, 0,
+                0, batch_all, batch_members, 0, n_events, n_disp_all, 0, last_completion);
+#ifdef SCLS_ILS_PROF
+  const long long t_d = clock64();
+  if (hist && P.hist_bins >= 8 && lane == 0) {
+    hist[4] = t_b - t_a;
+    hist[5] = t_c - t_b;
+    hist[6] = t_d - t_c;
+    hist[7] = completed;
+  }
+  if (hist && P.hist_bins >= 16 && lane == 0) {
+    hist[8] = pc_fast;
+    hist[9] = pc_slow;
+    hist[10] = pc_arr;
+    hist[11] = pc_outer;
+    hist[12] = cy_fast;
+    hist[13] = cy_arr;
+    hist[14] = cy_slow;
+    hist[15] = (long long)(s_trips[warp][0] << 32 | s_trips[warp][1]);
+  }
+#endif
+}
+
+}  // namespace
+}  // namespace scls

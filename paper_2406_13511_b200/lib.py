@@ -22,6 +22,8 @@ import numpy as np
 from . import capi
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libscls_b200.so")
+# Diagnostics only (profiling builds): another build of the same library.
+LIB_PATH = os.environ.get("SCLS_B200_LIB", LIB_PATH)
 
 # Every symbol include/scls_capi.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = [
@@ -167,6 +169,10 @@ class Context:
     def set_concurrent(self, on):
         """SCLS_OPT_SIM_CONCURRENT: run the per-policy simulator launches concurrently (default off)."""
         self._check(self.lib.scls_set_option(self.h, 3, 1 if on else 0))
+
+    def set_ils_lockstep(self, on):
+        """SCLS_OPT_ILS_KERNEL: 1 = the lock-step metrics-only ILS kernel, 0 = independent instance lanes."""
+        self._check(self.lib.scls_set_option(self.h, 4, 1 if on else 0))
 
     def set_dp_kernel(self, mode):
         """SCLS_OPT_DP_KERNEL: 0 auto (monotone decision kernel when allowed), 1 chain."""
