@@ -143,9 +143,9 @@ enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT
  * sequence on the context stream (results are identical; on the C5 sweep the
  * sequential order is faster: 124 vs 131 ms, the event-chain-bound ILS kernel
  * loses more to shared SMs than the others gain).  SCLS_OPT_ILS_KERNEL
- * (default 0): metrics-only ILS runs every instance in its own lane and
- * merges the completions (csrc/sim_ils_indep.cuh); 1 forces the lock-step
- * kernel that processes the global event order directly (results identical). */
+ * (default 0): metrics-only ILS and SLS run every instance / worker in its own
+ * lane and merge the completions (csrc/sim_indep.cuh); 1 forces the lock-step
+ * kernels that process the global event order directly (results identical). */
 scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value);
 /* Diagnostics: enable/disable clock64 phase counters in the DP chain kernel
  * and read-and-reset them (cycles: main chain, main barrier wait, helper

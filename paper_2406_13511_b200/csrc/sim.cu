@@ -1262,7 +1262,8 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
 
 template <int POL, bool kHash, bool kLog>
 __global__ void __launch_bounds__(kSimWarps * 32, POL == SCLS_POLICY_SCLS ? SCLS_SIM_MINB : 8) sim_kernel(SimParams p, const int32_t* __restrict__ list,
-                                                              int32_t count) {
+                                                              int32_t count, const int32_t* __restrict__ dcount = nullptr) {
+  if (dcount) count = *dcount;  // fallback launches: the job count lives on the device
   __shared__ int32_t bins[kSimWarps][256];
   __shared__ int32_t ssplit[POL == SCLS_POLICY_SCLS ? kSimWarps : 1][POL == SCLS_POLICY_SCLS ? kSplitSmem + 1 : 1];
   __shared__ double sT[POL == SCLS_POLICY_SCLS ? kSimWarps : 1][POL == SCLS_POLICY_SCLS ? kSplitSmem + 1 : 1];
@@ -1277,7 +1278,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, POL == SCLS_POLICY_SCLS ? SCLS
 }  // namespace scls
 
 #include "sim_ils.cuh"
-#include "sim_ils_indep.cuh"
+#include "sim_indep.cuh"
 
 namespace scls {
 namespace {
@@ -1616,6 +1617,13 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   else if (hash) sim_kernel<POLV, true, false><<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);        \
   else sim_kernel<POLV, false, false><<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);
     if (pol == SCLS_POLICY_SCLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SCLS) }
+    else if (pol == SCLS_POLICY_SLS && !want_log && !hash && !ctx->ils_lockstep) {
+      // independent worker lanes; exact cross-worker ties re-run in lock step
+      SCLS_CUDA(cudaMemsetAsync(d_fb, 0, sizeof(int32_t), ls));
+      sim_sls_indep_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, d_fb, d_fb + 1);
+      SCLS_LAUNCHED();
+      sim_kernel<SCLS_POLICY_SLS, false, false><<<grid, kSimWarps * 32, 0, ls>>>(p, d_fb + 1, cnt, d_fb);
+    }
     else if (pol == SCLS_POLICY_SLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SLS) }
     else if (!want_log && !hash && ctx->ils_lockstep) sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, nullptr);
     else if (!want_log && !hash) {

@@ -13,7 +13,7 @@ struct SimLayout {
   int64_t b_start, b_n, b_lin, b_served, b_next, b_est;   // SCLS batches
   int64_t tl_g, tl_t, tl_e, tl_s, tl_a;                   // SCLS slot state
   int64_t fifo, pf_t, pf_seq, pf_w, run, ex;              // SLS / ILS
-  int64_t ct, cp, cr, ra;                                 // ILS completion records, slot arrivals
+  int64_t ct, cp, cr, ra, cn;                             // ILS / SLS completion records, slot arrivals
   int64_t total;
 };
 
@@ -64,6 +64,10 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
     L.pf_t = take(8 * n1);
     L.pf_seq = take(8 * n1);
     L.pf_w = take(4 * n1);
+    L.ct = take(8 * (W * cap_w + 1));
+    L.cp = take(8 * (W * cap_w + 1));
+    L.cr = take(8 * (W * cap_w + 1));
+    L.cn = take(4 * (W * cap_w + 1));
   } else {
     L.fifo = take(4 * (W * cap_w + 1));
     L.run = take(16 * ((int64_t)W * mc + 1));

@@ -1,5 +1,5 @@
-// sim_ils_indep.cuh — metrics-only ILS simulator with independent instance
-// lanes (included by sim.cu after sim_ils.cuh).
+// sim_indep.cuh — metrics-only ILS and SLS simulators with independent instance
+// (worker) lanes (included by sim.cu after sim_ils.cuh).  ILS first; SLS at the end.
 //
 // ILS instances never interact.  Arrivals are assigned round-robin in id
 // order (sched_policies.cpp:279-281), so instance w sees exactly the requests
@@ -38,6 +38,111 @@ struct IlsRec {
 };
 
 constexpr int kMergeWin = 256;  // merge window entries per warp (time key + response), reused as p95 bins
+// Replays the W per-instance completion lists (sorted; list w of lane w,
+// comp records) in the reference's global order -- time, then push time of
+// the completing event -- into resp[0, completed).  Each instance streams its
+// records through a shared-memory window (kMergeWin / W entries, refilled by
+// the whole warp).  A step selects by a 32-bit fixed-point image of the time
+// (monotone, so its minimum holds the minimum time; one REDUX); only lanes
+// sharing that image compare the exact 64-bit keys.  With run lengths (cn:
+// the batch size at a batch's first record), the winner emits the whole run
+// -- members of one batch share (time, push time) and complete in member
+// order within the one event.
+// Returns true on an exact (time, push time) tie between instances, which
+// needs the push order one level further back: the caller hands the job to
+// the lock-step kernel.
+__device__ bool merge_completions(int lane, int W, int comp, int completed, double last_completion, int64_t cap_w,
+                                  const double* __restrict__ ct, const double* __restrict__ cp,
+                                  const double* __restrict__ cr, const int32_t* __restrict__ cn,
+                                  double* __restrict__ resp, uint64_t* wt, double* wr, uint32_t* wq, uint8_t* wn) {
+  const bool runs = cn != nullptr;
+  const int ws = kMergeWin / W;
+  const int mine = lane < W ? comp : 0;
+  double t_lo = mine > 0 ? ct[lane * cap_w] : dinf();
+  for (int o = 16; o; o >>= 1) t_lo = fmin(t_lo, __shfl_xor_sync(FULL, t_lo, o));
+  const double span = __dsub_rn(last_completion, t_lo);
+  const double scale = completed > 0 && span > 0.0 ? __ddiv_rn(4294967040.0, span) : 0.0;
+  int k = 0, h = 0;  // records consumed; head position in the window
+  int carry_run = 0;  // rest of a run that a window refill cut
+  unsigned need = __ballot_sync(FULL, mine > 0);
+  uint64_t kt = ~0ull;
+  uint32_t kq = 0xffffffffu;
+  for (int i = 0;;) {
+    while (need) {  // refill the windows of the instances in `need`
+      const int q = __ffs(need) - 1;
+      need &= need - 1u;
+      const int kk = shfl_i(k, q), mq = shfl_i(mine, q);
+      for (int e = lane; e < ws; e += 32) {
+        const int64_t idx = kk + e;
+        if (idx < mq) {
+          const double tv = ct[q * cap_w + idx];
+          wt[q * ws + e] = ordered_bits(tv);
+          wq[q * ws + e] = (uint32_t)__dmul_rn(__dsub_rn(tv, t_lo), scale);
+          wr[q * ws + e] = cr[q * cap_w + idx];
+          if (runs) wn[q * ws + e] = (uint8_t)min(cn[q * cap_w + idx], 255);
+        }
+      }
+      __syncwarp();
+      if (lane == q) {
+        h = 0;
+        kt = wt[q * ws];
+        kq = wq[q * ws];
+        if (carry_run > 0) wn[q * ws] = (uint8_t)carry_run;
+        carry_run = 0;
+      }
+    }
+    if (i >= completed) break;
+    const unsigned mq = __reduce_min_sync(FULL, kq);
+    unsigned win = __ballot_sync(FULL, kq == mq);
+    if (win & (win - 1u)) {  // same fixed-point image: exact time, then push order
+      bool in = (win >> lane) & 1u;
+      const unsigned hi = (unsigned)(kt >> 32), lo = (unsigned)kt;
+      const unsigned mh = __reduce_min_sync(FULL, in ? hi : 0xffffffffu);
+      in = in && hi == mh;
+      const unsigned ml = __reduce_min_sync(FULL, in ? lo : 0xffffffffu);
+      in = in && lo == ml;
+      win = __ballot_sync(FULL, in);
+      if (win & (win - 1u)) {
+        const uint64_t kp = in ? ordered_bits(cp[lane * cap_w + k]) : ~0ull;
+        const unsigned ph = (unsigned)(kp >> 32), pl = (unsigned)kp;
+        const unsigned mph = __reduce_min_sync(FULL, ph);
+        const unsigned mpl = __reduce_min_sync(FULL, ph == mph ? pl : 0xffffffffu);
+        win = __ballot_sync(FULL, in && ph == mph && pl == mpl);
+        if (win & (win - 1u)) return true;
+      }
+    }
+    const int wl = __ffs(win) - 1;
+    bool refill = false;
+    int emitted = 0;
+    if (lane == wl) {
+      // a run: the rest of this batch (at most 255 per step), same event
+      int left = runs ? max((int)wn[lane * ws + h], 1) : 1;
+      do {
+        resp[i + emitted] = wr[lane * ws + h];
+        ++emitted;
+        ++k;
+        ++h;
+        --left;
+        if (k == mine) {
+          kt = ~0ull;
+          kq = 0xffffffffu;
+          break;
+        }
+        if (h == ws) {
+          refill = true;
+          break;
+        }
+        kt = wt[lane * ws + h];
+        kq = wq[lane * ws + h];
+      } while (left > 0);
+      if (refill && left > 0) carry_run = left;
+    }
+    i += shfl_i(emitted, wl);
+    need = __ballot_sync(FULL, refill);
+  }
+  return false;
+}
+
 #ifndef SCLS_ILS_INDEP_MINB
 #define SCLS_ILS_INDEP_MINB 4
 #endif
@@ -297,91 +402,9 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
   const long long t_b = clock64();
 #endif
   // ---- phase 2: the completions in the reference's global order ----------------------
-  // W-way merge by (time, push time).  Each instance streams its records
-  // through a shared-memory window (kMergeWin / W entries, refilled by the
-  // whole warp).  A step selects by a 32-bit fixed-point image of the time
-  // (monotone, so its minimum holds the minimum time; one REDUX); only
-  // lanes sharing that image compare the exact 64-bit keys.
-  bool tie = false;
-  {
-    const int ws = kMergeWin / W;
-    uint64_t* wt = swin_t[warp];
-    double* wr = swin_r[warp];
-    uint32_t* wq = swin_q[warp];
-    const double* ct = (const double*)(base + Lay.ct);
-    const double* cp = (const double*)(base + Lay.cp);
-    const double* cr = (const double*)(base + Lay.cr);
-    const int mine = lane < W ? comp : 0;
-    double t_lo = mine > 0 ? ct[lane * cap_w] : dinf();
-    for (int o = 16; o; o >>= 1) t_lo = fmin(t_lo, __shfl_xor_sync(FULL, t_lo, o));
-    const double span = __dsub_rn(last_completion, t_lo);
-    const double scale = completed > 0 && span > 0.0 ? __ddiv_rn(4294967040.0, span) : 0.0;
-    int k = 0, h = 0;  // records consumed; head position in the window
-    unsigned need = __ballot_sync(FULL, mine > 0);
-    uint64_t kt = ~0ull;
-    uint32_t kq = 0xffffffffu;
-    for (int i = 0;; ++i) {
-      while (need) {  // refill the windows of the instances in `need`
-        const int q = __ffs(need) - 1;
-        need &= need - 1u;
-        const int kk = shfl_i(k, q), mq = shfl_i(mine, q);
-        for (int e = lane; e < ws; e += 32) {
-          const int64_t idx = kk + e;
-          if (idx < mq) {
-            const double tv = ct[q * cap_w + idx];
-            wt[q * ws + e] = ordered_bits(tv);
-            wq[q * ws + e] = (uint32_t)__dmul_rn(__dsub_rn(tv, t_lo), scale);
-            wr[q * ws + e] = cr[q * cap_w + idx];
-          }
-        }
-        __syncwarp();
-        if (lane == q) {
-          h = 0;
-          kt = wt[q * ws];
-          kq = wq[q * ws];
-        }
-      }
-      if (i == completed) break;
-      const unsigned mq = __reduce_min_sync(FULL, kq);
-      unsigned win = __ballot_sync(FULL, kq == mq);
-      if (win & (win - 1u)) {  // same fixed-point image: exact time, then push order
-        bool in = (win >> lane) & 1u;
-        const unsigned hi = (unsigned)(kt >> 32), lo = (unsigned)kt;
-        const unsigned mh = __reduce_min_sync(FULL, in ? hi : 0xffffffffu);
-        in = in && hi == mh;
-        const unsigned ml = __reduce_min_sync(FULL, in ? lo : 0xffffffffu);
-        in = in && lo == ml;
-        win = __ballot_sync(FULL, in);
-        if (win & (win - 1u)) {
-          const uint64_t kp = in ? ordered_bits(cp[lane * cap_w + k]) : ~0ull;
-          const unsigned ph = (unsigned)(kp >> 32), pl = (unsigned)kp;
-          const unsigned mph = __reduce_min_sync(FULL, ph);
-          const unsigned mpl = __reduce_min_sync(FULL, ph == mph ? pl : 0xffffffffu);
-          win = __ballot_sync(FULL, in && ph == mph && pl == mpl);
-          if (win & (win - 1u)) {
-            tie = true;
-            break;
-          }
-        }
-      }
-      bool refill = false;
-      if ((win >> lane) & 1u) {
-        resp[i] = wr[lane * ws + h];
-        ++k;
-        ++h;
-        if (k == mine) {
-          kt = ~0ull;
-          kq = 0xffffffffu;
-        } else if (h == ws) {
-          refill = true;
-        } else {
-          kt = wt[lane * ws + h];
-          kq = wq[lane * ws + h];
-        }
-      }
-      need = __ballot_sync(FULL, refill);
-    }
-  }
+  const bool tie = merge_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),
+                                     (const double*)(base + Lay.cp), (const double*)(base + Lay.cr), nullptr,
+                                     resp, swin_t[warp], swin_r[warp], swin_q[warp], nullptr);
   if (tie) {  // the exact lock-step kernel re-runs this job
     if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
     return;
@@ -412,6 +435,171 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
     hist[15] = (long long)(s_trips[warp][0] << 32 | s_trips[warp][1]);
   }
 #endif
+}
+
+
+// ---- SLS with independent worker lanes ------------------------------------------------
+// SLS workers never interact either: arrivals go round-robin in id order
+// (sched_policies.cpp:194-201), a worker dispatches only from its own FIFO
+// when idle (:207-243), and its batch ends complete only its members
+// (:245-273).  Within a worker, same-instant events run arrivals first (seq <
+// n), then in the worker's own push order; a policy event that finds the
+// worker busy or its FIFO empty changes nothing, so the worker's timeline is:
+// dispatch when idle after the arrivals of an instant, and at every batch end.
+// Completions are recorded as (t, push time = the batch's start, response)
+// with the batch size at its first member, and merged like ILS.
+__global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
+    sim_sls_indep_kernel(SimParams P, const int32_t* __restrict__ list, int32_t count, int32_t* __restrict__ fb_count,
+                         int32_t* __restrict__ fb_list) {
+  __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
+  __shared__ double swin_r[kSimWarps][kMergeWin];
+  __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
+  __shared__ uint8_t swin_n[kSimWarps][kMergeWin];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * kSimWarps + warp;
+  if (g >= count) return;
+  const int t = list[g];
+  int32_t* bins = (int32_t*)swin_t[warp];  // p95 bins (after the merge)
+  const int ts = P.src ? P.src[t] : t;
+  const int64_t r0 = P.req_off[ts];
+  const int n = (int)(P.req_off[ts + 1] - r0);
+  const double* __restrict__ arr = P.arr + r0;
+  const int32_t* __restrict__ inp = P.inp + r0;
+  const int32_t* __restrict__ tg = P.tg + r0;
+  const int ci = P.cfg_index ? P.cfg_index[t] : 0;
+  const int W = P.cfgs[ci].W, B = P.cfgs[ci].B, G = P.cfgs[ci].G;
+  const double horizon = P.cfgs[ci].horizon;
+  const Lat& lat = P.lat;
+  scls_trace_result* R = &P.res[t];
+  int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
+
+  int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
+  if (status == SCLS_OK) {
+    int bad = 0;
+    for (int i = 1 + lane; i < n; i += 32) bad |= arr[i] < arr[i - 1];
+    if (__any_sync(FULL, bad)) status = SCLS_ERR_ERROR;
+  }
+  if (hist)
+    for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
+  if (status != SCLS_OK) {
+    finish_report(lane, R, status, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0);
+    return;
+  }
+  char* base = P.arena + P.trace_base[t];
+  const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_SLS, P.trace_cap[t], 1);
+  double* resp = (double*)(base + Lay.resp);
+  const int64_t cap_w = (n + W - 1) / W;
+
+  int comp = 0, batch_count = 0, n_disp = 0, stuck = 0;
+  long long batch_members = 0, n_ev = 0, total_pad = 0, total_inv = 0;
+  double last_end = 0.0, last_comp = -dinf();
+  {
+    const int w = lane;
+    double* rt = (double*)(base + Lay.ct) + w * cap_w;
+    double* rp = (double*)(base + Lay.cp) + w * cap_w;
+    double* rr = (double*)(base + Lay.cr) + w * cap_w;
+    int32_t* rn = (int32_t*)(base + Lay.cn) + w * cap_w;
+    const int n_mine = lane < W && w < n ? (n - 1 - w) / W + 1 : 0;  // requests w, w + W, ...
+    int f_head = 0, f_tail = 0;  // dispatched / arrived (FIFO as counters)
+    bool busy = false;
+    int b_head = 0, b_n = 0, b_lin = 0, b_lout = 0;  // in-flight batch: FIFO positions [b_head, b_head + b_n)
+    double done_t = dinf(), b_start = 0.0;
+    double next_arr = n_mine > 0 ? arr[w] : dinf();
+    double next_arr2 = n_mine > 1 ? arr[w + W] : dinf();
+    bool live = n_mine > 0;
+    // try_dispatch at `now` (sched_policies.cpp:207-243): FCFS batch of <= B
+    // from the FIFO, started at once (enqueue_batch + start_next_batch)
+    auto dispatch = [&](double now) {
+      const int take = min(B, f_tail - f_head);
+      int lin = 0, lout = 0;
+      long long so = 0, sg = 0;
+      for (int j = 0; j < take; ++j) {
+        const int id = w + (f_head + j) * W;
+        const int o = inp[id], gm = min(tg[id], G);
+        lin = max(lin, o);
+        lout = max(lout, gm);
+        so += o;
+        sg += gm;
+      }
+      // batch_end accounting (sched_policies.cpp:255-266): pad = l_in - orig,
+      // invalid = served - min(gen, G), summed over members
+      total_pad += (long long)take * lin - so;
+      total_inv += (long long)take * lout - sg;
+      b_head = f_head;
+      b_n = take;
+      b_lin = lin;
+      b_lout = lout;
+      f_head += take;
+      busy = true;
+      b_start = now;
+      done_t = __dadd_rn(now, batch_serve_time(lat, take, lin, lout));
+      n_disp += 1;
+      n_ev += 2;  // dispatch + batch_start
+    };
+    for (;;) {
+      const bool arrive = live && next_arr <= done_t && next_arr <= horizon;  // arrivals first at an instant
+      const bool done = live && !arrive && busy && done_t < next_arr && done_t < horizon;
+      if (!__any_sync(FULL, arrive || done)) break;
+      if (arrive) {
+        // on_arrival (sched_policies.cpp:194-201) + its policy event, which runs
+        // after every arrival of this instant
+        const double now = next_arr;
+        ++f_tail;
+        next_arr = next_arr2;
+        next_arr2 = f_tail + 1 < n_mine ? arr[w + (f_tail + 1) * W] : dinf();
+        if (!busy && next_arr != now) dispatch(now);
+      } else if (done) {
+        // BatchDone (sim_engine.cpp:151-158, sched_policies.cpp:245-273)
+        const double now = done_t;
+        ++batch_count;
+        batch_members += b_n;
+        last_end = fmax(last_end, now);
+        for (int j = 0; j < b_n; ++j) {
+          const int id = w + (b_head + j) * W;
+          rt[comp + j] = now;
+          rp[comp + j] = b_start;
+          rr[comp + j] = now - arr[id];
+          rn[comp + j] = j == 0 ? b_n : 0;
+        }
+        comp += b_n;
+        n_ev += 1 + b_n;  // batch_end + completions
+        last_comp = now;
+        busy = false;
+        done_t = dinf();
+        if (f_tail > f_head) dispatch(now);
+      }
+      live = live && comp < n_mine;
+    }
+    stuck = comp < n_mine;
+  }
+  if (__any_sync(FULL, stuck)) {
+    finish_report(lane, R, SCLS_ERR_NON_TERMINATION, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0,
+                  0.0);
+    return;
+  }
+  const int completed = __reduce_add_sync(FULL, comp);
+  const long long n_events = n + __reduce_add_sync(FULL, (unsigned)n_ev);
+  const int n_disp_all = __reduce_add_sync(FULL, n_disp);
+  const int batch_all = __reduce_add_sync(FULL, batch_count);
+  for (int o = 16; o; o >>= 1) {
+    batch_members += __shfl_xor_sync(FULL, batch_members, o);
+    total_pad += __shfl_xor_sync(FULL, total_pad, o);
+    total_inv += __shfl_xor_sync(FULL, total_inv, o);
+  }
+  double last_completion = last_comp;
+  for (int o = 16; o; o >>= 1) last_completion = fmax(last_completion, __shfl_xor_sync(FULL, last_completion, o));
+  const bool tie = merge_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),
+                                     (const double*)(base + Lay.cp), (const double*)(base + Lay.cr),
+                                     (const int32_t*)(base + Lay.cn), resp, swin_t[warp], swin_r[warp],
+                                     swin_q[warp], swin_n[warp]);
+  if (tie) {  // the exact lock-step kernel re-runs this job
+    if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
+    return;
+  }
+  __syncwarp();
+  if (hist && P.hist_bins > 1 && lane == 0) hist[1] = completed;
+  finish_report(lane, R, SCLS_OK, n, W, completed, n > 0 ? arr[0] : dinf(), last_completion, resp, bins, last_end,
+                total_pad, total_inv, batch_all, batch_members, 0, n_events, n_disp_all, 0, last_completion);
 }
 
 }  // namespace

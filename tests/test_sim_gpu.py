@@ -300,28 +300,35 @@ def test_simulate_grid_matches_per_trace_runs(ctx, orc, digests, concurrent):
 
 @pytest.mark.parametrize("lockstep", [False, True])
 def test_ils_kernels_agree_and_tie_fallback(ctx, orc, lockstep):
-    """Metrics-only ILS: the independent-lane kernel (default) and the lock-step
-    kernel both match the oracle, including traces whose instances evolve
-    identically (exact cross-instance time ties: the independent kernel hands
-    those jobs to the lock-step kernel) and NonTermination horizons."""
+    """Metrics-only ILS and SLS: the independent-lane kernels (default) and the
+    lock-step kernels both match the oracle, including traces whose instances
+    evolve identically (exact cross-instance time ties: the independent
+    kernels hand those jobs to the lock-step kernels), simultaneous arrivals
+    and NonTermination horizons."""
     lat = capi.builtin_latency_model()
     rng = np.random.default_rng(11)
     traces, cfgs = [], []
-    for trial in range(40):
-        traces.append(orc.generate(capi.workload_spec(rate=float(rng.uniform(2, 40)),
-                                                      duration_s=float(rng.uniform(10, 120)), seed=8100 + trial)))
-        cfgs.append(capi.sched_cfg(policy="ils", worker_count=int(rng.integers(1, 33)),
+    for trial in range(80):
+        pol = ("ils", "sls")[trial % 2]
+        tr = orc.generate(capi.workload_spec(rate=float(rng.uniform(2, 40)),
+                                             duration_s=float(rng.uniform(10, 120)), seed=8100 + trial))
+        if trial % 7 == 3:  # bursts of simultaneous arrivals
+            tr = (np.floor(np.asarray(tr[0]) * 2.0) / 2.0, tr[1], tr[2])
+        traces.append(tr)
+        cfgs.append(capi.sched_cfg(policy=pol, worker_count=int(rng.integers(1, 33)),
                                    max_gen_limit=int(rng.choice([64, 512, 1024])),
                                    max_concurrent=int(rng.integers(1, 20)),
+                                   fixed_batch_size=int(rng.integers(1, 40)),
                                    horizon_s=1e7 if trial % 5 else float(rng.uniform(5, 60))))
     # identical instances: every instance gets the same requests at the same times
-    for w in (2, 4, 8):
-        k = 6
-        arr = np.repeat(np.arange(1, k + 1, dtype=np.float64), w)
-        inp = np.repeat(np.arange(100, 100 + 10 * k, 10, dtype=np.int32), w)
-        gen = np.repeat(np.arange(5, 5 + 3 * k, 3, dtype=np.int32), w)
-        traces.append((arr, inp, gen))
-        cfgs.append(capi.sched_cfg(policy="ils", worker_count=w, max_concurrent=3))
+    for pol in ("ils", "sls"):
+        for w in (2, 4, 8):
+            k = 6
+            arr = np.repeat(np.arange(1, k + 1, dtype=np.float64), w)
+            inp = np.repeat(np.arange(100, 100 + 10 * k, 10, dtype=np.int32), w)
+            gen = np.repeat(np.arange(5, 5 + 3 * k, 3, dtype=np.int32), w)
+            traces.append((arr, inp, gen))
+            cfgs.append(capi.sched_cfg(policy=pol, worker_count=w, max_concurrent=3, fixed_batch_size=2))
     idx = list(range(len(cfgs)))
     ctx.set_digests(False)
     ctx.set_ils_lockstep(lockstep)
