@@ -47,6 +47,7 @@ struct SimCfg {
   int32_t policy, S, G, B, MC, W;
   double lambda, gamma, horizon;
   int32_t table;  // cost-table index (SCLS), -1 otherwise
+  int32_t mono;   // monotone cost model (dp_mono.cuh): the tick DP may use decision rounds
 };
 
 struct SimParams {
@@ -587,6 +588,56 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
               kb = k;
             }
           }
+        }
+        if (C.mono) {
+          // decision rounds (dp_mono.cuh): with T[0..a] final, a pending row
+          // whose best candidate from sources <= a is strictly below
+          // LB = T[a] + c(L_r, 1) is final -- no later source reaches LB.
+          // The leading run of decided rows becomes final and is pushed into
+          // the rows still pending; row a+1 is always decided.
+          bool pend = valid;
+          int a = tb;
+          double ta = T[tb];
+          const double c1r = valid ? __ldg(crow + 1) : 0.0;
+          for (;;) {
+            const double lb = __dadd_rn(ta, c1r);
+            const bool und = pend && r != a + 1 && !(acc < lb);
+            const unsigned um = __ballot_sync(FULL, und);
+            const int first = um ? __ffs(um) - 1 : 32;  // lanes below it are final
+            if (pend && lane < first) {
+              T[r] = acc;
+              split[r] = r - kb;
+              pend = false;
+            }
+            if (!um) break;
+            const int a2 = tb + first;  // new frontier: rows a+1 .. a2 are final
+            // push sources j in (a, a2], ascending j (descending k, ties to the smaller k)
+            for (int j = a + 1; j <= a2; j += 4) {
+              double tv[4], cv[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int jj = min(j + u, a2);
+                tv[u] = shfl_d(acc, jj - tb - 1);
+                const int k = r - (j + u);
+                cv[u] = pend && j + u <= a2 && k >= 1 && k <= Wr ? __ldg(crow + k) : 0.0;
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int k = r - (j + u);
+                if (pend && j + u <= a2 && k >= 1 && k <= Wr) {
+                  const double cand = __dadd_rn(tv[u], cv[u]);
+                  if (cand <= acc) {
+                    acc = cand;
+                    kb = k;
+                  }
+                }
+              }
+            }
+            ta = shfl_d(acc, a2 - tb - 1);
+            a = a2;
+          }
+          __syncwarp();
+          continue;
         }
         // the in-tile chain: row tb+s finalises at step s-1 (lane s-1) after
         // T[tb+s-1] arrives; step s offers k = lane + 2 - s to this lane
@@ -1393,6 +1444,11 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   auto src_of = [&](int j) { return has_src ? h_src[j] : j; };
   // Configs: validate (Simulator::Simulator, sim_engine.cpp:32-35), limits.
   const bool model_ok = scls_validate_latency(lat) == SCLS_OK && scls_validate_memory(memm) == SCLS_OK;
+  // dp_mono.cuh: non-negative coefficients + a valid memory model make every
+  // tick's T non-decreasing, so the tick DP can decide rows in rounds
+  const bool mono = model_ok && !std::signbit(lat->p1) && !std::signbit(lat->p2) && !std::signbit(lat->p3) &&
+                    !std::signbit(lat->p4) && !std::signbit(lat->d1) && !std::signbit(lat->d2) &&
+                    !std::signbit(lat->d3) && !std::signbit(lat->d4);
   std::vector<SimCfg> hc(n_cfgs);
   std::vector<uint8_t> hok(n_cfgs);
   int n_tables = 0;
@@ -1403,7 +1459,7 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
       return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "device simulator supports worker_count <= 32");
     hok[c] = model_ok && validate_cfg_host(x) == SCLS_OK;
     hc[c] = SimCfg{x.policy, x.slice_len, x.max_gen_limit, x.fixed_batch_size, x.max_concurrent,
-                   x.worker_count, x.lambda, x.gamma, x.horizon_s, -1};
+                   x.worker_count, x.lambda, x.gamma, x.horizon_s, -1, mono && ctx->dp_mode != 1};
     if (hok[c] && x.policy == SCLS_POLICY_SCLS) hc[c].table = n_tables++;
     if (hok[c]) Gmax = std::max(Gmax, x.max_gen_limit);
     if (hok[c] && x.policy == SCLS_POLICY_ILS) hc[c].MC = std::max(1, std::min<int32_t>(x.max_concurrent, (int32_t)nmax));
