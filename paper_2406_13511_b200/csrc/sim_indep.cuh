@@ -37,7 +37,14 @@ struct IlsRec {
   double* r;   // response (t - arrival)
 };
 
-constexpr int kMergeWin = 256;  // merge window entries per warp (time key + response), reused as p95 bins
+#ifndef SCLS_MERGE_WIN
+#define SCLS_MERGE_WIN 256
+#endif
+#ifndef SCLS_INDEP_RUN
+#define SCLS_INDEP_RUN 128
+#endif
+constexpr int kMergeWin = SCLS_MERGE_WIN;  // merge window entries per warp (time key + response), reused as p95 bins
+constexpr int kIndepRun = SCLS_INDEP_RUN;  // ILS running slots per warp (W * MC), shared memory
 // Replays the W per-instance completion lists (sorted; list w of lane w,
 // comp records) in the reference's global order -- time, then push time of
 // the completing event -- into resp[0, completed).  Each instance streams its
@@ -153,8 +160,8 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
   __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
   __shared__ double swin_r[kSimWarps][kMergeWin];
   __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
-  __shared__ int4 srun[kSimWarps][2][kIlsRunSmem];   // running slots, ping-pong
-  __shared__ double sra[kSimWarps][2][kIlsRunSmem];  // their arrival times
+  __shared__ int4 srun[kSimWarps][2][kIndepRun];   // running slots, ping-pong
+  __shared__ double sra[kSimWarps][2][kIndepRun];  // their arrival times
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * kSimWarps + warp;
   if (g >= count) return;
@@ -185,7 +192,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
     finish_report(lane, R, status, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0);
     return;
   }
-  if (W * MC > kIlsRunSmem) {  // running slots do not fit this warp's shared memory
+  if (W * MC > kIndepRun) {  // running slots do not fit this warp's shared memory
     if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
     return;
   }
@@ -448,7 +455,10 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
 // dispatch when idle after the arrivals of an instant, and at every batch end.
 // Completions are recorded as (t, push time = the batch's start, response)
 // with the batch size at its first member, and merged like ILS.
-__global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
+#ifndef SCLS_SLS_INDEP_MINB
+#define SCLS_SLS_INDEP_MINB 7  // one wave of 4096 traces (7.3 ms vs 8.8 ms at 4)
+#endif
+__global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
     sim_sls_indep_kernel(SimParams P, const int32_t* __restrict__ list, int32_t count, int32_t* __restrict__ fb_count,
                          int32_t* __restrict__ fb_list) {
   __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
