@@ -1,0 +1,100 @@
+"""The reference CLI on the B200 path.
+
+tools/slicesim_main.cpp is compiled unchanged (CLI11 stand-in:
+paper_2406_13511_b200/dropin/cli/CLI11.hpp) into build/refsuite/slicesim_ref
+(reference core) and build/refsuite/slicesim_b200 (reference core with the
+B200 drop-in: batch_requests / offload / Simulator::run / sweep on the GPU).
+The reference's own cli_test.cpp runs against both, and every output file
+of `slicesim run` (report JSON, event-log JSONL), `slicesim sweep` (CSV) and
+`slicesim gen-workload` (trace CSV) must be byte-identical between them."""
+import os
+import subprocess
+
+import pytest
+
+from tests.conftest import ROOT
+
+BIN = os.path.join(ROOT, "build", "refsuite")
+
+
+def _require(name):
+    path = os.path.join(BIN, name)
+    if not os.path.exists(path):
+        if os.path.isdir("/root/reference/proj/tools"):
+            subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "refsuite"), "-j8"], check=True,
+                           capture_output=True)
+        else:
+            pytest.fail(f"{path} missing and /root/reference unavailable to build it")
+    return path
+
+
+def test_reference_cli_tests_on_reference():
+    """Harness check: the reference CLI built with the CLI11 stand-in passes
+    the reference's own CLI tests."""
+    _require("slicesim_ref")
+    p = subprocess.run([_require("cli_test_ref")], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+    assert "0 failed" in p.stdout
+
+
+@pytest.mark.gpu
+def test_reference_cli_tests_on_b200():
+    _require("slicesim_b200")
+    p = subprocess.run([_require("cli_test_b200")], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+    assert "0 failed" in p.stdout
+
+
+CASES = [
+    ("run_scls_default", "run --report {d}/r.json --event-log {d}/e.jsonl", ["r.json", "e.jsonl"]),
+    ("run_sls", "run --policy sls --set workload.duration=200 --report {d}/r.json --event-log {d}/e.jsonl",
+     ["r.json", "e.jsonl"]),
+    ("run_ils", "run --policy ils --set workload.duration=200 --report {d}/r.json --event-log {d}/e.jsonl",
+     ["r.json", "e.jsonl"]),
+    ("run_scls_one_worker", "run --seed 42 --set policy.workers=1 --set workload.rate=2 --set workload.duration=500 "
+     "--report {d}/r.json --event-log {d}/e.jsonl", ["r.json", "e.jsonl"]),
+    ("run_scls_s64_analytic", "run --set policy.slice_len=64 --set models.memory=builtin-analytic "
+     "--set workload.rate=25 --set workload.duration=120 --report {d}/r.json --event-log {d}/e.jsonl",
+     ["r.json", "e.jsonl"]),
+    ("sweep_rate", "sweep --param rate --values 5,10,20 --set workload.duration=120 --out {d}/s.csv", ["s.csv"]),
+    ("sweep_slice", "sweep --param slice_len --values 32,128,256 --set workload.duration=120 --out {d}/s.csv",
+     ["s.csv"]),
+    ("sweep_workers_ils", "sweep --param workers --values 1,4,8 --set policy.kind=ils --set workload.duration=120 "
+     "--out {d}/s.csv", ["s.csv"]),
+    ("gen_workload", "gen-workload --set workload.duration=60 --out {d}/t.csv", ["t.csv"]),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,args,files", CASES, ids=[c[0] for c in CASES])
+def test_cli_outputs_byte_identical(tmp_path, name, args, files):
+    ref, b200 = _require("slicesim_ref"), _require("slicesim_b200")
+    outs = {}
+    for tag, exe in (("ref", ref), ("b200", b200)):
+        d = tmp_path / tag
+        d.mkdir()
+        p = subprocess.run([exe] + args.format(d=d).split(), capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, (tag, p.stderr[-2000:])
+        outs[tag] = {f: (d / f).read_bytes() for f in files}
+        outs[tag]["stdout"] = p.stdout.replace(str(d), "<d>").encode()
+    for f in files + ["stdout"]:
+        assert outs["ref"][f] == outs["b200"][f], (name, f)
+        if f != "stdout":
+            assert len(outs["ref"][f]) > 0
+
+
+@pytest.mark.gpu
+def test_cli_trace_roundtrip_byte_identical(tmp_path):
+    """gen-workload -> run --set workload.kind=trace on both builds."""
+    ref, b200 = _require("slicesim_ref"), _require("slicesim_b200")
+    trace = tmp_path / "trace.csv"
+    subprocess.run([ref, "gen-workload", "--set", "workload.duration=90", "--out", str(trace)], check=True,
+                   capture_output=True)
+    got = {}
+    for tag, exe in (("ref", ref), ("b200", b200)):
+        rep, log = tmp_path / f"{tag}.json", tmp_path / f"{tag}.jsonl"
+        subprocess.run([exe, "run", "--set", "workload.kind=trace", "--set", f"workload.trace={trace}",
+                        "--set", "policy.workers=3", "--report", str(rep), "--event-log", str(log)], check=True,
+                       capture_output=True)
+        got[tag] = (rep.read_bytes(), log.read_bytes())
+    assert got["ref"] == got["b200"]
