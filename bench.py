@@ -190,8 +190,8 @@ def run_reference(args, rank, world):
             "n_gpus": world, "steps": len(times), "warmup": args.warmup, "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generators: Poisson arrivals, codefuse-like lengths)",
-            "config": {"workload": f"C5 sweep sample: {per} traces x 3 policies (600 s, 8 instances, "
-                                   "S=128, rates 10/15/20/25)", "host_threads": cores},
+            "config": {"workload": f"C5 sweep sample: {per} traces x 3 policies ({args.duration:.0f} s, "
+                                   "8 instances, S=128, rates 10/15/20/25)", "host_threads": cores},
             "cpu_baseline": {"value": value, "unit": "traces/s", "cores": cores, "kind": kind,
                              "sample": f"{per} traces per step: generate once + 3 policies"},
             "e2e": {"value": value, "unit": "traces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -26,7 +26,7 @@ struct scls_ctx {
   bool sim_digests = true;                // scls_simulate computes the log digests
   int dp_mode = 0;                        // 0 auto, 1 force the chain kernel (tests)
   bool dp_last_mono = false;              // the last DP ran the monotone decision kernel
-  bool sim_concurrent = false;            // scls_simulate runs its per-policy launches concurrently
+  bool sim_concurrent = true;             // scls_simulate runs its per-policy launches concurrently
   bool ils_lockstep = false;              // metrics-only ILS: the lock-step kernel instead of independent lanes
   cudaStream_t side[3] = {};              // forked streams for those launches (created on first use)
 

@@ -1632,6 +1632,12 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
     const int pol = hc[cfg_index ? h_idx[t] : 0].policy;
     lists[(pol >= 0 && pol <= 2) ? pol : 0].push_back(t);
   }
+  // Longest traces first: a launch that needs more than one wave of warps
+  // then starts its slowest jobs first and fills the tail with short ones.
+  for (auto& l : lists)
+    std::stable_sort(l.begin(), l.end(), [&](int32_t a, int32_t b) {
+      return h_off[src_of(a) + 1] - h_off[src_of(a)] > h_off[src_of(b) + 1] - h_off[src_of(b)];
+    });
   int32_t* d_lists = (int32_t*)ctx->buf(kSlotSim + 22, sizeof(int32_t) * (n_traces + 3));
   if (!d_lists) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
   {
@@ -1641,8 +1647,11 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
     SCLS_CUDA(cudaMemcpyAsync(d_lists, flat.data(), sizeof(int32_t) * n_traces, cudaMemcpyHostToDevice, s));
   }
   const bool hash = ctx->sim_digests;
-  int32_t* d_fb = (int32_t*)ctx->buf(kSlotSim + 24, sizeof(int32_t) * (n_traces + 1));  // ILS fallback list
-  if (!d_fb) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+  // lock-step fallback lists of the independent-lane kernels, one per policy
+  // (the per-policy launches may run concurrently)
+  int32_t* d_fb_ils = (int32_t*)ctx->buf(kSlotSim + 24, sizeof(int32_t) * (n_traces + 1));
+  int32_t* d_fb_sls = (int32_t*)ctx->buf(kSlotSim + 25, sizeof(int32_t) * (n_traces + 1));
+  if (!d_fb_ils || !d_fb_sls) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
   // Per-policy launches; with more than one policy they run concurrently on
   // forked streams so one kernel's tail overlaps the others' work.
   int n_pol = 0;
@@ -1675,20 +1684,20 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
     if (pol == SCLS_POLICY_SCLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SCLS) }
     else if (pol == SCLS_POLICY_SLS && !want_log && !hash && !ctx->ils_lockstep) {
       // independent worker lanes; exact cross-worker ties re-run in lock step
-      SCLS_CUDA(cudaMemsetAsync(d_fb, 0, sizeof(int32_t), ls));
-      sim_sls_indep_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, d_fb, d_fb + 1);
+      SCLS_CUDA(cudaMemsetAsync(d_fb_sls, 0, sizeof(int32_t), ls));
+      sim_sls_indep_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, d_fb_sls, d_fb_sls + 1);
       SCLS_LAUNCHED();
-      sim_kernel<SCLS_POLICY_SLS, false, false><<<grid, kSimWarps * 32, 0, ls>>>(p, d_fb + 1, cnt, d_fb);
+      sim_kernel<SCLS_POLICY_SLS, false, false><<<grid, kSimWarps * 32, 0, ls>>>(p, d_fb_sls + 1, cnt, d_fb_sls);
     }
     else if (pol == SCLS_POLICY_SLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SLS) }
     else if (!want_log && !hash && ctx->ils_lockstep) sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, nullptr);
     else if (!want_log && !hash) {
       // independent instance lanes; jobs with an exact cross-instance time tie
       // are re-run by the lock-step kernel from a device-side list
-      SCLS_CUDA(cudaMemsetAsync(d_fb, 0, sizeof(int32_t), ls));
-      sim_ils_indep_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, d_fb, d_fb + 1);
+      SCLS_CUDA(cudaMemsetAsync(d_fb_ils, 0, sizeof(int32_t), ls));
+      sim_ils_indep_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, d_fb_ils, d_fb_ils + 1);
       SCLS_LAUNCHED();
-      sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, d_fb + 1, cnt, d_fb);
+      sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, d_fb_ils + 1, cnt, d_fb_ils);
     }
     else { SCLS_SIM_LAUNCH(SCLS_POLICY_ILS) }
 #undef SCLS_SIM_LAUNCH

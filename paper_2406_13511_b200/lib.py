@@ -167,7 +167,7 @@ class Context:
         self._check(self.lib.scls_set_option(self.h, 1, 1 if on else 0))
 
     def set_concurrent(self, on):
-        """SCLS_OPT_SIM_CONCURRENT: run the per-policy simulator launches concurrently (default off)."""
+        """SCLS_OPT_SIM_CONCURRENT: run the per-policy simulator launches concurrently (default on)."""
         self._check(self.lib.scls_set_option(self.h, 3, 1 if on else 0))
 
     def set_ils_lockstep(self, on):

@@ -285,7 +285,7 @@ def test_simulate_grid_matches_per_trace_runs(ctx, orc, digests, concurrent):
         got, gh = ctx.simulate_grid(traces, cfgs, lat, MEMORIES["rule"](), hist_bins=16)
     finally:
         ctx.set_digests(True)
-        ctx.set_concurrent(False)
+        ctx.set_concurrent(True)
     rep = [t for _ in cfgs for t in traces]
     idx = [c for c in range(len(cfgs)) for _ in traces]
     want, wh = orc.simulate(rep, cfgs, lat, MEMORIES["rule"](), cfg_index=idx, hist_bins=16)
