@@ -251,6 +251,56 @@ def bench_c3(ctx, torch, lib, capi, stream, steps, warmup):
             "gpu_launches_per_call": launches // max(steps, 1)}
 
 
+def bench_configs(ctx, lib, capi, steps):
+    """BASELINE configs[0], [1], [3] as latency lines next to the headline:
+    C1 (1 instance, rate 2, 500 s, SCLS), C2 (8 instances, rate 20, 500 s, SCLS)
+    and C4 (one 5000 s / ~100k-request trace x {SCLS, SLS, ILS} x slice
+    {32, 64, 128, 256} x max_gen {256, 512, 1024}), each generated and
+    simulated on the device through scls_run_experiments; the CPU reference
+    (oracle/_ref) runs the same jobs on the host cores; every TraceResult
+    field is compared with it."""
+    from oracle.pyoracle import RefLib, REF_SO, OracleLib, ORACLE_SO
+    try:
+        ref, kind = RefLib(REF_SO), "reference"
+    except OSError:
+        ref, kind = OracleLib(ORACLE_SO), "port"
+    lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
+    cases = {
+        "C1": [(capi.workload_spec(rate=2.0, duration_s=500.0, seed=42), capi.sched_cfg(policy="scls", worker_count=1))],
+        "C2": [(capi.workload_spec(rate=20.0, duration_s=500.0, seed=42), capi.sched_cfg(policy="scls"))],
+    }
+    c4 = []
+    for pol in POLICIES:
+        for S in (32, 64, 128, 256):
+            for G in (256, 512, 1024):
+                if S <= G:
+                    c4.append((capi.workload_spec(rate=20.0, duration_s=5000.0, seed=42, max_gen_limit=G),
+                               capi.sched_cfg(policy=pol, slice_len=S, max_gen_limit=G)))
+    cases["C4"] = c4
+    cores = os.cpu_count() or 1
+    out = {}
+    for name, jobs in cases.items():
+        specs = [j[0] for j in jobs]
+        cfgs = [j[1] for j in jobs]
+        ms = []
+        for _ in range(max(3, steps)):
+            res, _h = ctx.run_experiments(specs, cfgs, lat, mem, hist_bins=16)
+            ms.append(ctx.timings()["total"])
+        traces = [ref.generate(sp) for sp in specs]
+        t0 = time.perf_counter()
+        want, _wh = ref.simulate(traces, cfgs, lat, mem, cfg_index=list(range(len(jobs))), hist_bins=16,
+                                 threads=cores)
+        cpu_s = time.perf_counter() - t0
+        bad = sum(1 for i in range(len(jobs)) for f, _ in capi.TraceResult._fields_
+                  if f not in ("sim_clock", "h_complete_ids", "h_dispatch", "h_complete_t", "h_log")
+                  and getattr(res[i], f) != getattr(want[i], f))
+        out[name] = {"jobs": len(jobs), "requests_per_trace": int(len(traces[0][0])),
+                     "device_ms": round(statistics.median(ms), 3),
+                     "cpu_reference_ms": round(cpu_s * 1e3, 1), "cpu_cores": min(cores, len(jobs)),
+                     "cpu_kind": kind, "mismatches": bad}
+    return out
+
+
 def run_ours(args, rank, world, dist):
     import torch
 
@@ -464,6 +514,7 @@ def run_ours(args, rank, world, dist):
     }
     if not args.no_c3:
         line["scheduler_c3"] = bench_c3(ctx, torch, lib, capi, stream, max(2, args.steps // 2), 2)
+        line["configs_c1_c2_c4"] = bench_configs(ctx, lib, capi, args.steps)
     if world == 1:
         line["cpu_baseline"] = cpu_baseline(args)
     print(json.dumps(line), flush=True)

@@ -1319,8 +1319,9 @@ __global__ void __launch_bounds__(kSimWarps * 32, POL == SCLS_POLICY_SCLS ? SCLS
   __shared__ int32_t ssplit[POL == SCLS_POLICY_SCLS ? kSimWarps : 1][POL == SCLS_POLICY_SCLS ? kSplitSmem + 1 : 1];
   __shared__ double sT[POL == SCLS_POLICY_SCLS ? kSimWarps : 1][POL == SCLS_POLICY_SCLS ? kSplitSmem + 1 : 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x * kSimWarps + warp;
+  const int g = blockIdx.x * (blockDim.x >> 5) + warp;  // launches use 1 or kSimWarps warps per CTA
   if (g >= count) return;
+  if (list[g] < 0) return;  // an empty slot (small launches: one job per CTA)
   run_trace<POL, kHash, kLog>(p, list[g], lane, bins[warp], ssplit[POL == SCLS_POLICY_SCLS ? warp : 0],
                               sT[POL == SCLS_POLICY_SCLS ? warp : 0]);
 }
@@ -1632,19 +1633,36 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
     const int pol = hc[cfg_index ? h_idx[t] : 0].policy;
     lists[(pol >= 0 && pol <= 2) ? pol : 0].push_back(t);
   }
-  // Longest traces first: a launch that needs more than one wave of warps
-  // then starts its slowest jobs first and fills the tail with short ones.
-  for (auto& l : lists)
-    std::stable_sort(l.begin(), l.end(), [&](int32_t a, int32_t b) {
-      return h_off[src_of(a) + 1] - h_off[src_of(a)] > h_off[src_of(b) + 1] - h_off[src_of(b)];
-    });
-  int32_t* d_lists = (int32_t*)ctx->buf(kSlotSim + 22, sizeof(int32_t) * (n_traces + 3));
+  // Longest jobs first (work ~ requests; SCLS: served slices): a launch that
+  // needs more than one wave of warps starts its slowest jobs first and fills
+  // the tail with short ones.  A launch with at most one job per SM (a single
+  // trace, a small grid) gives every job a CTA of its own (the other warps of
+  // the CTA get no job, -1), so no two jobs share an SM's L1.
+  size_t n_slots = 0;
+  for (auto& l : lists) {
+    auto work = [&](int32_t t) {
+      const SimCfg& c = hc[cfg_index ? h_idx[t] : 0];
+      return c.policy == SCLS_POLICY_SCLS ? caps[t] : h_off[src_of(t) + 1] - h_off[src_of(t)];
+    };
+    std::stable_sort(l.begin(), l.end(), [&](int32_t a, int32_t b) { return work(a) > work(b); });
+    if (l.size() > 1 && l.size() <= (size_t)ctx->sm_count) {
+      std::vector<int32_t> spread;
+      spread.reserve(l.size() * kSimWarps);
+      for (int32_t t : l) {
+        spread.push_back(t);
+        for (int w = 1; w < kSimWarps; ++w) spread.push_back(-1);
+      }
+      l.swap(spread);
+    }
+    n_slots += l.size();
+  }
+  int32_t* d_lists = (int32_t*)ctx->buf(kSlotSim + 22, sizeof(int32_t) * (n_slots + 3));
   if (!d_lists) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
   {
     std::vector<int32_t> flat;
-    flat.reserve(n_traces);
+    flat.reserve(n_slots);
     for (auto& l : lists) flat.insert(flat.end(), l.begin(), l.end());
-    SCLS_CUDA(cudaMemcpyAsync(d_lists, flat.data(), sizeof(int32_t) * n_traces, cudaMemcpyHostToDevice, s));
+    SCLS_CUDA(cudaMemcpyAsync(d_lists, flat.data(), sizeof(int32_t) * n_slots, cudaMemcpyHostToDevice, s));
   }
   const bool hash = ctx->sim_digests;
   // lock-step fallback lists of the independent-lane kernels, one per policy
@@ -1674,30 +1692,31 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
       ls = ctx->side[k];
       SCLS_CUDA(cudaStreamWaitEvent(ls, ctx->ev[8], 0));
     }
-    const int grid = div_up(cnt, kSimWarps);
+    const int wpb = kSimWarps;
+    const int grid = div_up(cnt, wpb);
     const int32_t* l = d_lists + off;
     at += cnt;
 #define SCLS_SIM_LAUNCH(POLV)                                                                      \
-  if (want_log) sim_kernel<POLV, true, true><<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);          \
-  else if (hash) sim_kernel<POLV, true, false><<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);        \
-  else sim_kernel<POLV, false, false><<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt);
+  if (want_log) sim_kernel<POLV, true, true><<<grid, wpb * 32, 0, ls>>>(p, l, cnt);          \
+  else if (hash) sim_kernel<POLV, true, false><<<grid, wpb * 32, 0, ls>>>(p, l, cnt);        \
+  else sim_kernel<POLV, false, false><<<grid, wpb * 32, 0, ls>>>(p, l, cnt);
     if (pol == SCLS_POLICY_SCLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SCLS) }
     else if (pol == SCLS_POLICY_SLS && !want_log && !hash && !ctx->ils_lockstep) {
       // independent worker lanes; exact cross-worker ties re-run in lock step
       SCLS_CUDA(cudaMemsetAsync(d_fb_sls, 0, sizeof(int32_t), ls));
-      sim_sls_indep_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, d_fb_sls, d_fb_sls + 1);
+      sim_sls_indep_kernel<<<grid, wpb * 32, 0, ls>>>(p, l, cnt, d_fb_sls, d_fb_sls + 1);
       SCLS_LAUNCHED();
-      sim_kernel<SCLS_POLICY_SLS, false, false><<<grid, kSimWarps * 32, 0, ls>>>(p, d_fb_sls + 1, cnt, d_fb_sls);
+      sim_kernel<SCLS_POLICY_SLS, false, false><<<grid, wpb * 32, 0, ls>>>(p, d_fb_sls + 1, cnt, d_fb_sls);
     }
     else if (pol == SCLS_POLICY_SLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SLS) }
-    else if (!want_log && !hash && ctx->ils_lockstep) sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, nullptr);
+    else if (!want_log && !hash && ctx->ils_lockstep) sim_ils_lean_kernel<<<grid, wpb * 32, 0, ls>>>(p, l, cnt, nullptr);
     else if (!want_log && !hash) {
       // independent instance lanes; jobs with an exact cross-instance time tie
       // are re-run by the lock-step kernel from a device-side list
       SCLS_CUDA(cudaMemsetAsync(d_fb_ils, 0, sizeof(int32_t), ls));
-      sim_ils_indep_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, l, cnt, d_fb_ils, d_fb_ils + 1);
+      sim_ils_indep_kernel<<<grid, wpb * 32, 0, ls>>>(p, l, cnt, d_fb_ils, d_fb_ils + 1);
       SCLS_LAUNCHED();
-      sim_ils_lean_kernel<<<grid, kSimWarps * 32, 0, ls>>>(p, d_fb_ils + 1, cnt, d_fb_ils);
+      sim_ils_lean_kernel<<<grid, wpb * 32, 0, ls>>>(p, d_fb_ils + 1, cnt, d_fb_ils);
     }
     else { SCLS_SIM_LAUNCH(SCLS_POLICY_ILS) }
 #undef SCLS_SIM_LAUNCH

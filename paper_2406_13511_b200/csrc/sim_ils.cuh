@@ -244,9 +244,10 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_MINB)
   __shared__ int4 srun[kSimWarps][kIlsRunSmem];
   __shared__ uint8_t sown[kSimWarps][kOwnBuckets];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x * kSimWarps + warp;
+  const int g = blockIdx.x * (blockDim.x >> 5) + warp;  // launches use 1 or kSimWarps warps per CTA
   if (g >= count) return;
   const int t = list[g];
+  if (t < 0) return;  // an empty slot (small launches: one job per CTA)
   int32_t* bins = sbins[warp];
   const int ts = P.src ? P.src[t] : t;  // source trace of job t
   const int64_t r0 = P.req_off[ts];

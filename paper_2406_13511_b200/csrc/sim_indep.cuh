@@ -163,9 +163,10 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
   __shared__ int4 srun[kSimWarps][2][kIndepRun];   // running slots, ping-pong
   __shared__ double sra[kSimWarps][2][kIndepRun];  // their arrival times
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x * kSimWarps + warp;
+  const int g = blockIdx.x * (blockDim.x >> 5) + warp;  // launches use 1 or kSimWarps warps per CTA
   if (g >= count) return;
   const int t = list[g];
+  if (t < 0) return;  // an empty slot (small launches: one job per CTA)
   int32_t* bins = (int32_t*)swin_t[warp];  // p95 bins (after the merge)
   const int ts = P.src ? P.src[t] : t;
   const int64_t r0 = P.req_off[ts];
@@ -466,9 +467,10 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
   __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
   __shared__ uint8_t swin_n[kSimWarps][kMergeWin];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x * kSimWarps + warp;
+  const int g = blockIdx.x * (blockDim.x >> 5) + warp;  // launches use 1 or kSimWarps warps per CTA
   if (g >= count) return;
   const int t = list[g];
+  if (t < 0) return;  // an empty slot (small launches: one job per CTA)
   int32_t* bins = (int32_t*)swin_t[warp];  // p95 bins (after the merge)
   const int ts = P.src ? P.src[t] : t;
   const int64_t r0 = P.req_off[ts];
