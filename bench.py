@@ -278,6 +278,7 @@ def bench_configs(ctx, lib, capi, steps):
                                capi.sched_cfg(policy=pol, slice_len=S, max_gen_limit=G)))
     cases["C4"] = c4
     cores = os.cpu_count() or 1
+    ctx.set_digests(False)  # the reference's run/sweep report metrics only
     out = {}
     for name, jobs in cases.items():
         specs = [j[0] for j in jobs]
