@@ -447,6 +447,12 @@ def run_ours(args, rank, world, dist):
         ctx.simulate_grid_flat(p_offs, p_arr, p_inp, p_gen, cfgs, lat, mem, hist_bins=hist_bins)
         sim_e2e.append(time.perf_counter() - t0)
 
+    # device generation parity on the whole shard: run_sweep == simulate_grid on
+    # the host-generated traces, every result word of every job
+    sweep_step()
+    r_sweep = d_res_all.clone()
+    sim_grid()
+    gen_mismatch = int((r_sweep.view(3 * ntr, nfields) != d_res_all.view(3 * ntr, nfields)).any(dim=1).sum().item())
     # parity of this rank's first traces vs the C oracle (outside the timed region)
     ctx.set_digests(True)
     from oracle.pyoracle import oracle_lib
@@ -460,12 +466,6 @@ def run_ours(args, rank, world, dist):
             for f, _ in capi.TraceResult._fields_:
                 if f != "sim_clock" and getattr(a[i], f) != getattr(b[i], f):
                     bad += 1
-    # device generation parity on the whole shard: run_sweep == simulate_grid on
-    # the host-generated traces, every result word of every job
-    sweep_step()
-    r_sweep = d_res_all.clone()
-    sim_grid()
-    gen_mismatch = int((r_sweep.view(3 * ntr, nfields) != d_res_all.view(3 * ntr, nfields)).any(dim=1).sum().item())
     statuses = set()
     for kk in range(3):
         r = d_res[kk].view(ntr, nfields).cpu().numpy()
