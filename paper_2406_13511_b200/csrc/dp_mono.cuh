@@ -42,6 +42,10 @@
 namespace scls {
 
 constexpr int kMonoSegs = kDpHelpers;  // 12 k-segments per row
+#ifndef SCLS_DP_FAR_TOP
+#define SCLS_DP_FAR_TOP 48
+#endif
+constexpr int kFarTop = SCLS_DP_FAR_TOP;  // far k's near the window, split finer
 
 struct DpMonoSmem {
   double ring[kDpRing];          // 32 KB of recent T
@@ -125,9 +129,23 @@ __global__ void __launch_bounds__(kDpThreads, 1)
     double best = kInf;
     int bk = 0;
     if (span > 0) {
-      const int len = (span + kMonoSegs - 1) / kMonoSegs;
-      const int k0 = kmin + h * len;
-      const int k1 = min(W, k0 + len - 1);
+      // Two tiers: the top kFarTop k's (the batch sizes near the window, where
+      // the minimum of these monotone costs lives and pruning rarely holds)
+      // in kMonoSegs/2 short segments, the rest in the other half (mostly
+      // pruned by the bound below) -- the helpers' work evens out.
+      constexpr int kHalf = kMonoSegs / 2;
+      const int top = min(span, kFarTop);
+      const int rest = span - top;
+      int k0, k1;
+      if (h < kHalf) {
+        const int len = (rest + kHalf - 1) / kHalf;
+        k0 = kmin + h * len;
+        k1 = min(kmin + rest - 1, k0 + len - 1);
+      } else {
+        const int len = (top + kHalf - 1) / kHalf;
+        k0 = kmin + rest + (h - kHalf) * len;
+        k1 = min(W, k0 + len - 1);
+      }
       // Exact segment pruning (monotone T and c): every candidate of the
       // segment is >= fl(T[r-k1] + c(L_r, k0)).  If that bound exceeds an
       // actual candidate of the row (k = W, the full window), no candidate
