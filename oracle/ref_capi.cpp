@@ -43,6 +43,7 @@ thread_local std::string g_err;
 thread_local int64_t g_err_request = -1;
 
 scls_status map_exception() {
+  g_err_request = -1;  // only an InfeasibleRequestError names a request
   try {
     throw;
   } catch (const S::InfeasibleRequestError& e) {

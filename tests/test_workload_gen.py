@@ -209,3 +209,35 @@ def test_run_experiments_equals_simulate(ctx):
         for f, _ in capi.TraceResult._fields_:
             assert getattr(a[t], f) == getattr(b[t], f), (t, f)
     assert np.array_equal(ha, hb)
+
+
+@pytest.mark.gpu
+def test_run_sweep_statuses_match_reference(ctx, orc):
+    """Device-generated sweeps carry the reference's failure statuses:
+    NonTermination (short horizon), InfeasibleRequest (a KV cap no request
+    fits), EmptyLog (no arrivals), per job, next to healthy jobs."""
+    from oracle import pyoracle
+    ref = pyoracle.ref_lib() or orc
+    lat = capi.builtin_latency_model()
+    specs = [capi.workload_spec(rate=15.0, duration_s=120.0, seed=5),
+             capi.workload_spec(rate=5.0, duration_s=0.0, seed=6),
+             capi.workload_spec(rate=30.0, duration_s=200.0, seed=7)]
+    for mem, cfgs in ((MEMORIES["rule"](), [capi.sched_cfg(policy=p, horizon_s=h) for p in ("scls", "sls", "ils")
+                                            for h in (1e7, 30.0)]),
+                      (capi.analytic(1000.0, 3.0, 2.0, 1.0, 1.0), [capi.sched_cfg(policy="scls")])):
+        ctx.set_digests(False)
+        try:
+            a, _ = ctx.run_sweep(specs, cfgs, lat, mem, hist_bins=16)
+        finally:
+            ctx.set_digests(True)
+        traces = [ref.generate(s) for s in specs]
+        n = len(specs)
+        statuses = set()
+        for c, cfg in enumerate(cfgs):
+            b, _ = ref.simulate(traces, cfg, lat, mem, hist_bins=16)
+            for t in range(n):
+                statuses.add(b[t].status)
+                for f, _ in capi.TraceResult._fields_:
+                    if not f.startswith("h_") and f != "sim_clock":
+                        assert getattr(a[c * n + t], f) == getattr(b[t], f), (c, t, f)
+        assert len(statuses) >= 2, statuses
