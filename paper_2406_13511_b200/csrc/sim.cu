@@ -498,11 +498,27 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       // 1. order the pool by (eff, id); ids are arrival ranks (sim_engine.cpp:110-114)
       const int idb = bits_of((uint32_t)max(n - 1, 1));
       uint32_t emax = 0;
-      for (int i = lane; i < P_; i += 32) {
-        const int id = pool[i];
-        const uint32_t e = (uint32_t)(inp[id] + gen[id]);
-        emax = max(emax, e);
-        sk[i] = ((uint64_t)e << idb) | (uint64_t)id;
+      // four rows per lane per trip, every load issued before any use: the
+      // pool and request arrays are L2 / DRAM resident, so memory-level
+      // parallelism, not issue, bounds this loop
+      for (int i0 = lane; i0 < P_; i0 += 128) {
+        int id[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) id[u] = i0 + 32 * u < P_ ? pool[i0 + 32 * u] : 0;
+        int ip[4], gn[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          ip[u] = i0 + 32 * u < P_ ? inp[id[u]] : 0;
+          gn[u] = i0 + 32 * u < P_ ? gen[id[u]] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (i0 + 32 * u < P_) {
+            const uint32_t e = (uint32_t)(ip[u] + gn[u]);
+            emax = max(emax, e);
+            sk[i0 + 32 * u] = ((uint64_t)e << idb) | (uint64_t)id[u];
+          }
+        }
       }
       emax = __reduce_max_sync(FULL, emax);
       __syncwarp();
@@ -513,19 +529,38 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       const uint64_t idmask = (1ull << idb) - 1ull;
       // 2. rows: L, singleton feasibility (batcher.cpp:40-46)
       int bad = 0x7fffffff;
-      for (int i = lane; i < P_; i += 32) {
-        const uint64_t key = keys[i];
-        const int id = (int)(key & idmask);
-        const int L = (int)(key >> idb);
-        const int64_t q = tl_pos + i;
-        tlog[q] = id;
-        tl_g[q] = gen[id];
-        tl_t[q] = tg[id];
-        tl_e[q] = L;
-        tl_s[q] = sl[id];
-        tl_a[q] = arr[id];
-        sv[i] = L;
-        if (L > P.Lmax || Kt[L] == 0) bad = min(bad, i);
+      for (int i0 = lane; i0 < P_; i0 += 64) {  // two rows per lane per trip, loads first
+        uint64_t key[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) key[u] = i0 + 32 * u < P_ ? keys[i0 + 32 * u] : 0ull;
+        int id[2], L[2], g_[2], t_[2], s_[2], k_[2];
+        double a_[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const bool ok = i0 + 32 * u < P_;
+          id[u] = (int)(key[u] & idmask);
+          L[u] = (int)(key[u] >> idb);
+          g_[u] = ok ? gen[id[u]] : 0;
+          t_[u] = ok ? tg[id[u]] : 0;
+          s_[u] = ok ? sl[id[u]] : 0;
+          a_[u] = ok ? arr[id[u]] : 0.0;
+          k_[u] = ok && L[u] <= P.Lmax ? Kt[L[u]] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = i0 + 32 * u;
+          if (i < P_) {
+            const int64_t q = tl_pos + i;
+            tlog[q] = id[u];
+            tl_g[q] = g_[u];
+            tl_t[q] = t_[u];
+            tl_e[q] = L[u];
+            tl_s[q] = s_[u];
+            tl_a[q] = a_[u];
+            sv[i] = L[u];
+            if (L[u] > P.Lmax || k_[u] == 0) bad = min(bad, i);
+          }
+        }
       }
       bad = __reduce_min_sync(FULL, bad);
       __syncwarp();
