@@ -222,9 +222,13 @@ __device__ bool warp_radix_sort(int n, uint64_t* k, int32_t* v, uint64_t* k2, in
     const uint32_t mask = bits - shift >= 8 ? 0xffu : ((1u << (bits - shift)) - 1u);
     for (int i = lane; i < 256; i += 32) bins[i] = 0;
     __syncwarp();
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + lane;
-      if (i < n) atomicAdd(&bins[(k[i] >> shift) & mask], 1);
+    for (int base = 0; base < n; base += 128) {  // four keys per lane per trip, loads first
+      uint64_t kk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) kk[u] = base + 32 * u + lane < n ? k[base + 32 * u + lane] : 0ull;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (base + 32 * u + lane < n) atomicAdd(&bins[(kk[u] >> shift) & mask], 1);
     }
     __syncwarp();
     {  // exclusive scan of 256 bins: 8 per lane
@@ -249,10 +253,14 @@ __device__ bool warp_radix_sort(int n, uint64_t* k, int32_t* v, uint64_t* k2, in
       }
     }
     __syncwarp();
+    // the next chunk's key is loaded before this chunk's scatter (the keys
+    // are only read here; the scatter writes the other buffer)
+    uint64_t next_key = lane < n ? k[lane] : 0;
     for (int base = 0; base < n; base += 32) {
       const int i = base + lane;
       const bool ok = i < n;
-      const uint64_t key = ok ? k[i] : 0;
+      const uint64_t key = next_key;
+      next_key = base + 32 + lane < n ? k[base + 32 + lane] : 0;
       const int32_t val = (ok && v) ? v[i] : 0;
       const int d = ok ? (int)((key >> shift) & mask) : 256 + lane;
       const unsigned peers = __match_any_sync(FULL, d);
