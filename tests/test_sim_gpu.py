@@ -343,3 +343,39 @@ def test_ils_kernels_agree_and_tie_fallback(ctx, orc, lockstep):
             if not f.startswith("h_"):
                 assert getattr(a[t], f) == getattr(b[t], f), (t, f, getattr(a[t], f), getattr(b[t], f))
     assert np.array_equal(ha, hb)
+
+
+@pytest.mark.slow
+def test_randomized_metrics_only_sweep_vs_reference(ctx, orc):
+    """A larger randomized parity sweep of the metrics-only kernels (the
+    bench path): 360 traces generated on the device under random configs of
+    all three policies -- workers 1..32, slices 16..512, max-gen 64..1024,
+    batch caps, concurrency caps, short horizons, both memory models --
+    against the compiled reference, every report field and histogram."""
+    from oracle import pyoracle
+    ref = pyoracle.ref_lib() or orc
+    lat = capi.builtin_latency_model()
+    rng = np.random.default_rng(2026)
+    for mem in (MEMORIES["rule"](), MEMORIES["analytic"]()):
+        specs, cfgs = [], []
+        for trial in range(180):
+            G = int(rng.choice([64, 256, 512, 1024]))
+            S = int(rng.choice([s for s in (16, 32, 64, 128, 256, 512) if s <= G]))
+            specs.append(capi.workload_spec(rate=float(rng.uniform(0.5, 40)), duration_s=float(rng.uniform(5, 150)),
+                                            seed=int(rng.integers(0, 2 ** 40)), max_gen_limit=G))
+            cfgs.append(capi.sched_cfg(policy=("scls", "sls", "ils")[trial % 3], worker_count=int(rng.integers(1, 33)),
+                                       slice_len=S, max_gen_limit=G, fixed_batch_size=int(rng.integers(1, 48)),
+                                       max_concurrent=int(rng.integers(1, 24)),
+                                       horizon_s=1e7 if trial % 9 else float(rng.uniform(5, 80))))
+        ctx.set_digests(False)
+        try:
+            a, ha = ctx.run_experiments(specs, cfgs, lat, mem, hist_bins=64)
+        finally:
+            ctx.set_digests(True)
+        traces = [ref.generate(s) for s in specs]
+        b, hb = ref.simulate(traces, cfgs, lat, mem, cfg_index=list(range(len(cfgs))), hist_bins=64, threads=8)
+        for t in range(len(specs)):
+            for f in FIELDS:
+                if not f.startswith("h_"):
+                    assert getattr(a[t], f) == getattr(b[t], f), (t, cfgs[t].policy, f)
+        assert np.array_equal(ha, np.asarray(hb).reshape(ha.shape))
