@@ -160,8 +160,8 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
   __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
   __shared__ double swin_r[kSimWarps][kMergeWin];
   __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
-  __shared__ int4 srun[kSimWarps][2][kIndepRun];   // running slots, ping-pong
-  __shared__ double sra[kSimWarps][2][kIndepRun];  // their arrival times
+  __shared__ int4 srun[kSimWarps][2][kIndepRun];   // running slots; [1]: the joins of a boundary
+  __shared__ double sra[kSimWarps][kIndepRun];     // their arrival times
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * (blockDim.x >> 5) + warp;  // launches use 1 or kSimWarps warps per CTA
   if (g >= count) return;
@@ -218,17 +218,17 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
   {
     const int w = lane;
     const bool active = lane < W;
-    // running slots {join iteration, min(gen, G), input, -} + their arrival
-    // times, in running order; a boundary compacts from one buffer to the other
+    // running slots {exit iteration, join iteration, input, -} + their
+    // arrival times, sorted by exit iteration (see the boundary below)
     int4* run = srun[warp][0] + w * MC;
-    double* ra = sra[warp][0] + w * MC;
+    double* ra = sra[warp] + w * MC;
     int4* run2 = srun[warp][1] + w * MC;
-    double* ra2 = sra[warp][1] + w * MC;
     IlsRec rec{(double*)(base + Lay.ct) + w * cap_w, (double*)(base + Lay.cp) + w * cap_w,
                (double*)(base + Lay.cr) + w * cap_w};
     const int n_mine = active && w < n ? (n - 1 - w) / W + 1 : 0;  // requests w, w + W, ...
     int f_head = 0, f_tail = 0;  // joined / arrived (FIFO as counters)
     int n_run = 0, it_cnt = 0, seg_it = 0, seg_n = 0, room = 0;
+    int mxd = (-2147483647 - 1);  // max over the running set of (input - join iteration)
     bool seg = false, boundary = false;
     double ev_t = dinf(), t_push = 0.0;
     double a1 = 0.0, a2 = 0.0, dl = 0.0;  // step-time terms of the current membership, next context
@@ -297,49 +297,47 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
         it_cnt = it1;
         ++seg_it;
       }
-      int nexit = 0, keep = 0, mc = 0, nx = 0x7fffffff;
-      // four slots per trip, loads first (the compiler cannot prove the
-      // ping-pong buffers disjoint, so it would not hoist them itself)
-      for (int i = 0; i < nr; i += 4) {
-        int4 v[4];
-        double a[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          v[u] = i + u < nr ? run[i + u] : make_int4(0, 0x7fffffff, 0, 0);
-          a[u] = i + u < nr ? ra[i + u] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (i + u >= nr) break;
-          if (it1 - v[u].x >= v[u].y) {
-            rec.t[comp + nexit] = now;
-            rec.tp[comp + nexit] = t_push;
-            rec.r[comp + nexit] = now - a[u];
-            ++nexit;
-          } else {
-            run2[keep] = v[u];
-            ra2[keep] = a[u];
-            ++keep;
-            mc = max(mc, v[u].z + (it1 - v[u].x));
-            nx = min(nx, v[u].x + v[u].y);
-          }
-        }
+      // The running set is kept sorted by exit iteration, descending, ties
+      // with the earliest joined last: a boundary's exits are a suffix
+      // (completed back to front = join order, sched_policies.cpp:300-313),
+      // a join is an insertion, and the first exit is the last slot.  The
+      // largest (input - join) over the set is kept in a register and
+      // rescanned only when its slot exits.
+      int nexit = 0;
+      bool lost_max = false;
+      while (nexit < nr) {
+        const int q = nr - 1 - nexit;
+        const int4 v = run[q];  // {exit iteration, join iteration, input, -}
+        if (v.x > it1) break;
+        rec.t[comp + nexit] = now;
+        rec.tp[comp + nexit] = t_push;
+        rec.r[comp + nexit] = now - ra[q];
+        lost_max |= v.z - v.y == mxd;
+        ++nexit;
       }
-      {  // the compacted buffer becomes the running set
-        int4* tr = run;
-        run = run2;
-        run2 = tr;
-        double* ta = ra;
-        ra = ra2;
-        ra2 = ta;
+      int keep = nr - nexit;
+      if (lost_max) {
+        mxd = (-2147483647 - 1);
+        for (int q = 0; q < keep; ++q) {
+          const int4 v = run[q];
+          mxd = max(mxd, v.z - v.y);
+        }
       }
       const int njoin = min(MC - keep, f_tail - f_head);
+      int* jin = (int*)run2;  // the joins' inputs in join order (prefill order)
       for (int j = 0; j < njoin; ++j) {
         const int lim = min(j_g, G);
-        run[keep + j] = make_int4(it1, lim, j_i, 0);
-        ra[keep + j] = j_a;
-        mc = max(mc, j_i);
-        nx = min(nx, it1 + lim);
+        const int ex = it1 + lim;
+        int pos = keep + j;
+        while (pos > 0 && run[pos - 1].x <= ex) {  // slots exiting no later move behind it
+          run[pos] = run[pos - 1];
+          ra[pos] = ra[pos - 1];
+          --pos;
+        }
+        run[pos] = make_int4(ex, it1, j_i, 0);
+        ra[pos] = j_a;
+        jin[j] = j_i;
+        mxd = max(mxd, j_i - it1);
         ++f_head;
         if (f_head < n_mine) {
           const int id = w + f_head * W;
@@ -350,6 +348,8 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
       }
       const int nr_new = keep + njoin;
       n_run = nr_new;
+      const int mc = mxd + it1;
+      const int nx = nr_new > 0 ? run[nr_new - 1].x : 0x7fffffff;
       const bool changed = nexit > 0 || njoin > 0;
       if (changed && seg && seg_it > 0) {  // batch_end record
         ++batch_count;
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
           seg_it = 0;
         }
         double it = decode_step_time(lat, mc, nr_new);
-        for (int j = keep; j < nr_new; ++j) it = __dadd_rn(it, prefill_time(lat, 1, run[j].z));
+        for (int j = 0; j < njoin; ++j) it = __dadd_rn(it, prefill_time(lat, 1, jin[j]));
         n_disp += njoin;
         n_ev += njoin;
         const double dn = (double)nr_new;
