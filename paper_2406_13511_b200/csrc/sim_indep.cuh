@@ -525,13 +525,21 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
       const int take = min(B, f_tail - f_head);
       int lin = 0, lout = 0;
       long long so = 0, sg = 0;
-      for (int j = 0; j < take; ++j) {
-        const int id = w + (f_head + j) * W;
-        const int o = inp[id], gm = min(tg[id], G);
-        lin = max(lin, o);
-        lout = max(lout, gm);
-        so += o;
-        sg += gm;
+      for (int j0 = 0; j0 < take; j0 += 4) {  // four members per trip, loads first
+        int o[4], gm[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int id = w + (f_head + j0 + u) * W;
+          o[u] = j0 + u < take ? inp[id] : 0;
+          gm[u] = j0 + u < take ? min(tg[id], G) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          lin = max(lin, o[u]);
+          lout = max(lout, gm[u]);
+          so += o[u];
+          sg += gm[u];
+        }
       }
       // batch_end accounting (sched_policies.cpp:255-266): pad = l_in - orig,
       // invalid = served - min(gen, G), summed over members
@@ -566,12 +574,20 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
         ++batch_count;
         batch_members += b_n;
         last_end = fmax(last_end, now);
-        for (int j = 0; j < b_n; ++j) {
-          const int id = w + (b_head + j) * W;
-          rt[comp + j] = now;
-          rp[comp + j] = b_start;
-          rr[comp + j] = now - arr[id];
-          rn[comp + j] = j == 0 ? b_n : 0;
+        for (int j0 = 0; j0 < b_n; j0 += 4) {  // four members per trip, loads first
+          double av[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) av[u] = j0 + u < b_n ? arr[w + (b_head + j0 + u) * W] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u;
+            if (j < b_n) {
+              rt[comp + j] = now;
+              rp[comp + j] = b_start;
+              rr[comp + j] = now - av[u];
+              rn[comp + j] = j == 0 ? b_n : 0;
+            }
+          }
         }
         comp += b_n;
         n_ev += 1 + b_n;  // batch_end + completions
