@@ -81,7 +81,7 @@ typedef struct scls_sched_cfg {
   int32_t max_gen_limit;
   int32_t fixed_batch_size;
   int32_t max_concurrent;
-  int32_t worker_count;
+  int32_t worker_count;  // >= 1; the device simulator takes up to 1024
   double lambda;
   double gamma;
   double horizon_s;

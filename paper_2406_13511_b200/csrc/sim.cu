@@ -15,7 +15,8 @@
 // accumulated in that order.
 //
 // Per-trace state lives in a per-trace arena (sim_layout) in global memory;
-// worker state lives in the lanes' registers (W <= 32).  The SCLS tick runs
+// worker state lives in the lanes' registers (W <= 32; wider configs run a
+// variant with 32 worker slots per lane, W <= 1024).  The SCLS tick runs
 // the scheduling core warp-wide: LSD radix sort of the pool by
 // (eff, arrival-rank == id), the Eq. 10 DP with a per-config cost table, the
 // backtrack, the stable descending estimate order and the max-min offload.
@@ -288,9 +289,78 @@ __device__ bool warp_radix_sort(int n, uint64_t* k, int32_t* v, uint64_t* k2, in
 
 __device__ __forceinline__ int bits_of(uint32_t x) { return x ? 32 - __clz(x) : 0; }
 
+// Per-worker (SCLS/SLS) / per-instance (ILS) state.  Worker w lives in lane
+// w & 31, slot w >> 5 of that lane's V slots: V = 1 (W <= 32, registers) or
+// kWideV (W <= 32 * kWideV, the slots in local memory).
+constexpr int kWideV = 32;
+constexpr int kMaxWorkers = 32 * kWideV;
+struct WorkerState {
+  double ev_t = dinf();  // pending BatchDone / ILS boundary
+  unsigned long long ev_s = ~0ull;
+  double load = 0.0, last_end = 0.0;
+  int busy = 0, infl = -1, q_head = -1, q_tail = -1;
+  int f_head = 0, f_tail = 0;  // SLS pending / ILS waiting FIFO
+  int inf_start = 0, inf_n = 0, inf_lin = 0, inf_lout = 0;  // SLS in-flight batch
+  long long inf_id = 0;
+  int n_run = 0, boundary = 0, seg_n = 0, seg_lin = 0, seg_it = 0;  // ILS
+  int it_cnt = 0, next_exit = 0, mctx = 0;
+  long long seg_id = -1;
+};
+
+// The (t, seq)-earliest pending worker event (seqs are distinct), or -1.
+template <int V>
+__device__ __forceinline__ int argmin_worker_event(const WorkerState* ws, int W, int lane, double* bt,
+                                                   unsigned long long* bs) {
+  if (V == 1) return argmin_event_redux(ws[0].ev_t, ws[0].ev_s, lane < W && ws[0].ev_t != dinf(), lane, bt, bs);
+  double t = dinf();
+  unsigned long long s = ~0ull;
+  int v = 0;
+  for (int q = 0; q < V; ++q) {
+    const bool ok = q * 32 + lane < W && ws[q].ev_t != dinf();
+    if (ok && (ws[q].ev_t < t || (ws[q].ev_t == t && ws[q].ev_s < s))) {
+      t = ws[q].ev_t;
+      s = ws[q].ev_s;
+      v = q;
+    }
+  }
+  const int l = argmin_event_redux(t, s, t != dinf(), lane, bt, bs);
+  return shfl_i(v, l) * 32 + l;
+}
+
+// The worker with the minimal (load, worker id) (offloader.cpp:41-48).
+template <int V>
+__device__ __forceinline__ int argmin_worker_load(const WorkerState* ws, int W, int lane) {
+  double bt;
+  unsigned long long bs;
+  if (V == 1)  // loads are >= 0, so (load, lane) keys order exactly
+    return argmin_event_redux(ws[0].load, (unsigned long long)lane, lane < W, lane, &bt, &bs);
+  double ld = dinf();
+  int v = 0;
+  bool has = false;
+  for (int q = 0; q < V; ++q)
+    if (q * 32 + lane < W && (!has || ws[q].load < ld)) {  // ascending slots: ties keep the lower id
+      ld = ws[q].load;
+      v = q;
+      has = true;
+    }
+  const int w = v * 32 + lane;
+  const int l = argmin_event_redux(ld, (unsigned long long)w, has, lane, &bt, &bs);
+  return shfl_i(w, l);
+}
+
+// min over workers of load (sched_policies.cpp:134-146).
+template <int V>
+__device__ __forceinline__ double min_worker_load(const WorkerState* ws, int W, int lane) {
+  double ml = dinf();
+  for (int q = 0; q < V; ++q)
+    if (q * 32 + lane < W) ml = fmin(ml, ws[q].load);
+  for (int o = 16; o; o >>= 1) ml = fmin(ml, __shfl_xor_sync(FULL, ml, o));
+  return ml;
+}
+
 // ---- the per-trace simulation -------------------------------------------------------
 
-template <int POL, bool kHash, bool kLog>
+template <int POL, bool kHash, bool kLog, int V>
 __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, int32_t* ssplit, double* sT) {
   const int ts = P.src ? P.src[t] : t;  // source trace of job t
   const int64_t r0 = P.req_off[ts];
@@ -341,20 +411,13 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
             logging ? P.mems + (int64_t)t * P.mem_cap : nullptr, logging ? P.rec_cap : 0,
             logging ? P.mem_cap : 0);
 
-  // Worker / instance registers (lane w < W).
-  double ev_t = dinf();            // pending BatchDone / ILS boundary
-  unsigned long long ev_s = ~0ull;
-  double load = 0.0, last_end = 0.0;
-  int busy = 0, infl = -1, q_head = -1, q_tail = -1;
-  int f_head = 0, f_tail = 0;      // SLS pending / ILS waiting FIFO
-  int inf_start = 0, inf_n = 0, inf_lin = 0, inf_lout = 0;  // SLS in-flight batch
-  long long inf_id = 0;
-  int n_run = 0, boundary = 0, seg_n = 0, seg_lin = 0, seg_it = 0;  // ILS
-  int it_cnt = 0, next_exit = 0, mctx = 0;
-  long long seg_id = -1;
+  // Worker / instance state: worker w in lane WL(w), slot WK(w) (see WorkerState).
+  WorkerState ws[V];
+#define WK(w) ws[V == 1 ? 0 : ((w) >> 5)]
+#define WL(w) (V == 1 ? (w) : ((w) & 31))
+#define MINE(w) (lane == WL(w))
 
   // Trace-wide uniform state.
-  const int rounds = W <= 1 ? 0 : bits_of((uint32_t)(W - 1));
   unsigned long long next_seq = (unsigned long long)n + 1;  // arrivals 0..n-1, EndOfRun n
   double clock = 0.0;
   int cur = 0, completed = 0;
@@ -390,7 +453,6 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   int32_t* b_next = (int32_t*)(base + Lay.b_next);
   double* b_est = (double*)(base + Lay.b_est);
   const int cap_w = W > 0 ? (n + W - 1) / W : 0;
-  int32_t* fifo = (int32_t*)(base + Lay.fifo) + (lane < W ? lane : 0) * (int64_t)cap_w;
   int32_t* fifo_base = (int32_t*)(base + Lay.fifo);
   double* pf_t = (double*)(base + Lay.pf_t);
   unsigned long long* pf_seq = (unsigned long long*)(base + Lay.pf_seq);
@@ -442,21 +504,23 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
 
   // sim_engine.cpp:63-84 start_next_batch (SCLS: batches queued per worker).
   auto start_next_scls = [&](int w) {
-    const int b = shfl_i(busy, w) ? -1 : shfl_i(q_head, w);
+    const int b = shfl_i(WK(w).busy, WL(w)) ? -1 : shfl_i(WK(w).q_head, WL(w));
     if (b < 0) return;
     const int nb_next = b_next[b];
-    if (lane == w) {
-      q_head = nb_next;
-      if (q_head < 0) q_tail = -1;
+    if (MINE(w)) {
+      WorkerState& k = WK(w);
+      k.q_head = nb_next;
+      if (k.q_head < 0) k.q_tail = -1;
     }
     const int bn = b_n[b], blin = b_lin[b], bsv = b_served[b];
     sink.record(lane, 3, clock, -1, w, b, bn, blin, 0, 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
     const double serve = batch_serve_time(lat, bn, blin, bsv);
-    if (lane == w) {
-      busy = 1;
-      infl = b;
-      ev_t = __dadd_rn(clock, serve);
-      ev_s = next_seq;
+    if (MINE(w)) {
+      WorkerState& k = WK(w);
+      k.busy = 1;
+      k.infl = b;
+      k.ev_t = __dadd_rn(clock, serve);
+      k.ev_s = next_seq;
     }
     ++next_seq;
   };
@@ -464,8 +528,8 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   // SLS try_dispatch (sched_policies.cpp:207-243): FCFS batch of <= B from
   // the worker's FIFO; starts at once (the worker is idle, queue empty).
   auto sls_try_dispatch = [&](int w) {
-    const int bz = shfl_i(busy, w);
-    const int head = shfl_i(f_head, w), tail = shfl_i(f_tail, w);
+    const int bz = shfl_i(WK(w).busy, WL(w));
+    const int head = shfl_i(WK(w).f_head, WL(w)), tail = shfl_i(WK(w).f_tail, WL(w));
     if (bz || tail == head) return;
     const int take = min(C.B, tail - head);
     const int32_t* q = fifo_base + (int64_t)w * cap_w;
@@ -484,16 +548,17 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     const double est = batch_serve_time(lat, take, lin, lout);
     sink.record(lane, 2, clock, -1, w, bid, take, lin, lout, 0, est, 0, 0, 0.0, 0, 0.0, 0);
     sink.record(lane, 3, clock, -1, w, bid, take, lin, 0, 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
-    if (lane == w) {
-      f_head = head + take;
-      busy = 1;
-      inf_start = head;
-      inf_n = take;
-      inf_lin = lin;
-      inf_lout = lout;
-      inf_id = bid;
-      ev_t = __dadd_rn(clock, est);  // serve time == est (served l_out == planned)
-      ev_s = next_seq;
+    if (MINE(w)) {
+      WorkerState& k = WK(w);
+      k.f_head = head + take;
+      k.busy = 1;
+      k.inf_start = head;
+      k.inf_n = take;
+      k.inf_lin = lin;
+      k.inf_lout = lout;
+      k.inf_id = bid;
+      k.ev_t = __dadd_rn(clock, est);  // serve time == est (served l_out == planned)
+      k.ev_s = next_seq;
     }
     ++next_seq;
   };
@@ -769,28 +834,25 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     for (int k = 0; k < nb; ++k) {
       const int b = first + order[k];
       const double e = b_est[b];
-      double bt;
-      unsigned long long bs;
-      // min (load, worker id): loads are >= 0, so (load, lane) keys order exactly
-      const int w = argmin_event_redux(load, (unsigned long long)lane, lane < W, lane, &bt, &bs);
-      if (lane == w) load = __dadd_rn(load, e);
+      const int w = argmin_worker_load<V>(ws, W, lane);  // min (load, worker id)
+      if (MINE(w)) WK(w).load = __dadd_rn(WK(w).load, e);
       // dispatch record (served l_out computed at emit), enqueue
       const int bn = b_n[b];
       sink.record(lane, 2, clock, -1, w, b, bn, b_lin[b], C.S, 0, e, 0, 0, 0.0, 0, 0.0, 0);
       if (lane == 0) b_next[b] = -1;
-      const int tail = shfl_i(q_tail, w);
+      const int tail = shfl_i(WK(w).q_tail, WL(w));
       if (lane == 0 && tail >= 0) b_next[tail] = b;
-      if (lane == w) {
-        if (q_tail < 0) q_head = b;
-        q_tail = b;
+      if (MINE(w)) {
+        WorkerState& k = WK(w);
+        if (k.q_tail < 0) k.q_head = b;
+        k.q_tail = b;
       }
       __syncwarp();
       start_next_scls(w);
     }
     SIM_PROF(7);
     // sched_policies.cpp:134-146: adaptive interval from the post-offload loads
-    double ml = lane < W ? load : dinf();
-    for (int o = 16; o; o >>= 1) ml = fmin(ml, __shfl_xor_sync(FULL, ml, o));
+    const double ml = min_worker_load<V>(ws, W, lane);
     const double a = __dmul_rn(C.lambda, ml);
     const double interval = a < C.gamma ? C.gamma : a;
     sink.record(lane, 1, clock, -1, -1, -1, nb, 0, 0, 0, 0.0, 0, 0, 0.0, 0, interval, 0);
@@ -881,18 +943,19 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       completed += cnt;
       if (cnt > 0) last_completion = clock;
     }
-    if (lane == w) {
-      last_end = fmax(last_end, clock);
-      load = load - best;  // offloader.cpp:56-59 complete_batch
-      if (load < 0.0) load = 0.0;
+    if (MINE(w)) {
+      WorkerState& k = WK(w);
+      k.last_end = fmax(k.last_end, clock);
+      k.load = k.load - best;  // offloader.cpp:56-59 complete_batch
+      if (k.load < 0.0) k.load = 0.0;
     }
   };
 
   // SLS on_batch_done (sched_policies.cpp:245-273).
   auto sls_done = [&](int w) {
-    const int start = shfl_i(inf_start, w), bn = shfl_i(inf_n, w), lin = shfl_i(inf_lin, w),
-              lout = shfl_i(inf_lout, w);
-    const long long bid = shfl_l(inf_id, w);
+    const int start = shfl_i(WK(w).inf_start, WL(w)), bn = shfl_i(WK(w).inf_n, WL(w)),
+              lin = shfl_i(WK(w).inf_lin, WL(w)), lout = shfl_i(WK(w).inf_lout, WL(w));
+    const long long bid = shfl_l(WK(w).inf_id, WL(w));
     sink.record(lane, 4, clock, -1, w, bid, bn, lin, lout, lout, 0.0, 0, 0, 0.0, 0, 0.0, bn);
     ++batch_count;
     batch_members += bn;
@@ -921,9 +984,10 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       const int id = lane < cnt ? q[start + c0 + lane] : 0;
       complete_chunk(cnt, id, w);
     }
-    if (lane == w) {
-      last_end = fmax(last_end, clock);
-      busy = 0;
+    if (MINE(w)) {
+      WorkerState& k = WK(w);
+      k.last_end = fmax(k.last_end, clock);
+      k.busy = 0;
     }
     sls_try_dispatch(w);
   };
@@ -940,25 +1004,27 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     const double now = clock;
     int4* run = (int4*)run_base + (int64_t)w * C.MC;
     const int32_t* wq = fifo_base + (int64_t)w * cap_w;
-    const int nr = shfl_i(n_run, w);
-    const int it1 = shfl_i(it_cnt, w) + (nr > 0 ? 1 : 0);
-    const int head = shfl_i(f_head, w), tail = shfl_i(f_tail, w);
-    const bool exit_possible = nr > 0 && it1 >= shfl_i(next_exit, w);
+    const int wl = WL(w);
+    const int nr = shfl_i(WK(w).n_run, wl);
+    const int it1 = shfl_i(WK(w).it_cnt, wl) + (nr > 0 ? 1 : 0);
+    const int head = shfl_i(WK(w).f_head, wl), tail = shfl_i(WK(w).f_tail, wl);
+    const bool exit_possible = nr > 0 && it1 >= shfl_i(WK(w).next_exit, wl);
     const bool join_possible = tail > head && (nr < C.MC || exit_possible);
     if (nr > 0 && !exit_possible && !join_possible) {  // unchanged iteration
-      if (lane == w) {
-        it_cnt = it1;
-        seg_it += 1;
-        mctx += 1;
-        ev_t = __dadd_rn(now, decode_step_time(lat, mctx, nr));
-        ev_s = next_seq;
+      if (lane == wl) {
+        WorkerState& k = WK(w);
+        k.it_cnt = it1;
+        k.seg_it += 1;
+        k.mctx += 1;
+        k.ev_t = __dadd_rn(now, decode_step_time(lat, k.mctx, nr));
+        k.ev_s = next_seq;
       }
       ++next_seq;
       return;
     }
-    if (nr > 0 && lane == w) {
-      it_cnt = it1;
-      seg_it += 1;
+    if (nr > 0 && lane == wl) {
+      WK(w).it_cnt = it1;
+      WK(w).seg_it += 1;
     }
     // retire: survivors compacted in order, exits in member order
     int nexit = 0, keep = 0;
@@ -988,21 +1054,21 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     }
     __syncwarp();
     const int nr_new = keep + njoin;
-    if (lane == w) {
-      f_head = head + njoin;
-      n_run = nr_new;
+    if (lane == wl) {
+      WK(w).f_head = head + njoin;
+      WK(w).n_run = nr_new;
     }
     const bool changed = nexit > 0 || njoin > 0;
-    const long long sid = shfl_l(seg_id, w);
-    const int sit = shfl_i(seg_it, w);
+    const long long sid = shfl_l(WK(w).seg_id, wl);
+    const int sit = shfl_i(WK(w).seg_it, wl);
     if (changed && sid >= 0 && sit > 0) {
-      const int sn = shfl_i(seg_n, w), slin = shfl_i(seg_lin, w);
+      const int sn = shfl_i(WK(w).seg_n, wl), slin = shfl_i(WK(w).seg_lin, wl);
       sink.record(lane, 4, now, -1, w, sid, sn, slin, sit, sit, 0.0, 0, 0, 0.0, 0, 0.0, 0);
       ++batch_count;
       batch_members += sn;
-      if (lane == w) {
-        seg_id = -1;
-        last_end = fmax(last_end, now);
+      if (lane == wl) {
+        WK(w).seg_id = -1;
+        WK(w).last_end = fmax(WK(w).last_end, now);
       }
     }
     for (int c0 = 0; c0 < nexit; c0 += 32) {
@@ -1012,7 +1078,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       complete_chunk(cnt, id, w);
     }
     if (nr_new == 0) {
-      if (lane == w) boundary = 0;
+      if (lane == wl) WK(w).boundary = 0;
       return;
     }
     int mc = 0, nx = 0x7fffffff;
@@ -1026,11 +1092,12 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     long long cur_seg = sid;
     if (changed) {
       cur_seg = next_batch++;
-      if (lane == w) {
-        seg_id = cur_seg;
-        seg_n = nr_new;
-        seg_lin = mc;
-        seg_it = 0;
+      if (lane == wl) {
+        WorkerState& k = WK(w);
+        k.seg_id = cur_seg;
+        k.seg_n = nr_new;
+        k.seg_lin = mc;
+        k.seg_it = 0;
       }
       sink.record(lane, 3, now, -1, w, cur_seg, nr_new, mc, 0, 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
     }
@@ -1042,12 +1109,13 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       // planned_l_out = remaining_gen() = true_gen (nothing generated yet), sched_policies.cpp:384
       sink.record(lane, 2, now, v.x, w, cur_seg, 1, v.w, tg[v.x], 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
     }
-    if (lane == w) {
-      mctx = mc;
-      next_exit = nx;
-      ev_t = __dadd_rn(now, it);
-      ev_s = next_seq;
-      boundary = 1;
+    if (lane == wl) {
+      WorkerState& k = WK(w);
+      k.mctx = mc;
+      k.next_exit = nx;
+      k.ev_t = __dadd_rn(now, it);
+      k.ev_s = next_seq;
+      k.boundary = 1;
     }
     ++next_seq;
   };
@@ -1059,7 +1127,8 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   unsigned long long na_s = ~0ull;
   int na_w = -1;  // -1: tick / FIFO head, >= 0: lane slot
   while (completed < n) {
-    if (POL == SCLS_POLICY_ILS) {
+    if (POL == SCLS_POLICY_ILS && V == 1) {
+      WorkerState& k = ws[0];
       // Fast lane: consecutive boundary events of instances whose iteration
       // neither retires nor admits anyone (see ils_event) — the bulk of an
       // ILS run.  Same (time, seq) order, same arithmetic as ils_event's
@@ -1068,11 +1137,11 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       // "next boundary is unchanged" flag; only the winner's lane changes
       // per step, the winner's time is rebuilt from the reduced key, and any
       // exact time tie is left to the general path (which orders by seq).
-      const bool has = lane < W && ev_t != dinf();
-      uint64_t key = has ? ordered_bits(ev_t) : ~0ull;
-      bool mine_fast = has && n_run > 0 && it_cnt + 1 < next_exit && !(f_tail > f_head && n_run < C.MC);
+      const bool has = lane < W && k.ev_t != dinf();
+      uint64_t key = has ? ordered_bits(k.ev_t) : ~0ull;
+      bool mine_fast = has && k.n_run > 0 && k.it_cnt + 1 < k.next_exit && !(k.f_tail > k.f_head && k.n_run < C.MC);
       // decode_step_time(mctx, n) = ((d1*n)*l + d2*n) + d3*l + d4: the n terms are fixed in a run
-      const double dn = (double)n_run;
+      const double dn = (double)k.n_run;
       const double a1 = __dmul_rn(lat.d1, dn), a2 = __dmul_rn(lat.d2, dn);
       for (;;) {
         const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
@@ -1089,15 +1158,15 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         if (!((__ballot_sync(FULL, mine_fast) >> w) & 1u)) break;
         clock = bt;
         if (lane == w) {
-          it_cnt += 1;
-          seg_it += 1;
-          mctx += 1;
-          const double dl = (double)mctx;
+          k.it_cnt += 1;
+          k.seg_it += 1;
+          k.mctx += 1;
+          const double dl = (double)k.mctx;
           const double it = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a1, dl), a2), __dmul_rn(lat.d3, dl)), lat.d4);
-          ev_t = __dadd_rn(bt, it);
-          ev_s = next_seq;
-          key = ordered_bits(ev_t);
-          mine_fast = it_cnt + 1 < next_exit;
+          k.ev_t = __dadd_rn(bt, it);
+          k.ev_s = next_seq;
+          key = ordered_bits(k.ev_t);
+          mine_fast = k.it_cnt + 1 < k.next_exit;
         }
         ++next_seq;
       }
@@ -1106,7 +1175,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     if (dirty) {
       double bt;
       unsigned long long bs;
-      const int bw = argmin_event_redux(ev_t, ev_s, lane < W && ev_t != dinf(), lane, &bt, &bs);
+      const int bw = argmin_worker_event<V>(ws, W, lane, &bt, &bs);
       na_t = bt;
       na_s = bs;
       na_w = bw;
@@ -1171,7 +1240,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       const int w = rr;
       rr = rr + 1 == W ? 0 : rr + 1;
       if (POL == SCLS_POLICY_SLS) {  // sched_policies.cpp:194-201
-        if (lane == w) fifo[f_tail++] = id;
+        if (MINE(w)) fifo_base[(int64_t)w * cap_w + WK(w).f_tail++] = id;
         if (lane == 0) {
           pf_t[pf_tail] = clock;
           pf_seq[pf_tail] = next_seq;
@@ -1181,13 +1250,14 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         ++next_seq;
         dirty = dirty || pf_tail - pf_head == 1;
       } else {  // ILS, sched_policies.cpp:279-290
-        if (lane == w) fifo[f_tail++] = id;
-        const int wake = shfl_i(n_run == 0 && !boundary, w);
+        if (MINE(w)) fifo_base[(int64_t)w * cap_w + WK(w).f_tail++] = id;
+        const int wake = shfl_i(WK(w).n_run == 0 && !WK(w).boundary, WL(w));
         if (wake) {
-          if (lane == w) {
-            ev_t = clock;
-            ev_s = next_seq;
-            boundary = 1;
+          if (MINE(w)) {
+            WorkerState& k = WK(w);
+            k.ev_t = clock;
+            k.ev_s = next_seq;
+            k.boundary = 1;
           }
           ++next_seq;
           dirty = true;
@@ -1217,15 +1287,15 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       }
     } else {
       const int w = na_w;
-      if (lane == w) {
-        ev_t = dinf();
-        ev_s = ~0ull;
+      if (MINE(w)) {
+        WK(w).ev_t = dinf();
+        WK(w).ev_s = ~0ull;
       }
       if (POL == SCLS_POLICY_SCLS) {
-        const int b = shfl_i(infl, w);
-        if (lane == w) {
-          busy = 0;
-          infl = -1;
+        const int b = shfl_i(WK(w).infl, WL(w));
+        if (MINE(w)) {
+          WK(w).busy = 0;
+          WK(w).infl = -1;
         }
         SIM_PROF(8);
         scls_done(w, b);
@@ -1294,10 +1364,10 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     }
     // population std of per-worker last batch end (metrics.cpp:93-101)
     double mean = 0.0, var = 0.0;
-    for (int w = 0; w < W; ++w) mean = __dadd_rn(mean, shfl_d(last_end, w));
+    for (int w = 0; w < W; ++w) mean = __dadd_rn(mean, shfl_d(WK(w).last_end, WL(w)));
     mean = __ddiv_rn(mean, (double)W);
     for (int w = 0; w < W; ++w) {
-      const double d = __dadd_rn(shfl_d(last_end, w), -mean);
+      const double d = __dadd_rn(shfl_d(WK(w).last_end, WL(w)), -mean);
       var = __dadd_rn(var, __dmul_rn(d, d));
     }
     var = __ddiv_rn(var, (double)W);
@@ -1352,9 +1422,12 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       P.mem_count[t] = sink.mem_n;
     }
   }
+#undef WK
+#undef WL
+#undef MINE
 }
 
-template <int POL, bool kHash, bool kLog>
+template <int POL, bool kHash, bool kLog, int V = 1>
 __global__ void __launch_bounds__(kSimWarps * 32, POL == SCLS_POLICY_SCLS ? SCLS_SIM_MINB : 8) sim_kernel(SimParams p, const int32_t* __restrict__ list,
                                                               int32_t count, const int32_t* __restrict__ dcount = nullptr) {
   if (dcount) count = *dcount;  // fallback launches: the job count lives on the device
@@ -1365,7 +1438,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, POL == SCLS_POLICY_SCLS ? SCLS
   const int g = blockIdx.x * (blockDim.x >> 5) + warp;  // launches use 1 or kSimWarps warps per CTA
   if (g >= count) return;
   if (list[g] < 0) return;  // an empty slot (small launches: one job per CTA)
-  run_trace<POL, kHash, kLog>(p, list[g], lane, bins[warp], ssplit[POL == SCLS_POLICY_SCLS ? warp : 0],
+  run_trace<POL, kHash, kLog, V>(p, list[g], lane, bins[warp], ssplit[POL == SCLS_POLICY_SCLS ? warp : 0],
                               sT[POL == SCLS_POLICY_SCLS ? warp : 0]);
 }
 
@@ -1499,8 +1572,8 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   int32_t Gmax = 1;
   for (int c = 0; c < n_cfgs; ++c) {
     const scls_sched_cfg& x = cfgs[c];
-    if (x.worker_count > 32 && validate_cfg_host(x) == SCLS_OK)
-      return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "device simulator supports worker_count <= 32");
+    if (x.worker_count > kMaxWorkers && validate_cfg_host(x) == SCLS_OK)
+      return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "device simulator supports worker_count <= 1024");
     hok[c] = model_ok && validate_cfg_host(x) == SCLS_OK;
     hc[c] = SimCfg{x.policy, x.slice_len, x.max_gen_limit, x.fixed_batch_size, x.max_concurrent,
                    x.worker_count, x.lambda, x.gamma, x.horizon_s, -1, mono && ctx->dp_mode != 1};
@@ -1671,10 +1744,12 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   SCLS_CUDA(cudaEventRecord(ctx->ev[1], s));
   // One launch per policy over that policy's traces (compile-time policy
   // keeps each kernel lean); invalid configs ride along (status Error).
-  std::vector<int32_t> lists[3];
+  // lists[3 + pol]: configs with more than 32 workers (the wide variant).
+  std::vector<int32_t> lists[6];
   for (int t = 0; t < n_traces; ++t) {
-    const int pol = hc[cfg_index ? h_idx[t] : 0].policy;
-    lists[(pol >= 0 && pol <= 2) ? pol : 0].push_back(t);
+    const SimCfg& c = hc[cfg_index ? h_idx[t] : 0];
+    const int pol = c.policy;
+    lists[((pol >= 0 && pol <= 2) ? pol : 0) + (c.W > 32 ? 3 : 0)].push_back(t);
   }
   // Longest jobs first (work ~ requests; SCLS: served slices): a launch that
   // needs more than one wave of warps starts its slowest jobs first and fills
@@ -1716,7 +1791,7 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   // Per-policy launches; with more than one policy they run concurrently on
   // forked streams so one kernel's tail overlaps the others' work.
   int n_pol = 0;
-  for (auto& l : lists) n_pol += !l.empty();
+  for (int q = 0; q < 3; ++q) n_pol += !lists[q].empty() || !lists[3 + q].empty();
   const bool fork = ctx->sim_concurrent && n_pol > 1;
   if (fork) {
     for (auto& st : ctx->side)
@@ -1726,10 +1801,11 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   int64_t at = 0;
   int k = 0;
   for (int pol : {SCLS_POLICY_ILS, SCLS_POLICY_SCLS, SCLS_POLICY_SLS}) {  // longest first
-    const int32_t cnt = (int32_t)lists[pol].size();
-    int64_t off = 0;
+    const int32_t cnt = (int32_t)lists[pol].size(), wcnt = (int32_t)lists[3 + pol].size();
+    int64_t off = 0, woff = 0;
     for (int q = 0; q < pol; ++q) off += (int64_t)lists[q].size();
-    if (cnt == 0) continue;
+    for (int q = 0; q < 3 + pol; ++q) woff += (int64_t)lists[q].size();
+    if (cnt == 0 && wcnt == 0) continue;
     cudaStream_t ls = s;
     if (fork) {
       ls = ctx->side[k];
@@ -1743,7 +1819,21 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   if (want_log) sim_kernel<POLV, true, true><<<grid, wpb * 32, 0, ls>>>(p, l, cnt);          \
   else if (hash) sim_kernel<POLV, true, false><<<grid, wpb * 32, 0, ls>>>(p, l, cnt);        \
   else sim_kernel<POLV, false, false><<<grid, wpb * 32, 0, ls>>>(p, l, cnt);
-    if (pol == SCLS_POLICY_SCLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SCLS) }
+#define SCLS_SIM_LAUNCH_WIDE(POLV)                                                                     \
+  if (want_log) sim_kernel<POLV, true, true, kWideV><<<wgrid, wpb * 32, 0, ls>>>(p, wl, wcnt);   \
+  else if (hash) sim_kernel<POLV, true, false, kWideV><<<wgrid, wpb * 32, 0, ls>>>(p, wl, wcnt); \
+  else sim_kernel<POLV, false, false, kWideV><<<wgrid, wpb * 32, 0, ls>>>(p, wl, wcnt);
+    if (wcnt > 0) {  // more than 32 workers: the lock-step kernel with 32 worker slots per lane
+      const int wgrid = div_up(wcnt, wpb);
+      const int32_t* wl = d_lists + woff;
+      if (pol == SCLS_POLICY_SCLS) { SCLS_SIM_LAUNCH_WIDE(SCLS_POLICY_SCLS) }
+      else if (pol == SCLS_POLICY_SLS) { SCLS_SIM_LAUNCH_WIDE(SCLS_POLICY_SLS) }
+      else { SCLS_SIM_LAUNCH_WIDE(SCLS_POLICY_ILS) }
+      SCLS_LAUNCHED();
+    }
+#undef SCLS_SIM_LAUNCH_WIDE
+    if (cnt == 0) {
+    } else if (pol == SCLS_POLICY_SCLS) { SCLS_SIM_LAUNCH(SCLS_POLICY_SCLS) }
     else if (pol == SCLS_POLICY_SLS && !want_log && !hash && !ctx->ils_lockstep) {
       // independent worker lanes; exact cross-worker ties re-run in lock step
       SCLS_CUDA(cudaMemsetAsync(d_fb_sls, 0, sizeof(int32_t), ls));
@@ -1763,7 +1853,7 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
     }
     else { SCLS_SIM_LAUNCH(SCLS_POLICY_ILS) }
 #undef SCLS_SIM_LAUNCH
-    SCLS_LAUNCHED();
+    if (cnt > 0) SCLS_LAUNCHED();
     if (fork) {
       SCLS_CUDA(cudaEventRecord(ctx->ev[9 + k], ls));
       SCLS_CUDA(cudaStreamWaitEvent(s, ctx->ev[9 + k], 0));

@@ -61,6 +61,12 @@ CASES = [
      ["s.csv"]),
     ("sweep_workers_ils", "sweep --param workers --values 1,4,8 --set policy.kind=ils --set workload.duration=120 "
      "--out {d}/s.csv", ["s.csv"]),
+    ("run_scls_64_workers", "run --set policy.workers=64 --set workload.rate=150 --set workload.duration=40 "
+     "--report {d}/r.json --event-log {d}/e.jsonl", ["r.json", "e.jsonl"]),
+    ("sweep_workers_wide", "sweep --param workers --values 16,48,100 --set workload.rate=120 "
+     "--set workload.duration=40 --out {d}/s.csv", ["s.csv"]),
+    ("sweep_workers_wide_sls", "sweep --param workers --values 40,200 --set policy.kind=sls --set workload.rate=120 "
+     "--set workload.duration=40 --out {d}/s.csv", ["s.csv"]),
     ("gen_workload", "gen-workload --set workload.duration=60 --out {d}/t.csv", ["t.csv"]),
 ]
 

@@ -379,3 +379,58 @@ def test_randomized_metrics_only_sweep_vs_reference(ctx, orc):
                 if not f.startswith("h_"):
                     assert getattr(a[t], f) == getattr(b[t], f), (t, cfgs[t].policy, f)
         assert np.array_equal(ha, np.asarray(hb).reshape(ha.shape))
+
+
+@pytest.mark.parametrize("digests", [True, False])
+def test_wide_worker_counts_vs_oracle(ctx, orc, digests):
+    """More than 32 workers / instances (the reference allows any count,
+    sched_policies.cpp:56): the wide lock-step variant (32 worker slots per
+    lane) against the oracle, mixed with narrow configs in one launch, with
+    and without digests (without: the metrics-only launch path)."""
+    lat = capi.builtin_latency_model()
+    rng = np.random.default_rng(33)
+    cfgs, traces, idx = [], [], []
+    for i, w in enumerate((33, 40, 64, 100, 257, 1024, 8)):
+        for pol in ("scls", "sls", "ils"):
+            cfgs.append(capi.sched_cfg(policy=pol, worker_count=w, slice_len=int(rng.choice([16, 64, 128])),
+                                       max_gen_limit=512, fixed_batch_size=int(rng.integers(1, 12)),
+                                       max_concurrent=int(rng.integers(1, 16))))
+    for j in range(len(cfgs)):
+        spec = capi.workload_spec(rate=float(rng.uniform(20, 400)), duration_s=float(rng.uniform(4, 20)),
+                                  seed=3300 + j)
+        traces.append(orc.generate(spec))
+        idx.append(j)
+    ctx.set_digests(digests)
+    try:
+        a, ha = ctx.simulate(traces, cfgs, lat, MEMORIES["rule"](), cfg_index=idx)
+    finally:
+        ctx.set_digests(True)
+    b, hb = orc.simulate(traces, cfgs, lat, MEMORIES["rule"](), cfg_index=idx)
+    for t in range(len(traces)):
+        for f in FIELDS:
+            if digests or not f.startswith("h_"):
+                assert getattr(a[t], f) == getattr(b[t], f), (t, cfgs[t].worker_count, cfgs[t].policy, f)
+    assert np.array_equal(ha, hb)
+
+
+def test_wide_worker_event_logs(ctx, orc):
+    lat = capi.builtin_latency_model()
+    traces = [orc.generate(capi.workload_spec(rate=150.0, duration_s=6.0, seed=91 + i)) for i in range(2)]
+    for pol in ("scls", "sls", "ils"):
+        cfg = capi.sched_cfg(policy=pol, worker_count=70, slice_len=64, max_concurrent=4, fixed_batch_size=4)
+        a, _, la = ctx.simulate(traces, cfg, lat, MEMORIES["rule"](), n_logged=2, rec_cap=40000, mem_cap=40000)
+        b, _, lb = orc.simulate(traces, cfg, lat, MEMORIES["rule"](), n_logged=2, rec_cap=40000, mem_cap=40000)
+        for t in range(2):
+            assert_results_equal(a[t], b[t], (pol, t))
+            ra, ma = _log_rows(la, t)
+            rb, mb = _log_rows(lb, t)
+            assert len(ra) == len(rb) and ma == mb, (pol, t)
+            assert ra == rb, pol
+            assert max(r[0][7] for r in ra) >= 33  # workers above 32 were used (record field `worker`)
+
+
+def test_worker_count_limit(ctx, orc):
+    lat = capi.builtin_latency_model()
+    trace = orc.generate(capi.workload_spec(rate=5.0, duration_s=5.0))
+    with pytest.raises(Exception, match="1024"):
+        ctx.simulate([trace], capi.sched_cfg(worker_count=1025), lat, MEMORIES["rule"]())
