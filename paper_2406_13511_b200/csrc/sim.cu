@@ -1783,6 +1783,52 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
     SCLS_CUDA(cudaMemcpyAsync(d_lists, flat.data(), sizeof(int32_t) * n_slots, cudaMemcpyHostToDevice, s));
   }
   const bool hash = ctx->sim_digests;
+  // Packs for the independent-lane kernels (sim_indep.cuh): up to 32 / W jobs
+  // of one config per warp (ILS: within kPackSlots running slots), packs in
+  // LPT order of their longest job; one pack per CTA for small launches.
+  auto make_packs = [&](const std::vector<int32_t>& l, bool ils, std::vector<int32_t>& off,
+                        std::vector<int32_t>& flat) {
+    std::vector<std::vector<int32_t>> packs, open(n_cfgs);
+    auto work = [&](int32_t t) { return h_off[src_of(t) + 1] - h_off[src_of(t)]; };
+    for (int32_t t : l) {
+      if (t < 0) continue;
+      const int ci = cfg_index ? h_idx[t] : 0;
+      const SimCfg& c = hc[ci];
+      int G = std::max(1, 32 / std::max(c.W, 1));
+      if (ils) G = std::max(1, std::min(G, kPackSlots / std::max(1, c.W * std::max(c.MC, 1))));
+      open[ci].push_back(t);
+      if ((int)open[ci].size() == G) {
+        packs.push_back(std::move(open[ci]));
+        open[ci].clear();
+      }
+    }
+    for (auto& o : open)
+      if (!o.empty()) packs.push_back(std::move(o));
+    std::stable_sort(packs.begin(), packs.end(),
+                     [&](const std::vector<int32_t>& a, const std::vector<int32_t>& b) { return work(a[0]) > work(b[0]); });
+    const bool spread = packs.size() > 1 && packs.size() <= (size_t)ctx->sm_count;
+    off.assign(1, 0);
+    flat.clear();
+    for (auto& pk : packs) {
+      flat.insert(flat.end(), pk.begin(), pk.end());
+      off.push_back((int32_t)flat.size());
+      if (spread)
+        for (int w = 1; w < kSimWarps; ++w) off.push_back((int32_t)flat.size());
+    }
+  };
+  const bool indep = !want_log && !hash;
+  std::vector<int32_t> pk_off[3], pk_jobs[3];
+  int32_t* d_pk[3] = {nullptr, nullptr, nullptr};
+  for (int pol : {SCLS_POLICY_ILS}) {
+    if (!indep || ctx->ils_lockstep || lists[pol].empty()) continue;
+    make_packs(lists[pol], pol == SCLS_POLICY_ILS, pk_off[pol], pk_jobs[pol]);
+    const size_t m = pk_off[pol].size() + pk_jobs[pol].size();
+    d_pk[pol] = (int32_t*)ctx->buf(kSlotSim + 26 + pol, sizeof(int32_t) * m);
+    if (!d_pk[pol]) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+    std::vector<int32_t> h(pk_off[pol]);
+    h.insert(h.end(), pk_jobs[pol].begin(), pk_jobs[pol].end());
+    SCLS_CUDA(cudaMemcpyAsync(d_pk[pol], h.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, s));
+  }
   // lock-step fallback lists of the independent-lane kernels, one per policy
   // (the per-policy launches may run concurrently)
   int32_t* d_fb_ils = (int32_t*)ctx->buf(kSlotSim + 24, sizeof(int32_t) * (n_traces + 1));
@@ -1847,7 +1893,11 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
       // independent instance lanes; jobs with an exact cross-instance time tie
       // are re-run by the lock-step kernel from a device-side list
       SCLS_CUDA(cudaMemsetAsync(d_fb_ils, 0, sizeof(int32_t), ls));
-      sim_ils_indep_kernel<<<grid, wpb * 32, 0, ls>>>(p, l, cnt, d_fb_ils, d_fb_ils + 1);
+      const int32_t npk = (int32_t)pk_off[pol].size() - 1;
+      SCLS_CUDA(cudaFuncSetAttribute(sim_ils_indep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kIlsPackSmem));
+      sim_ils_indep_kernel<<<div_up(npk, wpb), wpb * 32, kIlsPackSmem, ls>>>(p, d_pk[pol], d_pk[pol] + npk + 1, npk, d_fb_ils,
+                                                                  d_fb_ils + 1);
       SCLS_LAUNCHED();
       sim_ils_lean_kernel<<<grid, wpb * 32, 0, ls>>>(p, d_fb_ils + 1, cnt, d_fb_ils);
     }

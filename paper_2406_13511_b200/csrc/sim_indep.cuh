@@ -153,78 +153,118 @@ __device__ bool merge_completions(int lane, int W, int comp, int completed, doub
 #ifndef SCLS_ILS_INDEP_MINB
 #define SCLS_ILS_INDEP_MINB 4
 #endif
+#ifndef SCLS_PACK_SLOTS
+#define SCLS_PACK_SLOTS 192  // W = 8, MC = 12: two jobs per warp, one wave of 4096 jobs
+#endif
+constexpr int kPackSlots = SCLS_PACK_SLOTS;  // ILS running slots per warp: the pack's traces x W x MC
+// dynamic shared memory of sim_ils_indep_kernel: per warp, the running slots
+// (int4), their arrival times (double) and a boundary's join inputs (int)
+constexpr size_t kIlsPackSmem = (size_t)kSimWarps * kPackSlots * (sizeof(int4) + sizeof(double) + sizeof(int32_t));
+
+// Packs.  A warp takes a pack of up to 32 / W jobs of one config (host:
+// pack_off / jobs); in phase 1 lane gi * W + w simulates instance w of job
+// gi, so with W = 8 all 32 lanes do work instead of 8.  The merges and
+// reports then run job by job over the whole warp.
+struct PackJob {
+  int t, n;
+  const double* arr;
+  char* base;
+  SimLayout Lay;
+  int64_t cap_w;
+};
+
+__device__ __forceinline__ PackJob pack_job(const SimParams& P, int t, int W, int policy, int MC) {
+  PackJob j;
+  j.t = t;
+  const int ts = P.src ? P.src[t] : t;
+  const int64_t r0 = P.req_off[ts];
+  j.n = (int)(P.req_off[ts + 1] - r0);
+  j.arr = P.arr + r0;
+  j.base = P.arena + P.trace_base[t];
+  j.Lay = sim_layout(j.n, W, policy, P.trace_cap[t], MC);
+  j.cap_w = (j.n + W - 1) / W;
+  return j;
+}
+
+// Validates each job of the pack (Simulator::Simulator, sim_engine.cpp:32-35,
+// 102-114) and reports the failed ones; returns the mask of jobs to simulate.
+__device__ unsigned pack_validate(const SimParams& P, const int32_t* jobs, int np, int ci, int W, int lane,
+                                  int32_t* bins) {
+  unsigned ok = 0;
+  for (int q = 0; q < np; ++q) {
+    const int t = jobs[q];
+    const int ts = P.src ? P.src[t] : t;
+    const int64_t r0 = P.req_off[ts];
+    const int n = (int)(P.req_off[ts + 1] - r0);
+    const double* arr = P.arr + r0;
+    int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
+    if (status == SCLS_OK) {
+      int bad = 0;
+      for (int i = 1 + lane; i < n; i += 32) bad |= arr[i] < arr[i - 1];
+      if (__any_sync(FULL, bad)) status = SCLS_ERR_ERROR;
+    }
+    int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
+    if (hist)
+      for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
+    if (status != SCLS_OK)
+      finish_report(lane, &P.res[t], status, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0);
+    else
+      ok |= 1u << q;
+  }
+  return ok;
+}
 
 __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
-    sim_ils_indep_kernel(SimParams P, const int32_t* __restrict__ list, int32_t count, int32_t* __restrict__ fb_count,
-                         int32_t* __restrict__ fb_list) {
+    sim_ils_indep_kernel(SimParams P, const int32_t* __restrict__ pack_off, const int32_t* __restrict__ jobs,
+                         int32_t count, int32_t* __restrict__ fb_count, int32_t* __restrict__ fb_list) {
   __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
   __shared__ double swin_r[kSimWarps][kMergeWin];
   __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
-  __shared__ int4 srun[kSimWarps][2][kIndepRun];   // running slots; [1]: the joins of a boundary
-  __shared__ double sra[kSimWarps][kIndepRun];     // their arrival times
+  extern __shared__ __align__(16) unsigned char ils_dyn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int4* srun = (int4*)ils_dyn + warp * kPackSlots;  // running slots
+  double* sra = (double*)(ils_dyn + (size_t)kSimWarps * kPackSlots * sizeof(int4)) + warp * kPackSlots;
+  int32_t* sjin = (int32_t*)(ils_dyn + (size_t)kSimWarps * kPackSlots * (sizeof(int4) + sizeof(double))) +
+                  warp * kPackSlots;
   const int g = blockIdx.x * (blockDim.x >> 5) + warp;  // launches use 1 or kSimWarps warps per CTA
   if (g >= count) return;
-  const int t = list[g];
-  if (t < 0) return;  // an empty slot (small launches: one job per CTA)
+  const int p0 = pack_off[g], np = pack_off[g + 1] - p0;
+  if (np <= 0) return;  // an empty slot (small launches: one pack per CTA)
+  const int32_t* pj = jobs + p0;
   int32_t* bins = (int32_t*)swin_t[warp];  // p95 bins (after the merge)
-  const int ts = P.src ? P.src[t] : t;
-  const int64_t r0 = P.req_off[ts];
-  const int n = (int)(P.req_off[ts + 1] - r0);
-  const double* __restrict__ arr = P.arr + r0;
-  const int32_t* __restrict__ inp = P.inp + r0;
-  const int32_t* __restrict__ tg = P.tg + r0;
-  const int ci = P.cfg_index ? P.cfg_index[t] : 0;
+  const int ci = P.cfg_index ? P.cfg_index[pj[0]] : 0;  // one config per pack
   const int W = P.cfgs[ci].W, MC = P.cfgs[ci].MC, G = P.cfgs[ci].G;
   const double horizon = P.cfgs[ci].horizon;
   const Lat& lat = P.lat;
-  scls_trace_result* R = &P.res[t];
-  int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
-
-  int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
-  if (status == SCLS_OK) {
-    int bad = 0;
-    for (int i = 1 + lane; i < n; i += 32) bad |= arr[i] < arr[i - 1];
-    if (__any_sync(FULL, bad)) status = SCLS_ERR_ERROR;
-  }
-  if (hist)
-    for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
-  if (status != SCLS_OK) {
-    finish_report(lane, R, status, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0);
+  unsigned okm = pack_validate(P, pj, np, ci, W, lane, bins);
+  if (okm && np * W * MC > kPackSlots) {  // running slots do not fit this warp's shared memory (np == 1)
+    if (lane == 0)
+      for (int q = 0; q < np; ++q)
+        if ((okm >> q) & 1u) fb_list[atomicAdd(fb_count, 1)] = pj[q];
     return;
   }
-  if (W * MC > kIndepRun) {  // running slots do not fit this warp's shared memory
-    if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
-    return;
-  }
-  char* base = P.arena + P.trace_base[t];
-  const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_ILS, P.trace_cap[t], MC);
-  double* resp = (double*)(base + Lay.resp);
-  const int64_t cap_w = (n + W - 1) / W;
 
-#ifdef SCLS_ILS_PROF  // debug build: per-phase clock64 totals into hist[4..7]
-  long long t_a = clock64();
-#endif
-  // ---- phase 1: lane w simulates instance w ------------------------------------------
+  // ---- phase 1: lane gi * W + w simulates instance w of job gi -----------------------
   int comp = 0, batch_count = 0, n_disp = 0, stuck = 0;
   long long batch_members = 0, n_ev = 0;
-#ifdef SCLS_ILS_PROF
-  long long pc_fast = 0, pc_slow = 0, pc_arr = 0, pc_outer = 0, cy_fast = 0, cy_arr = 0, cy_slow = 0;
-  __shared__ unsigned long long s_trips[kSimWarps][2];
-  if (lane == 0) s_trips[warp][0] = s_trips[warp][1] = 0;
-  __syncwarp();
-#endif
   double last_end = 0.0, last_comp = -dinf();
   {
-    const int w = lane;
-    const bool active = lane < W;
+    const int gi = lane / W, w = lane - gi * W;
+    const bool active = gi < np && ((okm >> gi) & 1u);
+    const PackJob J = pack_job(P, active ? pj[gi] : pj[0], W, SCLS_POLICY_ILS, MC);
+    const int n = J.n;
+    const double* __restrict__ arr = J.arr;
+    const int64_t r0 = P.req_off[P.src ? P.src[active ? pj[gi] : pj[0]] : (active ? pj[gi] : pj[0])];
+    const int32_t* __restrict__ inp = P.inp + r0;
+    const int32_t* __restrict__ tg = P.tg + r0;
+    const int64_t cap_w = J.cap_w;
     // running slots {exit iteration, join iteration, input, -} + their
     // arrival times, sorted by exit iteration (see the boundary below)
-    int4* run = srun[warp][0] + w * MC;
-    double* ra = sra[warp] + w * MC;
-    int4* run2 = srun[warp][1] + w * MC;
-    IlsRec rec{(double*)(base + Lay.ct) + w * cap_w, (double*)(base + Lay.cp) + w * cap_w,
-               (double*)(base + Lay.cr) + w * cap_w};
+    int4* run = srun + lane * MC;
+    double* ra = sra + lane * MC;
+    int* jin = sjin + lane * MC;
+    IlsRec rec{(double*)(J.base + J.Lay.ct) + w * cap_w, (double*)(J.base + J.Lay.cp) + w * cap_w,
+               (double*)(J.base + J.Lay.cr) + w * cap_w};
     const int n_mine = active && w < n ? (n - 1 - w) / W + 1 : 0;  // requests w, w + W, ...
     int f_head = 0, f_tail = 0;  // joined / arrived (FIFO as counters)
     int n_run = 0, it_cnt = 0, seg_it = 0, seg_n = 0, room = 0;
@@ -262,18 +302,11 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
           room -= k;
           it_cnt += k;
           seg_it += k;
-#ifdef SCLS_ILS_PROF
-          pc_fast += k;
-          if (lane == __ffs(__activemask()) - 1) ++s_trips[warp][0];
-#endif
         }
       }
       const bool arrive = live && next_arr <= ev_t && next_arr <= horizon;
       const bool slow = live && !arrive && boundary && ev_t < next_arr && ev_t < horizon;
       if (!__any_sync(FULL, arrive || slow)) break;
-#ifdef SCLS_ILS_PROF
-      if (lane == 0) ++s_trips[warp][1];
-#endif
       if (arrive) {
         // on_arrival (sched_policies.cpp:279-290)
         ++f_tail;
@@ -284,9 +317,6 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
         }
         next_arr = next_arr2;
         next_arr2 = f_tail + 1 < n_mine ? arr[w + (f_tail + 1) * W] : dinf();
-#ifdef SCLS_ILS_PROF
-        ++pc_arr;
-#endif
       } else if (slow) {
       // a boundary (sched_policies.cpp:292-391): retire, compact, admit FCFS,
       // and the next step's context / first exit, in one pass over the slots
@@ -324,7 +354,6 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
         }
       }
       const int njoin = min(MC - keep, f_tail - f_head);
-      int* jin = (int*)run2;  // the joins' inputs in join order (prefill order)
       for (int j = 0; j < njoin; ++j) {
         const int lim = min(j_g, G);
         const int ex = it1 + lim;
@@ -385,64 +414,56 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
         t_push = now;
         ev_t = __dadd_rn(now, it);
       }
-#ifdef SCLS_ILS_PROF
-        ++pc_slow;
-#endif
       }
       live = live && (comp < n_mine);
     }
     stuck = comp < n_mine;
   }
-  if (__any_sync(FULL, stuck)) {
-    finish_report(lane, R, SCLS_ERR_NON_TERMINATION, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0,
-                  0.0);
-    return;
-  }
-  const int completed = __reduce_add_sync(FULL, comp);
-  const long long n_events = n + __reduce_add_sync(FULL, (unsigned)n_ev);
-  const int n_disp_all = __reduce_add_sync(FULL, n_disp);
-  const int batch_all = __reduce_add_sync(FULL, batch_count);
-  for (int o = 16; o; o >>= 1) batch_members += __shfl_xor_sync(FULL, batch_members, o);
-  double last_completion = last_comp;
-  for (int o = 16; o; o >>= 1) last_completion = fmax(last_completion, __shfl_xor_sync(FULL, last_completion, o));
 
-#ifdef SCLS_ILS_PROF
-  const long long t_b = clock64();
-#endif
-  // ---- phase 2: the completions in the reference's global order ----------------------
-  const bool tie = merge_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),
-                                     (const double*)(base + Lay.cp), (const double*)(base + Lay.cr), nullptr,
-                                     resp, swin_t[warp], swin_r[warp], swin_q[warp], nullptr);
-  if (tie) {  // the exact lock-step kernel re-runs this job
-    if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
-    return;
+  // ---- phase 2, job by job: the completions in the reference's global order ----------
+  for (int q = 0; q < np; ++q) {
+    if (!((okm >> q) & 1u)) continue;
+    __syncwarp();
+    const bool in = lane < W;
+    const int src = in ? q * W + lane : lane;  // lane w < W takes instance w of job q
+    int c = shfl_i(comp, src), st = shfl_i(stuck, src), nd = shfl_i(n_disp, src), bc = shfl_i(batch_count, src);
+    long long ne = shfl_l(n_ev, src), bm = shfl_l(batch_members, src);
+    double lc = shfl_d(last_comp, src), le = shfl_d(last_end, src);
+    if (!in) {
+      c = st = nd = bc = 0;
+      ne = bm = 0;
+      lc = -dinf();
+      le = 0.0;
+    }
+    const PackJob J = pack_job(P, pj[q], W, SCLS_POLICY_ILS, MC);
+    scls_trace_result* R = &P.res[J.t];
+    int64_t* hist = P.hist ? P.hist + (int64_t)J.t * P.hist_bins : nullptr;
+    if (__any_sync(FULL, st)) {
+      finish_report(lane, R, SCLS_ERR_NON_TERMINATION, J.n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0,
+                    0, 0.0);
+      continue;
+    }
+    const int completed = __reduce_add_sync(FULL, c);
+    const long long n_events = J.n + __reduce_add_sync(FULL, (unsigned)ne);  // per-instance counts fit 32 bits
+    const int n_disp_all = __reduce_add_sync(FULL, nd);
+    const int batch_all = __reduce_add_sync(FULL, bc);
+    for (int o = 16; o; o >>= 1) bm += __shfl_xor_sync(FULL, bm, o);
+    double last_completion = lc;
+    for (int o = 16; o; o >>= 1) last_completion = fmax(last_completion, __shfl_xor_sync(FULL, last_completion, o));
+    double* resp = (double*)(J.base + J.Lay.resp);
+    const bool tie = merge_completions(lane, W, c, completed, last_completion, J.cap_w,
+                                       (const double*)(J.base + J.Lay.ct), (const double*)(J.base + J.Lay.cp),
+                                       (const double*)(J.base + J.Lay.cr), nullptr, resp, swin_t[warp], swin_r[warp],
+                                       swin_q[warp], nullptr);
+    if (tie) {  // the exact lock-step kernel re-runs this job
+      if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = J.t;
+      continue;
+    }
+    __syncwarp();
+    if (hist && P.hist_bins > 1 && lane == 0) hist[1] = completed;
+    finish_report(lane, R, SCLS_OK, J.n, W, completed, J.n > 0 ? J.arr[0] : dinf(), last_completion, resp, bins, le,
+                  0, 0, batch_all, bm, 0, n_events, n_disp_all, 0, last_completion);
   }
-#ifdef SCLS_ILS_PROF
-  const long long t_c = clock64();
-#endif
-  __syncwarp();
-  if (hist && P.hist_bins > 1 && lane == 0) hist[1] = completed;
-  finish_report(lane, R, SCLS_OK, n, W, completed, n > 0 ? arr[0] : dinf(), last_completion, resp, bins, last_end, 0,
-                0, batch_all, batch_members, 0, n_events, n_disp_all, 0, last_completion);
-#ifdef SCLS_ILS_PROF
-  const long long t_d = clock64();
-  if (hist && P.hist_bins >= 8 && lane == 0) {
-    hist[4] = t_b - t_a;
-    hist[5] = t_c - t_b;
-    hist[6] = t_d - t_c;
-    hist[7] = completed;
-  }
-  if (hist && P.hist_bins >= 16 && lane == 0) {
-    hist[8] = pc_fast;
-    hist[9] = pc_slow;
-    hist[10] = pc_arr;
-    hist[11] = pc_outer;
-    hist[12] = cy_fast;
-    hist[13] = cy_arr;
-    hist[14] = cy_slow;
-    hist[15] = (long long)(s_trips[warp][0] << 32 | s_trips[warp][1]);
-  }
-#endif
 }
 
 
