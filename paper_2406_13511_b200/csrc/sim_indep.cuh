@@ -120,6 +120,25 @@ __device__ bool merge_completions(int lane, int W, int comp, int completed, doub
     }
     const int wl = __ffs(win) - 1;
     bool refill = false;
+    if (!runs) {  // ILS: one record per step, i advances by one on every lane
+      if (lane == wl) {
+        resp[i] = wr[lane * ws + h];
+        ++k;
+        ++h;
+        if (k == mine) {
+          kt = ~0ull;
+          kq = 0xffffffffu;
+        } else if (h == ws) {
+          refill = true;
+        } else {
+          kt = wt[lane * ws + h];
+          kq = wq[lane * ws + h];
+        }
+      }
+      ++i;
+      need = __ballot_sync(FULL, refill);
+      continue;
+    }
     int emitted = 0;
     if (lane == wl) {
       // a run: the rest of this batch (at most 255 per step), same event
