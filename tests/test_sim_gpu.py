@@ -434,3 +434,46 @@ def test_worker_count_limit(ctx, orc):
     trace = orc.generate(capi.workload_spec(rate=5.0, duration_s=5.0))
     with pytest.raises(Exception, match="1024"):
         ctx.simulate([trace], capi.sched_cfg(worker_count=1025), lat, MEMORIES["rule"]())
+
+
+@pytest.mark.parametrize("pol", ["ils", "sls"])
+def test_packed_jobs_mixed_outcomes(ctx, orc, pol):
+    """Several jobs of one config share a warp (ILS packs: up to 32 / W jobs):
+    normal jobs, jobs with exact cross-instance ties (handed to the lock-step
+    kernel from inside a pack), jobs that fail validation (unsorted arrivals)
+    and NonTermination horizons, all in the same packs, against the oracle."""
+    lat = capi.builtin_latency_model()
+    rng = np.random.default_rng(5)
+    traces = []
+    for i in range(40):
+        kind = i % 8
+        if kind == 5:  # identical instances: exact time ties
+            k, w = 5, 4
+            traces.append((np.repeat(np.arange(1, k + 1, dtype=np.float64), w),
+                           np.repeat(np.arange(100, 100 + 10 * k, 10, dtype=np.int32), w),
+                           np.repeat(np.arange(5, 5 + 3 * k, 3, dtype=np.int32), w)))
+        elif kind == 6:  # unsorted arrivals: Error from the simulator's constructor checks
+            tr = orc.generate(capi.workload_spec(rate=10.0, duration_s=20.0, seed=700 + i))
+            arr = np.asarray(tr[0]).copy()
+            arr[[3, 4]] = arr[[4, 3]] if arr[3] != arr[4] else (arr[3] + 1.0, arr[4])
+            traces.append((arr, tr[1], tr[2]))
+        else:
+            traces.append(orc.generate(capi.workload_spec(rate=float(rng.uniform(5, 30)),
+                                                          duration_s=float(rng.uniform(20, 90)), seed=700 + i)))
+    cfgs = [capi.sched_cfg(policy=pol, worker_count=4, max_concurrent=3, fixed_batch_size=3),
+            capi.sched_cfg(policy=pol, worker_count=4, max_concurrent=3, fixed_batch_size=3, horizon_s=15.0)]
+    ctx.set_digests(False)
+    try:
+        a, ha = ctx.simulate_grid(traces, cfgs, lat, MEMORIES["rule"](), hist_bins=16)
+    finally:
+        ctx.set_digests(True)
+    statuses = set()
+    for c, cfg in enumerate(cfgs):
+        b, hb = orc.simulate(traces, cfg, lat, MEMORIES["rule"](), hist_bins=16)
+        for t in range(len(traces)):
+            statuses.add(b[t].status)
+            for f in FIELDS:
+                if not f.startswith("h_"):
+                    assert getattr(a[c][t], f) == getattr(b[t], f), (c, t, f, getattr(a[c][t], f), getattr(b[t], f))
+        assert np.array_equal(ha[c], hb), c
+    assert len(statuses) >= 3, statuses  # ok, error and non-termination all occurred
