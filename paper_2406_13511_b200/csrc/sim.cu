@@ -43,6 +43,22 @@ constexpr int kSimWarps = 4;  // traces per CTA
 #define SCLS_SIM_MINB 7
 #endif
 constexpr int kSplitSmem = SCLS_SPLIT_SMEM;
+#ifndef SCLS_FAR_U
+#define SCLS_FAR_U 4
+#endif
+#ifndef SCLS_KEYS_U
+#define SCLS_KEYS_U 2
+#endif
+constexpr int kFarU = SCLS_FAR_U;    // tick DP: far sources per trip (loads first)
+constexpr int kKeysU = SCLS_KEYS_U;  // tick keys: pool rows per lane per trip
+#ifndef SCLS_HIST_U
+#define SCLS_HIST_U 2
+#endif
+constexpr int kHistU = SCLS_HIST_U;  // radix histogram: keys per lane per trip
+#ifndef SCLS_ROWS_U
+#define SCLS_ROWS_U 2
+#endif
+constexpr int kRowsU = SCLS_ROWS_U;  // tick rows: sorted rows per lane per trip
 
 struct SimCfg {
   int32_t policy, S, G, B, MC, W;
@@ -223,12 +239,12 @@ __device__ bool warp_radix_sort(int n, uint64_t* k, int32_t* v, uint64_t* k2, in
     const uint32_t mask = bits - shift >= 8 ? 0xffu : ((1u << (bits - shift)) - 1u);
     for (int i = lane; i < 256; i += 32) bins[i] = 0;
     __syncwarp();
-    for (int base = 0; base < n; base += 128) {  // four keys per lane per trip, loads first
-      uint64_t kk[4];
+    for (int base = 0; base < n; base += 32 * kHistU) {  // kHistU keys per lane per trip, loads first
+      uint64_t kk[kHistU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) kk[u] = base + 32 * u + lane < n ? k[base + 32 * u + lane] : 0ull;
+      for (int u = 0; u < kHistU; ++u) kk[u] = base + 32 * u + lane < n ? k[base + 32 * u + lane] : 0ull;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kHistU; ++u)
         if (base + 32 * u + lane < n) atomicAdd(&bins[(kk[u] >> shift) & mask], 1);
     }
     __syncwarp();
@@ -574,18 +590,18 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       // four rows per lane per trip, every load issued before any use: the
       // pool and request arrays are L2 / DRAM resident, so memory-level
       // parallelism, not issue, bounds this loop
-      for (int i0 = lane; i0 < P_; i0 += 128) {
-        int id[4];
+      for (int i0 = lane; i0 < P_; i0 += 32 * kKeysU) {
+        int id[kKeysU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) id[u] = i0 + 32 * u < P_ ? pool[i0 + 32 * u] : 0;
-        int ip[4], gn[4];
+        for (int u = 0; u < kKeysU; ++u) id[u] = i0 + 32 * u < P_ ? pool[i0 + 32 * u] : 0;
+        int ip[kKeysU], gn[kKeysU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kKeysU; ++u) {
           ip[u] = i0 + 32 * u < P_ ? inp[id[u]] : 0;
           gn[u] = i0 + 32 * u < P_ ? gen[id[u]] : 0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kKeysU; ++u) {
           if (i0 + 32 * u < P_) {
             const uint32_t e = (uint32_t)(ip[u] + gn[u]);
             emax = max(emax, e);
@@ -602,14 +618,14 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       const uint64_t idmask = (1ull << idb) - 1ull;
       // 2. rows: L, singleton feasibility (batcher.cpp:40-46)
       int bad = 0x7fffffff;
-      for (int i0 = lane; i0 < P_; i0 += 64) {  // two rows per lane per trip, loads first
-        uint64_t key[2];
+      for (int i0 = lane; i0 < P_; i0 += 32 * kRowsU) {  // kRowsU rows per lane per trip, loads first
+        uint64_t key[kRowsU];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) key[u] = i0 + 32 * u < P_ ? keys[i0 + 32 * u] : 0ull;
-        int id[2], L[2], g_[2], t_[2], s_[2], k_[2];
-        double a_[2];
+        for (int u = 0; u < kRowsU; ++u) key[u] = i0 + 32 * u < P_ ? keys[i0 + 32 * u] : 0ull;
+        int id[kRowsU], L[kRowsU], g_[kRowsU], t_[kRowsU], s_[kRowsU], k_[kRowsU];
+        double a_[kRowsU];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kRowsU; ++u) {
           const bool ok = i0 + 32 * u < P_;
           id[u] = (int)(key[u] & idmask);
           L[u] = (int)(key[u] >> idb);
@@ -620,7 +636,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           k_[u] = ok && L[u] <= P.Lmax ? Kt[L[u]] : 0;
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kRowsU; ++u) {
           const int i = i0 + 32 * u;
           if (i < P_) {
             const int64_t q = tl_pos + i;
@@ -666,16 +682,16 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         const int wmax = __reduce_max_sync(FULL, Wr);
         // candidates with j <= tb, ascending j (k descending)
         int j = max(0, tb + 1 - wmax);
-        for (; j + 3 <= tb; j += 4) {
-          double tv[4], cv[4];
+        for (; j + kFarU - 1 <= tb; j += kFarU) {
+          double tv[kFarU], cv[kFarU];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kFarU; ++u) {
             const int k = r - (j + u);
             tv[u] = T[j + u];
             cv[u] = k <= Wr ? __ldg(crow + k) : 0.0;
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kFarU; ++u) {
             const int k = r - (j + u);
             if (k <= Wr) {
               const double cand = __dadd_rn(tv[u], cv[u]);
