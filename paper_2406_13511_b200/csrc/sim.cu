@@ -59,6 +59,10 @@ constexpr int kHistU = SCLS_HIST_U;  // radix histogram: keys per lane per trip
 #define SCLS_ROWS_U 2
 #endif
 constexpr int kRowsU = SCLS_ROWS_U;  // tick rows: sorted rows per lane per trip
+#ifndef SCLS_PUSH_U
+#define SCLS_PUSH_U 4
+#endif
+constexpr int kPushU = SCLS_PUSH_U;  // tick DP decision rounds: final sources pushed per trip
 
 struct SimCfg {
   int32_t policy, S, G, B, MC, W;
@@ -736,17 +740,17 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
             if (!um) break;
             const int a2 = tb + first;  // new frontier: rows a+1 .. a2 are final
             // push sources j in (a, a2], ascending j (descending k, ties to the smaller k)
-            for (int j = a + 1; j <= a2; j += 4) {
-              double tv[4], cv[4];
+            for (int j = a + 1; j <= a2; j += kPushU) {
+              double tv[kPushU], cv[kPushU];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
+              for (int u = 0; u < kPushU; ++u) {
                 const int jj = min(j + u, a2);
                 tv[u] = shfl_d(acc, jj - tb - 1);
                 const int k = r - (j + u);
                 cv[u] = pend && j + u <= a2 && k >= 1 && k <= Wr ? __ldg(crow + k) : 0.0;
               }
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
+              for (int u = 0; u < kPushU; ++u) {
                 const int k = r - (j + u);
                 if (pend && j + u <= a2 && k >= 1 && k <= Wr) {
                   const double cand = __dadd_rn(tv[u], cv[u]);
