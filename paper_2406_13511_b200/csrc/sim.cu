@@ -59,6 +59,10 @@ constexpr int kHistU = SCLS_HIST_U;  // radix histogram: keys per lane per trip
 #define SCLS_ROWS_U 2
 #endif
 constexpr int kRowsU = SCLS_ROWS_U;  // tick rows: sorted rows per lane per trip
+#ifndef SCLS_EMIT_U
+#define SCLS_EMIT_U 1
+#endif
+constexpr int kEmitU = SCLS_EMIT_U;  // tick emit: served l_out scan unroll
 #ifndef SCLS_PUSH_U
 #define SCLS_PUSH_U 4
 #endif
@@ -816,6 +820,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           b_est[bi] = cost[coff[L] - 1 + (end - beg)];
           // slice_served_l_out (sched_policies.cpp:72-80): max over members
           int served = 0;
+#pragma unroll kEmitU
           for (int q = tl_pos + beg; q < tl_pos + end; ++q) served = max(served, min(tl_t[q] - tl_g[q], C.S));
           b_served[bi] = served;
         }
