@@ -1821,6 +1821,7 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
       const SimCfg& c = hc[ci];
       int G = std::max(1, 32 / std::max(c.W, 1));
       if (ils) G = std::max(1, std::min(G, kPackSlots / std::max(1, c.W * std::max(c.MC, 1))));
+      if (ils) G = std::min(G, kIlsPackMax);
       open[ci].push_back(t);
       if ((int)open[ci].size() == G) {
         packs.push_back(std::move(open[ci]));

@@ -176,6 +176,10 @@ __device__ bool merge_completions(int lane, int W, int comp, int completed, doub
 #define SCLS_PACK_SLOTS 192  // W = 8, MC = 12: two jobs per warp, one wave of 4096 jobs
 #endif
 constexpr int kPackSlots = SCLS_PACK_SLOTS;  // ILS running slots per warp: the pack's traces x W x MC
+#ifndef SCLS_ILS_PACK_MAX
+#define SCLS_ILS_PACK_MAX 2
+#endif
+constexpr int kIlsPackMax = SCLS_ILS_PACK_MAX;  // jobs per pack (their merges run in series)
 // dynamic shared memory of sim_ils_indep_kernel: per warp, the running slots
 // (int4), their arrival times (double) and a boundary's join inputs (int)
 constexpr size_t kIlsPackSmem = (size_t)kSimWarps * kPackSlots * (sizeof(int4) + sizeof(double) + sizeof(int32_t));
@@ -656,10 +660,16 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
   }
   double last_completion = last_comp;
   for (int o = 16; o; o >>= 1) last_completion = fmax(last_completion, __shfl_xor_sync(FULL, last_completion, o));
-  const bool tie = merge_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),
-                                     (const double*)(base + Lay.cp), (const double*)(base + Lay.cr),
-                                     (const int32_t*)(base + Lay.cn), resp, swin_t[warp], swin_r[warp],
-                                     swin_q[warp], swin_n[warp]);
+  bool tie = false;
+  if (W == 1) {  // one list: already in completion order
+    const double* cr = (const double*)(base + Lay.cr);
+    for (int i = lane; i < completed; i += 32) resp[i] = cr[i];
+  } else {
+    tie = merge_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),
+                            (const double*)(base + Lay.cp), (const double*)(base + Lay.cr),
+                            (const int32_t*)(base + Lay.cn), resp, swin_t[warp], swin_r[warp], swin_q[warp],
+                            swin_n[warp]);
+  }
   if (tie) {  // the exact lock-step kernel re-runs this job
     if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
     return;
