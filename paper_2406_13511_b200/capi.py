@@ -44,6 +44,7 @@ ERR_INFEASIBLE_REQUEST = 5
 ERR_NO_WORKERS = 6
 ERR_EMPTY_LOG = 9
 ERR_NON_TERMINATION = 10
+ERR_INVALID_ARGUMENT = 11
 ERR_CUDA = 12
 ERR_CAPACITY = 13
 

@@ -106,6 +106,24 @@ struct SimParams {
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000ll); }
 
+// Per-trace input checks, run before any arena write: arrivals in order
+// (sim_engine.cpp:102-114 -> Error) and lengths >= 1.  generate() clamps both
+// lengths to [1, limit] (workload.cpp:120-128); a hand-built Request with a
+// length < 1 would drive the reference's counters negative, which no device
+// policy models (the SCLS sort key packs eff >= 1, the arena is sized by
+// ceil(gen / S) slices), so such a trace is refused as INVALID_ARGUMENT.
+__device__ __forceinline__ int trace_input_status(const double* arr, const int32_t* inp, const int32_t* tg, int n,
+                                                  int lane) {
+  int order = 0, len = 0;
+  for (int i = lane; i < n; i += 32) {
+    if (i > 0) order |= arr[i] < arr[i - 1];
+    len |= inp[i] < 1 || tg[i] < 1;
+  }
+  if (__any_sync(0xffffffffu, order)) return SCLS_ERR_ERROR;
+  if (__any_sync(0xffffffffu, len)) return SCLS_ERR_INVALID_ARGUMENT;
+  return SCLS_OK;
+}
+
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(FULL, v, src); }
 __device__ __forceinline__ int shfl_i(int v, int src) { return __shfl_sync(FULL, v, src); }
 __device__ __forceinline__ long long shfl_l(long long v, int src) { return __shfl_sync(FULL, v, src); }
@@ -402,11 +420,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   // Constructor validation (host-checked per config) and the arrival-order
   // rule (sim_engine.cpp:102-114).
   int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
-  if (status == SCLS_OK) {
-    int bad = 0;
-    for (int i = 1 + lane; i < n; i += 32) bad |= arr[i] < arr[i - 1];
-    if (__any_sync(FULL, bad)) status = SCLS_ERR_ERROR;
-  }
+  if (status == SCLS_OK) status = trace_input_status(arr, inp, tg, n, lane);
   if (hist)
     for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
   if (status != SCLS_OK) {
@@ -1488,7 +1502,7 @@ __global__ void slice_caps_kernel(int32_t n_traces, const int64_t* __restrict__ 
   if (c.policy == SCLS_POLICY_SCLS && c.S > 0)
     for (int64_t i = req_off[src ? src[warp] : warp] + lane; i < req_off[(src ? src[warp] : warp) + 1]; i += 32) {
       const int g = min(tg[i], c.G);
-      s += (g + c.S - 1) / c.S;
+      s += g >= 1 ? (g + c.S - 1) / c.S : 1;  // lengths < 1 are refused by the kernel; keep the arena sane
     }
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
   if (lane == 0) caps[warp] = s;
@@ -1808,8 +1822,9 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
     SCLS_CUDA(cudaMemcpyAsync(d_lists, flat.data(), sizeof(int32_t) * n_slots, cudaMemcpyHostToDevice, s));
   }
   const bool hash = ctx->sim_digests;
-  // Packs for the independent-lane kernels (sim_indep.cuh): up to 32 / W jobs
-  // of one config per warp (ILS: within kPackSlots running slots), packs in
+  // Packs for the independent-lane ILS kernel (sim_indep.cuh): up to
+  // min(kIlsPackMax = 2, 32 / W, kPackSlots / (W * MC)) jobs of one config
+  // per warp, packs in
   // LPT order of their longest job; one pack per CTA for small launches.
   auto make_packs = [&](const std::vector<int32_t>& l, bool ils, std::vector<int32_t>& off,
                         std::vector<int32_t>& flat) {

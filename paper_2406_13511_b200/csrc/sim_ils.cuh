@@ -263,11 +263,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_MINB)
   int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
 
   int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
-  if (status == SCLS_OK) {
-    int bad = 0;
-    for (int i = 1 + lane; i < n; i += 32) bad |= arr[i] < arr[i - 1];
-    if (__any_sync(FULL, bad)) status = SCLS_ERR_ERROR;
-  }
+  if (status == SCLS_OK) status = trace_input_status(arr, inp, tg, n, lane);
   if (hist)
     for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
   if (status != SCLS_OK) {

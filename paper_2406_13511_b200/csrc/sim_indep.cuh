@@ -62,6 +62,7 @@ __device__ bool merge_completions(int lane, int W, int comp, int completed, doub
                                   const double* __restrict__ ct, const double* __restrict__ cp,
                                   const double* __restrict__ cr, const int32_t* __restrict__ cn,
                                   double* __restrict__ resp, uint64_t* wt, double* wr, uint32_t* wq, uint8_t* wn) {
+  __syncwarp();  // every lane's completion records (written in the simulation phase) are visible
   const bool runs = cn != nullptr;
   const int ws = kMergeWin / W;
   const int mine = lane < W ? comp : 0;
@@ -184,8 +185,8 @@ constexpr int kIlsPackMax = SCLS_ILS_PACK_MAX;  // jobs per pack (their merges r
 // (int4), their arrival times (double) and a boundary's join inputs (int)
 constexpr size_t kIlsPackSmem = (size_t)kSimWarps * kPackSlots * (sizeof(int4) + sizeof(double) + sizeof(int32_t));
 
-// Packs.  A warp takes a pack of up to 32 / W jobs of one config (host:
-// pack_off / jobs); in phase 1 lane gi * W + w simulates instance w of job
+// Packs.  A warp takes a pack of up to min(kIlsPackMax = 2, 32 / W,
+// kPackSlots / (W * MC)) jobs of one config (host: pack_off / jobs); in phase 1 lane gi * W + w simulates instance w of job
 // gi, so with W = 8 all 32 lanes do work instead of 8.  The merges and
 // reports then run job by job over the whole warp.
 struct PackJob {
@@ -221,11 +222,7 @@ __device__ unsigned pack_validate(const SimParams& P, const int32_t* jobs, int n
     const int n = (int)(P.req_off[ts + 1] - r0);
     const double* arr = P.arr + r0;
     int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
-    if (status == SCLS_OK) {
-      int bad = 0;
-      for (int i = 1 + lane; i < n; i += 32) bad |= arr[i] < arr[i - 1];
-      if (__any_sync(FULL, bad)) status = SCLS_ERR_ERROR;
-    }
+    if (status == SCLS_OK) status = trace_input_status(arr, P.inp + r0, P.tg + r0, n, lane);
     int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
     if (hist)
       for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
@@ -530,11 +527,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
   int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
 
   int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
-  if (status == SCLS_OK) {
-    int bad = 0;
-    for (int i = 1 + lane; i < n; i += 32) bad |= arr[i] < arr[i - 1];
-    if (__any_sync(FULL, bad)) status = SCLS_ERR_ERROR;
-  }
+  if (status == SCLS_OK) status = trace_input_status(arr, inp, tg, n, lane);
   if (hist)
     for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
   if (status != SCLS_OK) {
@@ -663,6 +656,7 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
   bool tie = false;
   if (W == 1) {  // one list: already in completion order
     const double* cr = (const double*)(base + Lay.cr);
+    __syncwarp();  // lane 0 wrote cr[] in the simulation phase
     for (int i = lane; i < completed; i += 32) resp[i] = cr[i];
   } else {
     tie = merge_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),

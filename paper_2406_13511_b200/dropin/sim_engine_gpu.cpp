@@ -41,6 +41,58 @@ void Simulator::schedule_tick(double) { host_hook(); }
 void Simulator::schedule_policy_event(double, WorkerId) { host_hook(); }
 void Simulator::complete_request(RequestId, WorkerId) { host_hook(); }
 
+namespace {
+// The post-run Simulator state the reference leaves behind (clock(),
+// request(id), workers()), rebuilt from the device event log in log order:
+//   - request progress: first dispatch (sched_policies.cpp:128,225,373),
+//     generated / slices (:174-175 SCLS, :266-267 SLS, :304,372 ILS) and
+//     completion time (sim_engine.cpp:86-99);
+//   - worker load_estimate (SCLS): offload's += est in dispatch order
+//     (offloader.cpp:50, written back at sched_policies.cpp:111) and
+//     complete_batch's clamped -= est at each batch end (offloader.cpp:56-59);
+//   - busy_until: the end of the worker's last served batch (sim_engine.cpp:80;
+//     ILS never enqueues batches, so it stays 0).
+void replay(const EventLog& log, int policy, int max_gen, std::vector<Request>& reqs,
+            std::vector<WorkerSim>& workers) {
+  std::vector<double> disp_t, est;  // per batch id (SCLS / SLS)
+  auto slot = [](std::vector<double>& v, int64_t b) -> double& {
+    if (b >= (int64_t)v.size()) v.resize((size_t)b + 1, 0.0);
+    return v[(size_t)b];
+  };
+  for (const EventRecord& e : log.events) {
+    if (e.kind == EventKind::kDispatch) {
+      if (policy == SCLS_POLICY_ILS) {
+        Request& r = reqs[(size_t)e.request];
+        r.slices_served = 1;
+        if (!r.first_dispatch_time) r.first_dispatch_time = e.t;
+        continue;
+      }
+      slot(disp_t, e.batch) = e.t;
+      slot(est, e.batch) = e.est_serve_s;
+      if (policy == SCLS_POLICY_SCLS) workers[(size_t)e.worker].load_estimate += e.est_serve_s;
+    } else if (e.kind == EventKind::kBatchEnd) {
+      if (policy == SCLS_POLICY_ILS) continue;
+      WorkerSim& w = workers[(size_t)e.worker];
+      w.busy_until = e.t;
+      for (const MemberAccounting& m : e.members) {
+        Request& r = reqs[(size_t)m.request];
+        if (!r.first_dispatch_time) r.first_dispatch_time = slot(disp_t, e.batch);
+        r.generated_so_far += m.gen;
+        r.slices_served += 1;
+      }
+      if (policy == SCLS_POLICY_SCLS) {
+        w.load_estimate -= slot(est, e.batch);
+        if (w.load_estimate < 0.0) w.load_estimate = 0.0;
+      }
+    } else if (e.kind == EventKind::kComplete) {
+      Request& r = reqs[(size_t)e.request];
+      r.completion_time = e.t;
+      if (policy == SCLS_POLICY_ILS) r.generated_so_far = std::min(r.true_gen_len, max_gen);
+    }
+  }
+}
+}  // namespace
+
 EventLog Simulator::run(std::vector<Request> workload, Scheduler& policy) {
   std::stable_sort(workload.begin(), workload.end(), [](const Request& a, const Request& b) {
     if (a.arrival_time != b.arrival_time) return a.arrival_time < b.arrival_time;
@@ -87,8 +139,13 @@ EventLog Simulator::run(std::vector<Request> workload, Scheduler& policy) {
         throw InfeasibleRequestError(res.error_request_id,
                                      "request " + std::to_string(res.error_request_id) +
                                          " does not fit memory even as a singleton batch");
-      if (res.status == SCLS_ERR_NON_TERMINATION)
-        throw NonTerminationError("simulated clock reached horizon " + std::to_string(horizon_s_) + " s");
+      if (res.status == SCLS_ERR_NON_TERMINATION) {
+        // sim_engine.cpp:159-163; the device log holds every record up to EndOfRun
+        int64_t done = 0;
+        for (int64_t k = 0; k < std::min(rc, rec_cap); ++k) done += recs[k].kind == 5;
+        throw NonTerminationError("simulated clock reached horizon " + std::to_string(horizon_s_) + " s with " +
+                                  std::to_string(done) + " of " + std::to_string(n) + " requests completed");
+      }
       throw Error("device simulation failed with status " + std::to_string(res.status));
     }
     log_.events.clear();
@@ -117,6 +174,8 @@ EventLog Simulator::run(std::vector<Request> workload, Scheduler& policy) {
       }
       log_.add(std::move(e));
     }
+    replay(log_, c.policy, cfg_.max_gen_limit, requests_, workers_);
+    clock_ = res.sim_clock;
     return std::move(log_);
   }
   throw Error("device event log capacity could not be established");

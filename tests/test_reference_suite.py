@@ -55,3 +55,28 @@ def test_reference_suite_on_b200(name):
     assert "0 failed" in out
     if name == "acceptance_test":
         assert out.count("PASS") == 11, out
+
+
+def _post_run_state(kind):
+    path = os.path.join(BIN, "post_run_state_" + kind)
+    _require(path)
+    p = subprocess.run([path], capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-2000:]
+    return p.stdout
+
+
+def test_post_run_state_reference_harness():
+    out = _post_run_state("ref")
+    assert out.count("horizon: simulated clock reached horizon") == 9, out[-2000:]
+
+
+@pytest.mark.gpu
+def test_post_run_state_b200_matches_reference():
+    """clock(), request(id) progress, workers() loads / busy_until and the
+    NonTermination message after Simulator::run, drop-in vs reference
+    (sim_engine.h:64-79, sim_engine.cpp:159-163)."""
+    want = _post_run_state("ref").splitlines()
+    got = _post_run_state("b200").splitlines()
+    assert len(got) == len(want)
+    for a, b in zip(got, want):
+        assert a == b, (a, b)

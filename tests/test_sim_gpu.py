@@ -145,6 +145,18 @@ def test_error_statuses(ctx, orc):
     bad = (np.array([1.0, 0.5]), np.array([10, 10], np.int32), np.array([10, 10], np.int32))
     a, _ = ctx.simulate([bad], capi.sched_cfg(), lat, MEMORIES["rule"]())
     assert a[0].status == 1
+    # a length < 1 -> INVALID_ARGUMENT for that trace only, every policy and
+    # kernel (lock-step, independent-lane), other traces unaffected
+    for g0, i0 in ((0, 10), (-3, 10), (10, 0)):
+        zero = (np.array([0.0, 0.5, 1.0]), np.array([10, i0, 10], np.int32), np.array([10, g0, 10], np.int32))
+        for pol in ("scls", "sls", "ils"):
+            for digests in (True, False):
+                ctx.set_digests(digests)
+                a, _ = ctx.simulate([trace, zero, zero, trace], capi.sched_cfg(policy=pol), lat, MEMORIES["rule"]())
+                ctx.set_digests(True)
+                assert [r.status for r in a] == [0, capi.ERR_INVALID_ARGUMENT, capi.ERR_INVALID_ARGUMENT, 0], pol
+                b, _ = orc.simulate([trace], capi.sched_cfg(policy=pol), lat, MEMORIES["rule"]())
+                assert_results_equal(a[3], b[0], pol)
     # invalid config -> Error, other traces unaffected
     a, _ = ctx.simulate([trace, trace], [capi.sched_cfg(), capi.sched_cfg(lambda_=2.0)], lat,
                         MEMORIES["rule"](), cfg_index=[0, 1])
