@@ -1,7 +1,8 @@
 /* scls_capi.h — C-ABI boundary of the B200-native SCLS scheduling core.
  *
  * Plain C types only (no torch, no C++), so any FFI (ctypes, cgo, JNI) or the
- * C++ drop-in layer (include/slicesim_b200/*.hpp) can bind it.  Every entry point
+ * C++ drop-in layer (paper_2406_13511_b200/dropin/, which re-creates the
+ * reference's own headers on top of it) can bind it.  Every entry point
  * replaces one public function of the reference library `slicesim`
  * (/root/reference/proj/core/include/slicesim/*.h); the replaced interface is
  * cited on each declaration as reference file:line.
@@ -348,6 +349,63 @@ scls_status scls_run_experiments(scls_ctx* ctx, int32_t n_runs, const scls_workl
 scls_status scls_generate_batch(scls_ctx* ctx, int32_t n_specs, const scls_workload_spec* specs,
                                 int64_t cap, int64_t* req_offset, double* arrival,
                                 int32_t* input_len, int32_t* gen_len, int32_t mem);
+
+/* ---- multi-GPU sweep: SURVEY §8(e), the reference's sequential sweep loop
+ * (experiment.cpp:62-85) sharded over devices ---------------------------------
+ * The trace dimension is the only one that shards: trace t belongs to shard
+ * floor(t * N / n_traces) (contiguous ranges, scls_shard_range).  Each shard is
+ * generated and simulated on its own device exactly as scls_run_sweep, and
+ * the fixed-size per-job result records (+ histograms) are then all-gathered
+ * with one ncclAllGather over NVLink -- the only collective -- so every device
+ * ends with the full grid in the scls_run_sweep job order (j = c * n_traces + t).
+ *
+ * Two launch shapes:
+ *  - one process per GPU (torchrun): every rank creates its context, joins a
+ *    communicator with scls_comm_init (the 128-byte id comes from
+ *    scls_comm_unique_id on rank 0, broadcast by the caller), then calls
+ *    scls_run_sweep_sharded with the GLOBAL spec list;
+ *  - one process, many GPUs: scls_multi_create binds N devices (one context
+ *    and one host thread each, one NCCL clique via ncclCommInitAll) and
+ *    scls_multi_run_sweep runs the sharded sweep across them.  A device may
+ *    appear more than once (shards sharing a GPU); the gather then uses peer
+ *    copies instead of NCCL, which cannot put two ranks on one device.
+ * NCCL is loaded at run time (libnccl.so.2); without it these calls fail with
+ * SCLS_ERR_CUDA, except a 1-shard run, which needs no collective. */
+void scls_shard_range(int64_t total, int32_t shard, int32_t n_shards, int64_t* lo, int64_t* hi);
+scls_status scls_comm_unique_id(uint8_t out[128]);
+scls_status scls_comm_init(scls_ctx* ctx, int32_t world, int32_t rank, const uint8_t id[128]);
+/* Ranks of the context's communicator as NCCL reports them (1 without one). */
+int32_t scls_comm_size(const scls_ctx* ctx);
+/* results / slice_hist: n_cfgs * n_traces entries (the whole grid) in `mem`
+ * (device memory = this rank's device).  Timings: [6] = this rank's shard
+ * (generate + simulate), [5] = the gather + reorder, [0] = total. */
+scls_status scls_run_sweep_sharded(scls_ctx* ctx, int32_t n_traces, const scls_workload_spec* specs,
+                                   int32_t n_cfgs, const scls_sched_cfg* cfgs, const scls_latency* lat,
+                                   const scls_memory* memm, scls_trace_result* results, int32_t hist_bins,
+                                   int64_t* slice_hist, int32_t mem);
+
+/* Number of visible CUDA devices (0 without a usable driver). */
+int32_t scls_device_count(void);
+
+typedef struct scls_multi scls_multi;
+scls_status scls_multi_create(int32_t n_dev, const int32_t* devices, scls_multi** out);
+void scls_multi_destroy(scls_multi* m);
+size_t scls_multi_last_error(const scls_multi* m, char* buf, size_t cap);
+/* 1 when the gather runs over NCCL (distinct devices), 0 for peer copies. */
+int32_t scls_multi_uses_nccl(const scls_multi* m);
+/* results / slice_hist in host memory.  out_ms (optional, n_dev + 2 floats):
+ * per-device shard time (device events), then the gather and the wall time. */
+scls_status scls_multi_run_sweep(scls_multi* m, int32_t n_traces, const scls_workload_spec* specs, int32_t n_cfgs,
+                                 const scls_sched_cfg* cfgs, const scls_latency* lat, const scls_memory* memm,
+                                 scls_trace_result* results, int32_t hist_bins, int64_t* slice_hist,
+                                 float* out_ms);
+
+/* scls_run_experiments across the devices: run i (specs[i] under cfgs[i])
+ * belongs to shard floor(i * N / n_runs); results / slice_hist by run, host memory. */
+scls_status scls_multi_run_experiments(scls_multi* m, int32_t n_runs, const scls_workload_spec* specs,
+                                       const scls_sched_cfg* cfgs, const scls_latency* lat, const scls_memory* memm,
+                                       scls_trace_result* results, int32_t hist_bins, int64_t* slice_hist,
+                                       float* out_ms);
 
 /* Diagnostics: the device port of glibc's log (csrc/glibc_log.cuh) on n
  * inputs, for the bit-exactness check against the host libm. */

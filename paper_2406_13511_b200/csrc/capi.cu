@@ -185,6 +185,7 @@ void scls_ctx_destroy(scls_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  scls::comm_release(ctx);
   for (auto& b : ctx->bufs)
     if (b.p) cudaFree(b.p);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);

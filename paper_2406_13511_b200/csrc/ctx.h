@@ -29,6 +29,8 @@ struct scls_ctx {
   bool sim_concurrent = true;             // scls_simulate runs its per-policy launches concurrently
   bool ils_lockstep = false;              // metrics-only ILS: the lock-step kernel instead of independent lanes
   cudaStream_t side[3] = {};              // forked streams for those launches (created on first use)
+  void* comm = nullptr;                   // ncclComm_t of scls_comm_init (multi.cu)
+  int world = 1, rank = 0;
 
   // Named grow-only device buffers (scratch reused across calls).
   struct Buf {
@@ -55,7 +57,8 @@ enum ScratchSlot : int {
   kSlotStage = 60,    // 60..79: host<->device staging of entry-point arguments
   kSlotSim = 80,      // 80..109: simulator
   kSlotGen = 110,     // 110..119: device trace generation
-  kNumSlots = 120,
+  kSlotMulti = 120,   // 120..123: sharded sweep (local grid, gather buffers)
+  kNumSlots = 124,
 };
 
 // Status plumbing shared by the C-ABI entry points.
@@ -74,6 +77,8 @@ scls_status cuda_error(scls_ctx* ctx, cudaError_t e, const char* where);
     cudaError_t _e = cudaPeekAtLastError();                                     \
     if (_e != cudaSuccess) return ::scls::cuda_error(ctx, _e, "kernel launch"); \
   } while (0)
+
+void comm_release(scls_ctx* ctx);  // multi.cu
 
 inline int div_up(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 

@@ -26,6 +26,11 @@ namespace b200 {
 // the drop-in has no CPU fallback.
 scls_ctx* context();
 
+// All visible GPUs for device-generated sweeps (scls_multi: contiguous run
+// shards, NCCL gather); nullptr with a single GPU.  SCLS_DEVICES=k caps it
+// at devices 0..k-1; a list ("0,1", or "0,0" to shard on one GPU) names them.
+scls_multi* multi();
+
 // Rethrows the last failure of `ctx` as the matching reference exception
 // (errors.h:26-87).
 [[noreturn]] void raise(scls_ctx* ctx, scls_status st);

@@ -1,7 +1,9 @@
 // dropin_common.cpp — context, error mapping and struct conversion for the
 // B200 drop-in (see dropin.h).
+#include <algorithm>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "dropin.h"
 
@@ -34,6 +36,46 @@ scls_ctx* context() {
     g_ctx.ctx = c;
   }
   return g_ctx.ctx;
+}
+
+namespace {
+struct MultiHolder {
+  scls_multi* m = nullptr;
+  bool tried = false;
+  ~MultiHolder() {
+    if (m) scls_multi_destroy(m);
+  }
+};
+thread_local MultiHolder g_multi;
+}  // namespace
+
+// Every visible GPU (SCLS_DEVICES=k limits it to devices 0..k-1); null when
+// there is only one, so single-GPU callers keep the plain context.
+scls_multi* multi() {
+  if (!g_multi.tried) {
+    g_multi.tried = true;
+    const int count = scls_device_count();
+    std::vector<int32_t> devs;
+    const char* env = std::getenv("SCLS_DEVICES");
+    if (env && std::string(env).find(',') != std::string::npos) {  // an explicit list, e.g. "0,1" or "0,0"
+      std::string s(env);
+      for (size_t p = 0; p <= s.size();) {
+        const size_t q = std::min(s.find(',', p), s.size());
+        devs.push_back(std::atoi(s.substr(p, q - p).c_str()));
+        p = q + 1;
+      }
+    } else {
+      const int n = env ? std::min(count, std::atoi(env)) : count;
+      for (int i = 0; i < n; ++i) devs.push_back(i);
+    }
+    if (devs.size() > 1) {
+      scls_multi* m = nullptr;
+      if (scls_multi_create((int32_t)devs.size(), devs.data(), &m) != SCLS_OK)
+        throw Error("B200 multi-GPU sweep unavailable: " + last_error(nullptr));
+      g_multi.m = m;
+    }
+  }
+  return g_multi.m;
 }
 
 void raise(scls_ctx* ctx, scls_status st) {

@@ -173,8 +173,21 @@ std::vector<SweepRow> sweep(const RunConfig& base, const std::string& param,
     if (on_dev[v0]) {
       std::vector<scls_workload_spec> gs;
       for (std::size_t v : group) gs.push_back(specs[v]);
-      b200::check(ctx, scls_run_experiments(ctx, static_cast<int32_t>(group.size()), gs.data(), gc.data(), &lats[v0],
-                                            &mems[v0], gr.data(), hist_bins, gh.data(), nullptr, SCLS_MEM_HOST));
+      scls_multi* m = group.size() > 1 ? b200::multi() : nullptr;
+      if (m) {  // the runs sharded over every visible GPU, results gathered over NCCL
+        const scls_status st = scls_multi_run_experiments(m, static_cast<int32_t>(group.size()), gs.data(), gc.data(),
+                                                          &lats[v0], &mems[v0], gr.data(), hist_bins, gh.data(),
+                                                          nullptr);
+        if (st != SCLS_OK) {
+          char buf[1024];
+          scls_multi_last_error(m, buf, sizeof buf);
+          throw Error(std::string("B200 multi-GPU sweep failed: ") + buf);
+        }
+      } else {
+        b200::check(ctx, scls_run_experiments(ctx, static_cast<int32_t>(group.size()), gs.data(), gc.data(),
+                                              &lats[v0], &mems[v0], gr.data(), hist_bins, gh.data(), nullptr,
+                                              SCLS_MEM_HOST));
+      }
     } else {
       b200::check(ctx, scls_simulate(ctx, static_cast<int32_t>(group.size()), offs.data(), arr.data(), inp.data(),
                                      gen.data(), static_cast<int32_t>(gc.size()), gc.data(), idx.data(), &lats[v0],

@@ -34,6 +34,9 @@ EXPORTS = [
     "scls_batch_requests", "scls_offload", "scls_schedule", "scls_simulate",
     "scls_simulate_grid", "scls_generate", "scls_make_pool", "scls_debug_dp_profile", "scls_set_option",
     "scls_run_sweep", "scls_run_experiments", "scls_generate_batch", "scls_debug_log",
+    "scls_shard_range", "scls_comm_unique_id", "scls_comm_init", "scls_comm_size", "scls_run_sweep_sharded",
+    "scls_multi_create", "scls_multi_destroy", "scls_multi_last_error", "scls_multi_uses_nccl",
+    "scls_multi_run_sweep", "scls_multi_run_experiments", "scls_device_count",
 ]
 
 
@@ -93,6 +96,21 @@ def load():
                                        P(capi.TraceResult), i32, vp, P(capi.EventLog), i32]),
         "scls_generate_batch": (i32, [vp, i32, P(capi.WorkloadSpec), i64, vp, vp, vp, vp, i32]),
         "scls_debug_log": (i32, [vp, i64, vp, vp, i32]),
+        "scls_shard_range": (None, [i64, i32, i32, P(i64), P(i64)]),
+        "scls_comm_unique_id": (i32, [vp]),
+        "scls_comm_init": (i32, [vp, i32, i32, vp]),
+        "scls_comm_size": (i32, [vp]),
+        "scls_run_sweep_sharded": (i32, [vp, i32, P(capi.WorkloadSpec), i32, S, L, M,
+                                         P(capi.TraceResult), i32, vp, i32]),
+        "scls_multi_create": (i32, [i32, vp, P(vp)]),
+        "scls_multi_destroy": (None, [vp]),
+        "scls_multi_last_error": (C.c_size_t, [vp, C.c_char_p, C.c_size_t]),
+        "scls_multi_uses_nccl": (i32, [vp]),
+        "scls_multi_run_sweep": (i32, [vp, i32, P(capi.WorkloadSpec), i32, S, L, M,
+                                       P(capi.TraceResult), i32, vp, vp]),
+        "scls_multi_run_experiments": (i32, [vp, i32, P(capi.WorkloadSpec), S, L, M,
+                                             P(capi.TraceResult), i32, vp, vp]),
+        "scls_device_count": (i32, []),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -413,12 +431,123 @@ class Context:
                                                   hist_bins, _ptr(hist), None, capi.MEM_HOST))
         return res, hist[:n * hist_bins].reshape(n, hist_bins)
 
+    # -- the sharded sweep (one process per GPU, NCCL gather in the library) ----------
+    def comm_init(self, world, rank, uid):
+        """scls_comm_init: join the NCCL communicator `uid` (128 bytes from comm_unique_id())."""
+        b = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
+        self._check(self.lib.scls_comm_init(self.h, world, rank, b))
+
+    def comm_size(self):
+        return self.lib.scls_comm_size(self.h)
+
+    def run_sweep_sharded(self, specs, cfgs, lat, mem, hist_bins=64):
+        """scls_run_sweep_sharded with host outputs: this rank's shard of the
+        GLOBAL spec list, gathered so every rank returns the whole grid
+        (results[c * ntr + t], hist[c, t])."""
+        if isinstance(cfgs, capi.SchedCfg):
+            cfgs = [cfgs]
+        specs = list(specs)
+        ntr, nc = len(specs), len(cfgs)
+        sp = (capi.WorkloadSpec * max(ntr, 1))(*specs)
+        cfg_arr = (capi.SchedCfg * nc)(*cfgs)
+        res = (capi.TraceResult * max(ntr * nc, 1))()
+        hist = np.zeros(max(ntr * nc * hist_bins, 1), np.int64)
+        self._check(self.lib.scls_run_sweep_sharded(self.h, ntr, sp, nc, cfg_arr, C.byref(lat), C.byref(mem), res,
+                                                    hist_bins, _ptr(hist), capi.MEM_HOST))
+        return res, hist[:ntr * nc * hist_bins].reshape(nc, ntr, hist_bins)
+
     def debug_log(self, x):
         """The device port of glibc log on x (float64 array)."""
         x = np.ascontiguousarray(x, np.float64)
         y = np.zeros_like(x)
         self._check(self.lib.scls_debug_log(self.h, len(x), _ptr(x), _ptr(y), capi.MEM_HOST))
         return y
+
+
+def shard_range(total, shard, n_shards):
+    """scls_shard_range: contiguous [lo, hi) of `shard` (trace t -> floor(t * N / total))."""
+    lo, hi = C.c_int64(), C.c_int64()
+    load().scls_shard_range(total, shard, n_shards, C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
+
+
+def comm_unique_id():
+    """scls_comm_unique_id (rank 0): 128 bytes to broadcast to every rank."""
+    lib = load()
+    b = (C.c_uint8 * 128)()
+    st = lib.scls_comm_unique_id(b)
+    if st:
+        buf = C.create_string_buffer(4096)
+        lib.scls_last_error(None, buf, 4096)
+        raise SclsError(st, buf.value.decode())
+    return bytes(b)
+
+
+class Multi:
+    """scls_multi: one process driving several GPUs (a shard and a host
+    thread per entry of `devices`; NCCL gather when the devices are distinct)."""
+
+    def __init__(self, devices):
+        self.lib = load()
+        devs = (C.c_int32 * len(devices))(*devices)
+        h = C.c_void_p()
+        st = self.lib.scls_multi_create(len(devices), devs, C.byref(h))
+        if st:
+            buf = C.create_string_buffer(4096)
+            self.lib.scls_last_error(None, buf, 4096)
+            raise SclsError(st, buf.value.decode())
+        self.h = h
+        self.n = len(devices)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.scls_multi_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def uses_nccl(self):
+        return bool(self.lib.scls_multi_uses_nccl(self.h))
+
+    def run_sweep(self, specs, cfgs, lat, mem, hist_bins=64):
+        """Returns (results, hist, ms) with ms = per-shard device ms, gather ms, wall ms."""
+        if isinstance(cfgs, capi.SchedCfg):
+            cfgs = [cfgs]
+        specs = list(specs)
+        ntr, nc = len(specs), len(cfgs)
+        sp = (capi.WorkloadSpec * max(ntr, 1))(*specs)
+        cfg_arr = (capi.SchedCfg * nc)(*cfgs)
+        res = (capi.TraceResult * max(ntr * nc, 1))()
+        hist = np.zeros(max(ntr * nc * hist_bins, 1), np.int64)
+        ms = np.zeros(self.n + 2, np.float32)
+        st = self.lib.scls_multi_run_sweep(self.h, ntr, sp, nc, cfg_arr, C.byref(lat), C.byref(mem), res,
+                                           hist_bins, _ptr(hist), _ptr(ms))
+        if st:
+            buf = C.create_string_buffer(4096)
+            self.lib.scls_multi_last_error(self.h, buf, 4096)
+            raise SclsError(st, buf.value.decode())
+        return res, hist[:ntr * nc * hist_bins].reshape(nc, ntr, hist_bins), ms
+
+    def run_experiments(self, specs, cfgs, lat, mem, hist_bins=64):
+        """scls_multi_run_experiments: run i = specs[i] under cfgs[i], runs sharded over the devices."""
+        specs, cfgs = list(specs), list(cfgs)
+        n = len(specs)
+        sp = (capi.WorkloadSpec * max(n, 1))(*specs)
+        cfg_arr = (capi.SchedCfg * max(n, 1))(*cfgs)
+        res = (capi.TraceResult * max(n, 1))()
+        hist = np.zeros(max(n * hist_bins, 1), np.int64)
+        ms = np.zeros(self.n + 2, np.float32)
+        st = self.lib.scls_multi_run_experiments(self.h, n, sp, cfg_arr, C.byref(lat), C.byref(mem), res,
+                                                 hist_bins, _ptr(hist), _ptr(ms))
+        if st:
+            buf = C.create_string_buffer(4096)
+            self.lib.scls_multi_last_error(self.h, buf, 4096)
+            raise SclsError(st, buf.value.decode())
+        return res, hist[:n * hist_bins].reshape(n, hist_bins), ms
 
 
 def _flatten(traces):

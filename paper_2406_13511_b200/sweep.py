@@ -2,10 +2,16 @@
 
 The trace dimension of a sweep (reference `sweep`, experiment.cpp:62-85, and
 the C5 Monte Carlo grid) is the only dimension that shards: trace t goes to
-rank floor(t * N / T) (contiguous ranges).  Each rank simulates its shard on
-its own GPU with scls_simulate; the fixed-size per-trace result records are
-then all-gathered — the only collective, NCCL over NVLink on the GPU path,
-gloo in the CPU tests.
+rank floor(t * N / T) (contiguous ranges).  Each rank generates and
+simulates its shard on its own GPU, and the fixed-size per-trace result
+records are then all-gathered — the only collective.
+
+On the GPU path both steps live in the library: scls_run_sweep_sharded
+(csrc/multi.cu) runs the rank's shard and issues the ncclAllGather itself,
+on a communicator the ranks join with scls_comm_init; `join_comm` below
+broadcasts the NCCL id over the caller's process group.  `gather_records`
+is the torch.distributed restatement of the same gather (gloo in the CPU
+tests).
 """
 from __future__ import annotations
 
@@ -21,6 +27,18 @@ RECORD_WORDS = C.sizeof(capi.TraceResult) // 8
 def shard_range(total: int, rank: int, world: int):
     """Contiguous [lo, hi) of the traces owned by `rank`."""
     return rank * total // world, (rank + 1) * total // world
+
+
+def join_comm(ctx, rank: int, world: int, dist):
+    """Rank 0 draws the NCCL unique id (scls_comm_unique_id), every rank
+    receives it over `dist` and joins the library's communicator with
+    scls_comm_init.  Returns the id (for tests); ctx may be None (CPU tests)."""
+    from . import lib
+    box = [lib.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    if ctx is not None:
+        ctx.comm_init(world, rank, box[0])
+    return box[0]
 
 
 def records_to_array(results, count) -> np.ndarray:

@@ -104,3 +104,23 @@ def test_cli_trace_roundtrip_byte_identical(tmp_path):
                        capture_output=True)
         got[tag] = (rep.read_bytes(), log.read_bytes())
     assert got["ref"] == got["b200"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", ["0,0", "0,0,0"])
+def test_cli_sweep_sharded_byte_identical(tmp_path, devices):
+    """`slicesim sweep` with its runs sharded across devices (SCLS_DEVICES
+    lists the shards; on the one-GPU test box several shards share device 0
+    and the gather uses peer copies, on an 8-GPU node NCCL): the CSV is
+    byte-identical to the reference's sequential sweep."""
+    ref, b200 = _require("slicesim_ref"), _require("slicesim_b200")
+    args = "sweep --param rate --values 4,8,12,16,20 --set workload.duration=120 --out {d}/s.csv"
+    outs = {}
+    for tag, exe in (("ref", ref), ("b200", b200)):
+        d = tmp_path / tag
+        d.mkdir()
+        env = dict(os.environ, SCLS_DEVICES=devices)
+        p = subprocess.run([exe] + args.format(d=d).split(), capture_output=True, text=True, timeout=600, env=env)
+        assert p.returncode == 0, (tag, p.stderr[-2000:])
+        outs[tag] = (d / "s.csv").read_bytes()
+    assert outs["ref"] == outs["b200"] and len(outs["ref"]) > 0

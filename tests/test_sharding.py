@@ -70,3 +70,35 @@ def test_gather_world2_gloo(tmp_path):
     assert np.array_equal(full, want)
     back = sweep.array_to_records(full)
     assert back[3].completed == res[3].completed and back[6].throughput == res[6].throughput
+
+
+def test_library_shard_range_matches():
+    """scls_shard_range (the C++ sharded sweep's partition) == sweep.shard_range."""
+    from paper_2406_13511_b200 import lib
+    for total in (0, 1, 7, 12288, 4096):
+        for world in (1, 2, 3, 8):
+            for r in range(world):
+                assert lib.shard_range(total, r, world) == sweep.shard_range(total, r, world)
+
+
+def _comm_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    uid = sweep.join_comm(None, rank, world, dist)  # no GPU here: id exchange only
+    with open(f"{out_path}.{rank}", "wb") as f:
+        f.write(uid)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_id_broadcast_world2_gloo(tmp_path):
+    """The rank-0 NCCL id reaches every rank intact (scls_comm_unique_id works
+    without a GPU; scls_comm_init itself is covered by tests/test_multi_gpu.py)."""
+    pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "uid")
+    mp.start_processes(_comm_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
+    a, b = open(out + ".0", "rb").read(), open(out + ".1", "rb").read()
+    assert len(a) == 128 and a == b
