@@ -5,24 +5,29 @@ Monte Carlo sweep — 4096 traces (1024 seeds x arrival rates 10/15/20/25 req/s,
 600 s, 8 instances, S = 128, codefuse-like lengths, builtin latency model and
 rule-table memory) x the three policies {SCLS, SLS, ILS}: 12,288 simulations
 per step.  One step is the reference's sweep() (experiment.cpp:62-85:
-generate -> Simulator::run -> compute per run) through scls_run_sweep: the
-traces are generated on the device from their WorkloadSpecs (bit-exact with
-generate()), then every policy runs on every trace.  The trace dimension is
-sharded across ranks (contiguous ranges, strong scaling: the sweep is fixed as
-N grows); each rank generates and simulates its shard on its GPU and the
-per-trace result records are all-gathered over NCCL (the only collective).
-Device time, CUDA events on the launching stream, max over ranks.
+generate -> Simulator::run -> compute per run) through the C-ABI
+scls_run_sweep_sharded: the rank's contiguous shard of traces is generated on
+its GPU from the WorkloadSpecs (bit-exact with generate()), every policy runs
+on every trace, and the library all-gathers the fixed-size result records
+with one ncclAllGather (the only collective).  Strong scaling: the sweep is
+fixed as N grows.  Device time, CUDA events on the launching stream, max over
+ranks.
+
+Parity, outside the timed region: rank 0 runs the unmodified reference
+(oracle/_ref, compiled from /root/reference) on ALL 4096 traces x 3 policies
+on the host cores -- that run is also the cpu_baseline -- and compares every
+MetricsReport field, the slice histogram and the counters of all 12,288 jobs
+with the gathered device grid.
 
 The same JSON line carries the scheduling-core number (configs[2]): requests
 scheduled/s for batch_requests + offload of the 1M-request pool
 (bench_batcher.cpp make_pool(2^20, 7), analytic KV cap, S = 128, 8 workers),
-with its phase breakdown.
-
-Inputs are synthetic (the reference's own generators, exact); parity of the
-measured shard is checked against the C oracle and the host generator
-outside the timed region.
+with its phase breakdown and roofline, and C1 / C2 / C4 latency lines.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--gpus N > 1 without a torchrun environment relaunches itself under
+torch.distributed.run with N ranks (one per GPU, 127.0.0.1 rendezvous).
 """
 from __future__ import annotations
 
@@ -42,6 +47,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2406_13511_b200 import capi  # noqa: E402  (ctypes structs only)
+
 METRIC = ("requests scheduled/sec (sort+DP batching+offload) and simulated traces/sec "
           "at 1/2/4/8 B200")
 RATES = (10.0, 15.0, 20.0, 25.0)
@@ -56,31 +63,13 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--traces", type=int, default=4096)
     p.add_argument("--duration", type=float, default=600.0)
-    p.add_argument("--cpu-sample", type=int, default=0,
-                   help="traces per policy in the CPU baseline sample (0 = auto)")
-    p.add_argument("--no-c3", action="store_true")
+    p.add_argument("--no-c3", action="store_true", help="skip the C1-C4 side lines")
+    p.add_argument("--no-cpu", action="store_true", help="skip the CPU reference run (parity + cpu_baseline)")
     return p.parse_args()
 
 
 def trace_spec(i, duration):
-    from paper_2406_13511_b200 import capi
     return capi.workload_spec(rate=RATES[i % 4], duration_s=duration, seed=1000 + i // 4)
-
-
-def gen_traces(ids, duration, gen_fn):
-    """Generate traces in parallel host threads (ctypes releases the GIL)."""
-    with cf.ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
-        return list(ex.map(lambda i: gen_fn(trace_spec(i, duration)), ids))
-
-
-def flatten(traces):
-    offs = np.zeros(len(traces) + 1, np.int64)
-    for i, t in enumerate(traces):
-        offs[i + 1] = offs[i] + len(t[0])
-    arr = np.concatenate([t[0] for t in traces]).astype(np.float64)
-    inp = np.concatenate([t[1] for t in traces]).astype(np.int32)
-    gen = np.concatenate([t[2] for t in traces]).astype(np.int32)
-    return offs, arr, inp, gen
 
 
 class ClockSampler:
@@ -156,44 +145,65 @@ def ncu_traffic(name):
 
 
 # ------------------------------------------------------------------------------------------
+def ref_checker():
+    """(library, kind): the compiled reference (oracle/_ref) when present, else the C port."""
+    from oracle.pyoracle import RefLib, REF_SO, OracleLib, ORACLE_SO
+    try:
+        return RefLib(REF_SO), "reference"
+    except OSError:
+        return OracleLib(ORACLE_SO), "port"
+
+
+def ref_sweep(lib, kind, specs, cfgs, lat, mem, hist_bins, cores):
+    """The reference's sweep body on the host cores: per trace generate() once,
+    then Simulator::run + compute for every policy (ref_run_sweep)."""
+    if kind == "reference":
+        return lib.run_sweep(specs, cfgs, lat, mem, hist_bins=hist_bins, threads=cores)
+    traces = [lib.generate(sp) for sp in specs]  # the C port: same work, composed here
+    res, hist = [], []
+    for c in cfgs:
+        r, h = lib.simulate(traces, c, lat, mem, hist_bins=hist_bins, threads=cores)
+        res.extend(r)
+        hist.append(h)
+    out = (capi.TraceResult * len(res))(*res)
+    return out, np.stack(hist)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's own CPU implementation (oracle/_ref,
-    compiled from /root/reference sources) on the host cores, rank 0 only."""
+    compiled from /root/reference sources) on the host cores, rank 0 only,
+    on the SAME workload as our arm: every step is the full 4096-trace x 3
+    policy sweep, with the same warm-up and step counts."""
     if rank != 0:
         return
-    from oracle.pyoracle import RefLib, REF_SO, OracleLib, ORACLE_SO
-    from paper_2406_13511_b200 import capi
-    kind = "reference"
-    lib = RefLib(REF_SO) if os.path.exists(REF_SO) else None
-    if lib is None:
-        lib, kind = OracleLib(ORACLE_SO), "port"
+    lib, kind = ref_checker()
     cores = os.cpu_count() or 1
-    per = args.cpu_sample or max(8, min(64, cores * 4))
-    ids = list(range(per))
+    specs = [trace_spec(i, args.duration) for i in range(args.traces)]
     lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
     cfgs = [capi.sched_cfg(policy=p) for p in POLICIES]
 
     def step():
-        # experiment.cpp sweep on the host: generate each trace, run every policy
         t0 = time.perf_counter()
-        traces = gen_traces(ids, args.duration, lib.generate)
-        for c in cfgs:
-            lib.simulate(traces, c, lat, mem, threads=cores)
+        ref_sweep(lib, kind, specs, cfgs, lat, mem, 16, cores)
         return time.perf_counter() - t0
 
-    for _ in range(max(0, min(args.warmup, 1))):
+    for _ in range(args.warmup):
         step()
-    times = [step() for _ in range(max(1, min(args.steps, 2)))]
-    sec = statistics.median(times)
-    value = 3 * per / sec
+    times = [step() for _ in range(args.steps)]
+    sec = sum(times) / len(times)
+    value = 3 * args.traces / sec
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "traces/s",
-            "n_gpus": world, "steps": len(times), "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference generators: Poisson arrivals, codefuse-like lengths)",
-            "config": {"workload": f"C5 sweep sample: {per} traces x 3 policies ({args.duration:.0f} s, "
-                                   "8 instances, S=128, rates 10/15/20/25)", "host_threads": cores},
+            "data": "synthetic (the reference's own generate(): Poisson arrivals, codefuse-like lengths)",
+            "config": {"workload": f"C5 Monte Carlo sweep: {args.traces} traces (seeds x rates 10/15/20/25 req/s), "
+                                   f"{args.duration:.0f} s, 8 instances, S=128, max_gen 1024, x {{SCLS,SLS,ILS}} = "
+                                   f"{3 * args.traces} simulations per step", "traces": args.traces,
+                       "host_threads": cores},
             "cpu_baseline": {"value": value, "unit": "traces/s", "cores": cores, "kind": kind,
-                             "sample": f"{per} traces per step: generate once + 3 policies"},
+                             "sample": f"the full workload every step: {args.traces} traces x 3 policies "
+                                       "(generate once per trace + Simulator::run + compute per policy, "
+                                       "one digest-free counting pass per log)"},
             "e2e": {"value": value, "unit": "traces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -302,93 +312,85 @@ def bench_configs(ctx, lib, capi, steps):
     return out
 
 
+SIM_NCU = {"scls": ("sim_kernel_scls_4096", "sim_kernel<SCLS>"),
+           "ils": ("sim_ils_indep_4096", "sim_ils_indep_kernel"),
+           "sls": ("sim_sls_indep_4096", "sim_sls_indep_kernel")}
+REPORT_FIELDS = [f for f, _ in capi.TraceResult._fields_
+                 if f not in ("sim_clock", "h_complete_ids", "h_dispatch", "h_complete_t", "h_log")]
+FIELD_WORD = {f: getattr(capi.TraceResult, f).offset // 8 for f, _ in capi.TraceResult._fields_}
+
+
+def ncu_row(name):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+def issue_line(name, kname, units, unit_name, ms):
+    """SM / warp-issue efficiency of a latency-bound kernel (north star):
+    units/s measured live, and the ncu counters of the committed capture."""
+    row = ncu_row(name) or {}
+    return {"kernel": kname, unit_name + "_per_launch": units, "launch_ms": ms,
+            unit_name + "_per_s": units / (ms / 1e3) if ms else None,
+            "issue_active_pct": row.get("issue_active_pct"), "warps_active_pct": row.get("warps_active_pct"),
+            "top_stalls": row.get("stall_share"), "ncu_capture": row.get("report")}
+
+
 def run_ours(args, rank, world, dist):
     import torch
 
-    from paper_2406_13511_b200 import capi, lib, sweep
+    from paper_2406_13511_b200 import lib, sweep
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     ctx = lib.Context(local, C.c_void_p(stream.cuda_stream))
+    if world > 1:  # the library's own NCCL communicator (the gather runs inside scls_run_sweep_sharded)
+        sweep.join_comm(ctx, rank, world, dist)
+    nranks = ctx.comm_size()
+    assert nranks == world, (nranks, world)
     T = args.traces
     lo, hi = sweep.shard_range(T, rank, world)
-    ids = list(range(lo, hi))
-    traces = gen_traces(ids, args.duration, lib.generate)
-    offs, arr, inp, gen = flatten(traces)
-    nreq = int(offs[-1])
+    ntr = hi - lo
     lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
     cfgs = [capi.sched_cfg(policy=p) for p in POLICIES]
-    ntr = len(ids)
-    # device-resident inputs
-    d_offs = torch.from_numpy(offs).to(dev)
-    d_arr = torch.from_numpy(arr).to(dev)
-    d_inp = torch.from_numpy(inp).to(dev)
-    d_gen = torch.from_numpy(gen).to(dev)
     nfields = C.sizeof(capi.TraceResult) // 8
-    # one result row per (policy, trace) job of the grid, policy-major
-    d_res_all = torch.empty(3 * ntr * nfields, dtype=torch.int64, device=dev)
-    d_res = [d_res_all.view(3, ntr * nfields)[k] for k in range(3)]
     hist_bins = 16
-    d_hist = torch.empty(3 * ntr * hist_bins, dtype=torch.int64, device=dev)
+    # the whole grid (every rank holds it after the gather), policy-major: job c * T + t
+    d_res = torch.empty(3 * T * nfields, dtype=torch.int64, device=dev)
+    d_hist = torch.empty(3 * T * hist_bins, dtype=torch.int64, device=dev)
     ctx.set_digests(False)  # the reference's sweep reports metrics only
     cfg_arr = (capi.SchedCfg * 3)(*cfgs)
-
-    spec_arr = (capi.WorkloadSpec * ntr)(*[trace_spec(i, args.duration) for i in ids])
+    spec_arr = (capi.WorkloadSpec * T)(*[trace_spec(i, args.duration) for i in range(T)])
+    res_ptr = C.cast(C.c_void_p(d_res.data_ptr()), C.POINTER(capi.TraceResult))
 
     def sweep_step():
-        # experiment.cpp sweep: generate every trace on the device
-        # (workload.cpp:163-181, bit-exact) and run every policy on it
-        st = ctx.lib.scls_run_sweep(ctx.h, ntr, spec_arr, 3, cfg_arr, C.byref(lat), C.byref(mem),
-                                    C.cast(C.c_void_p(d_res_all.data_ptr()), C.POINTER(capi.TraceResult)),
-                                    hist_bins, C.c_void_p(d_hist.data_ptr()), None, capi.MEM_DEVICE)
+        # experiment.cpp sweep, sharded: this rank's traces generated on the
+        # device (workload.cpp:163-181, bit-exact), every policy on each, the
+        # result records all-gathered (ncclAllGather inside the library)
+        st = ctx.lib.scls_run_sweep_sharded(ctx.h, T, spec_arr, 3, cfg_arr, C.byref(lat), C.byref(mem), res_ptr,
+                                            hist_bins, C.c_void_p(d_hist.data_ptr()), capi.MEM_DEVICE)
         ctx._check(st)
-
-    def sim_grid():
-        # every policy on every trace (experiment.cpp sweep), inputs staged once
-        st = ctx.lib.scls_simulate_grid(ctx.h, ntr, C.c_void_p(d_offs.data_ptr()), C.c_void_p(d_arr.data_ptr()),
-                                        C.c_void_p(d_inp.data_ptr()), C.c_void_p(d_gen.data_ptr()), 3, cfg_arr,
-                                        C.byref(lat), C.byref(mem),
-                                        C.cast(C.c_void_p(d_res_all.data_ptr()), C.POINTER(capi.TraceResult)),
-                                        hist_bins, C.c_void_p(d_hist.data_ptr()), None, capi.MEM_DEVICE)
-        ctx._check(st)
-
-    def sim_policy(k):
-        # one policy alone (per-policy kernel times for the roofline line)
-        one = (capi.SchedCfg * 1)(cfgs[k])
-        st = ctx.lib.scls_simulate(ctx.h, ntr, C.c_void_p(d_offs.data_ptr()), C.c_void_p(d_arr.data_ptr()),
-                                   C.c_void_p(d_inp.data_ptr()), C.c_void_p(d_gen.data_ptr()), 1, one, None,
-                                   C.byref(lat), C.byref(mem),
-                                   C.cast(C.c_void_p(d_res[k].data_ptr()), C.POINTER(capi.TraceResult)),
-                                   hist_bins, C.c_void_p(d_hist.data_ptr()), None, capi.MEM_DEVICE)
-        ctx._check(st)
-
-    def gather():
-        # the sweep's only collective: per-trace result records to every rank
-        if world == 1:
-            return None
-        return [sweep.gather_records(d_res[k].view(ntr, nfields), T, world, dist) for k in range(3)]
-
-    def step():
-        sweep_step()
-        gather()
 
     for _ in range(args.warmup):
-        step()
+        sweep_step()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches = 0
+    shard_ms, gather_ms = [], []
     with ClockSampler(local) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        gen_ms = []
         for _ in range(args.steps):
             sweep_step()
             launches += ctx.launches()
-            gen_ms.append(ctx.timings()["generate"])
-            gather()
+            tm = ctx.timings()
+            shard_ms.append(tm["simulate"])
+            gather_ms.append(tm["offload"])
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -398,90 +400,49 @@ def run_ours(args, rank, world, dist):
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     elapsed = float(t_max.item())
-    total_sims = 3 * T * args.steps
-    value = total_sims / elapsed
+    value = 3 * T * args.steps / elapsed
+    grid = d_res.view(3 * T, nfields).cpu().numpy().copy()
+    grid_hist = d_hist.view(3, T, hist_bins).cpu().numpy().copy()
 
-    # per-policy kernel times (each policy launched alone; outside the timed region)
-    kernel_ms = {p: [] for p in POLICIES}
-    for _ in range(2):
-        for k in range(3):
-            sim_policy(k)
-            kernel_ms[POLICIES[k]].append(ctx.timings()["simulate"])
+    # per-policy launches of this rank's shard alone (outside the timed region):
+    # the kernel times and event counts behind the roofline / issue lines
+    specs_local = [trace_spec(i, args.duration) for i in range(lo, hi)]
+    pol_ms, pol_events, pol_gen = {}, {}, []
+    for k, p in enumerate(POLICIES):
+        ms = []
+        for _ in range(2):
+            r, _h = ctx.run_sweep(specs_local, [cfgs[k]], lat, mem, hist_bins=hist_bins)
+            tm = ctx.timings()
+            ms.append(tm["simulate"])
+            pol_gen.append(tm["generate"])
+        pol_ms[p] = statistics.median(ms)
+        pol_events[p] = int(sum(r[i].n_events for i in range(ntr)))
+    nreq = int(grid[:T, FIELD_WORD["n_requests"]].sum())  # requests of the sweep (one row per trace)
 
-    # e2e through the public C-ABI with host buffers: scls_run_sweep takes the
-    # WorkloadSpecs from host memory (H2D inside the call), generates and
-    # simulates on the device, and returns the result records and histograms
-    # to host memory (D2H inside the call) — the reference's sweep() call shape
-    specs_host = [trace_spec(i, args.duration) for i in ids]
-    ctx.run_sweep(specs_host, cfgs, lat, mem, hist_bins=hist_bins)  # warm-up (host result buffers)
+    # e2e through the public C-ABI with host buffers: WorkloadSpecs in from the
+    # host (H2D inside the call), the gathered grid out to host memory (D2H)
+    ctx.run_sweep_sharded(spec_arr, cfgs, lat, mem, hist_bins=hist_bins)  # warm-up of the host path
     e2e_t = []
     for _ in range(max(3, args.steps)):
         t0 = time.perf_counter()
-        ctx.run_sweep(specs_host, cfgs, lat, mem, hist_bins=hist_bins)
+        ctx.run_sweep_sharded(spec_arr, cfgs, lat, mem, hist_bins=hist_bins)
         e2e_t.append(time.perf_counter() - t0)
-    e2e_local = statistics.median(e2e_t)
-    t_e2e = torch.tensor([e2e_local], dtype=torch.float64, device=dev)
+    t_e2e = torch.tensor([statistics.median(e2e_t)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     h2d = ntr * C.sizeof(capi.WorkloadSpec)
-    d2h = 3 * ntr * (C.sizeof(capi.TraceResult) + 8 * hist_bins)
-
-    # the simulator alone on pre-generated traces: device-resident inputs, and
-    # e2e with the 16 B/request inputs copied from pinned host memory per call
-    sim_only = []
-    for _ in range(max(2, args.steps // 2)):
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        sim_grid()
-        s1.record(stream)
-        torch.cuda.synchronize()
-        sim_only.append(s0.elapsed_time(s1))
-    p_offs = torch.from_numpy(offs).pin_memory().numpy()
-    p_arr = torch.from_numpy(arr).pin_memory().numpy()
-    p_inp = torch.from_numpy(inp).pin_memory().numpy()
-    p_gen = torch.from_numpy(gen).pin_memory().numpy()
-    ctx.simulate_grid_flat(p_offs, p_arr, p_inp, p_gen, cfgs, lat, mem, hist_bins=hist_bins)  # warm-up
-    sim_e2e = []
-    for _ in range(max(3, args.steps)):
-        t0 = time.perf_counter()
-        ctx.simulate_grid_flat(p_offs, p_arr, p_inp, p_gen, cfgs, lat, mem, hist_bins=hist_bins)
-        sim_e2e.append(time.perf_counter() - t0)
-
-    # device generation parity on the whole shard: run_sweep == simulate_grid on
-    # the host-generated traces, every result word of every job
-    sweep_step()
-    r_sweep = d_res_all.clone()
-    sim_grid()
-    gen_mismatch = int((r_sweep.view(3 * ntr, nfields) != d_res_all.view(3 * ntr, nfields)).any(dim=1).sum().item())
-    # parity of this rank's first traces vs the C oracle (outside the timed region)
-    ctx.set_digests(True)
-    from oracle.pyoracle import oracle_lib
-    orc = oracle_lib()
-    k = min(ntr, 6)
-    bad = 0
-    for c in cfgs:
-        a, _ = ctx.simulate(traces[:k], c, lat, mem)
-        b, _ = orc.simulate(traces[:k], c, lat, mem)
-        for i in range(k):
-            for f, _ in capi.TraceResult._fields_:
-                if f != "sim_clock" and getattr(a[i], f) != getattr(b[i], f):
-                    bad += 1
-    statuses = set()
-    for kk in range(3):
-        r = d_res[kk].view(ntr, nfields).cpu().numpy()
-        statuses |= set(int(x) & 0xffffffff for x in r[:, 0])
+    d2h = 3 * T * (C.sizeof(capi.TraceResult) + 8 * hist_bins)
+    statuses = sorted(set(int(x) & 0xffffffff for x in grid[:, 0]))
 
     if rank != 0:
         return
     hbm, peak_src = peaks()
-    pol_ms = {p: statistics.median(v) for p, v in kernel_ms.items()}
-    dom = max(pol_ms, key=pol_ms.get)  # the dominant launch (SCLS on this sweep)
-    # the sweep's launches (digests off): SCLS sim_kernel, ILS / SLS independent-lane kernels
-    ncu_name = {"scls": "sim_kernel_scls", "ils": "sim_ils_indep", "sls": "sim_sls_indep"}[dom]
-    kname = {"scls": "sim_kernel<SCLS>", "ils": "sim_ils_indep_kernel", "sls": "sim_sls_indep_kernel"}[dom]
-    sim_ms = pol_ms[dom] / 1e3
-    bytes_per_launch = nreq * 16 + ntr * (C.sizeof(capi.TraceResult) + 8 * hist_bins)
-    achieved = bytes_per_launch / sim_ms / 1e9
+    dom = max(pol_ms, key=pol_ms.get)  # the dominant launch
+    ncu_name, kname = SIM_NCU[dom]
+    sim_s = pol_ms[dom] / 1e3
+    shard_req = int(grid[lo:hi, FIELD_WORD["n_requests"]].sum())
+    bytes_per_launch = shard_req * 16 + ntr * (C.sizeof(capi.TraceResult) + 8 * hist_bins)
+    achieved = bytes_per_launch / sim_s / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "traces/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
@@ -491,70 +452,100 @@ def run_ours(args, rank, world, dist):
         "config": {"workload": f"C5 Monte Carlo sweep (experiment.cpp sweep: generate + simulate + metrics): "
                                f"{T} traces (seeds x rates 10/15/20/25 req/s), {args.duration:.0f} s, 8 instances, "
                                f"S=128, max_gen 1024, x {{SCLS,SLS,ILS}} = {3 * T} simulations per step",
-                   "traces": T, "requests_per_rank": nreq, "parallelism": f"trace-sharded dp{world}",
-                   "l2": "generated traces (%.0f MB per rank) > L2, rewritten every step" % (nreq * 16 / 1e6)},
+                   "traces": T, "requests": nreq, "parallelism": f"trace-sharded dp{world}",
+                   "l2": "generated traces (%.0f MB per rank) > L2, rewritten every step" % (shard_req * 16 / 1e6)},
         "e2e": {"value": 3 * T / float(t_e2e.item()), "unit": "traces/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
+        "comm": {"backend": "nccl (library-owned communicator, scls_comm_init)" if world > 1 else "none (one rank)",
+                 "nranks": nranks, "comm_nranks_ok": nranks == world,
+                 "gather_ms_per_step": statistics.median(gather_ms), "shard_ms_per_step": statistics.median(shard_ms)},
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(f"{ncu_name}_{T}"),
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(ncu_name),
                      "peak_source": peak_src, "bytes_per_launch": bytes_per_launch,
                      "launch_ms": pol_ms[dom],
-                     "note": "event-chain latency/issue bound (ncu: profiles/ncu_summary.json); algorithmic "
-                             "bytes = 16 B/request in + result records out"},
+                     "note": "the simulators are event-chain (issue / latency) bound, not HBM bound: "
+                             "algorithmic bytes = 16 B/request in + result records out; the issue efficiency "
+                             "the north star asks for is in `issue_efficiency`"},
+        "issue_efficiency": {p: issue_line(SIM_NCU[p][0], SIM_NCU[p][1], pol_events[p], "events", pol_ms[p])
+                             for p in POLICIES},
         "kernel_ms_per_policy": pol_ms,
-        "generate_ms_per_step": statistics.median(gen_ms),
-        "simulate_only": {"value": 3 * ntr / (statistics.median(sim_only) / 1e3),
-                          "e2e_value": 3 * ntr / statistics.median(sim_e2e), "unit": "traces/s",
-                          "note": "scls_simulate_grid on host-generated traces (this rank); e2e copies "
-                                  "16 B/request from pinned host memory per call"},
-        "parity": {"checked": f"{k} traces x 3 policies vs C oracle, all TraceResult fields bit-exact; "
-                              f"device-generated sweep vs host-generated traces, all {3 * ntr} jobs of this rank",
-                   "mismatches": bad, "generate_mismatches": gen_mismatch, "statuses": sorted(statuses)},
+        "generate_ms_per_shard": statistics.median(pol_gen),
+        "statuses": statuses,
         "clocks": clk.summary(),
     }
     if not args.no_c3:
         line["scheduler_c3"] = bench_c3(ctx, torch, lib, capi, stream, max(2, args.steps // 2), 2)
         line["configs_c1_c2_c4"] = bench_configs(ctx, lib, capi, args.steps)
-    if world == 1:
-        line["cpu_baseline"] = cpu_baseline(args)
+    if not args.no_cpu:
+        cpu, parity = cpu_reference(args, T, cfgs, lat, mem, hist_bins, grid, grid_hist)
+        line["cpu_baseline"] = cpu
+        line["parity"] = parity
+        if not args.no_c3:
+            line["cpu_baseline"]["scheduler_c3"] = cpu_c3()
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(args):
-    """The reference (oracle/_ref) on this host's cores, bounded sample."""
-    from oracle.pyoracle import RefLib, REF_SO, OracleLib, ORACLE_SO
-    from paper_2406_13511_b200 import capi
-    kind = "reference"
-    try:
-        lib = RefLib(REF_SO)
-    except OSError:
-        lib, kind = OracleLib(ORACLE_SO), "port"
+def cpu_reference(args, T, cfgs, lat, mem, hist_bins, grid, grid_hist):
+    """The unmodified reference on ALL T traces x 3 policies on this host's
+    cores (timed: the cpu_baseline), then every job compared with the device
+    grid: every MetricsReport field, the slice histogram and the counters."""
+    lib, kind = ref_checker()
     cores = os.cpu_count() or 1
-    per = args.cpu_sample or max(8, min(64, cores * 4))
-    lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
+    specs = [trace_spec(i, args.duration) for i in range(T)]
     t0 = time.perf_counter()
-    traces = gen_traces(list(range(per)), args.duration, lib.generate)
-    for p in POLICIES:
-        lib.simulate(traces, capi.sched_cfg(policy=p), lat, mem, threads=cores)
+    want, want_hist = ref_sweep(lib, kind, specs, cfgs, lat, mem, hist_bins, cores)
     sec = time.perf_counter() - t0
-    out = {"value": 3 * per / sec, "unit": "traces/s", "cores": cores, "kind": kind,
-           "sample": f"{per} traces of the C5 sweep: generate once + 3 policies, {cores} host threads"}
-    # C3 single-thread (the reference API is one serial call)
+    cpu = {"value": 3 * T / sec, "unit": "traces/s", "cores": cores, "kind": kind,
+           "sample": f"the full workload: {T} traces x 3 policies (generate once per trace + Simulator::run + "
+                     f"compute per policy, one digest-free counting pass per log), {cores} host threads"}
+    nfields = C.sizeof(capi.TraceResult) // 8
+    wg = np.frombuffer(C.string_at(C.addressof(want), 3 * T * C.sizeof(capi.TraceResult)),
+                       np.int64).reshape(3 * T, nfields)
+    word = sorted(set(FIELD_WORD[f] for f in REPORT_FIELDS))  # status + worker_count share word 0
+    bad_jobs = np.nonzero((grid[:, word] != wg[:, word]).any(axis=1))[0]
+    bad_hist = np.nonzero((grid_hist.reshape(3 * T, -1) != want_hist.reshape(3 * T, -1)).any(axis=1))[0]
+    parity = {"checked": f"all {3 * T} jobs ({T} traces x 3 policies) vs the {kind} on the host: every "
+                         "MetricsReport field bit-exact, slice histogram, completed/batch/pad/invalid/event counters",
+              "jobs": 3 * T, "mismatched_jobs": int(len(set(bad_jobs) | set(bad_hist))),
+              "first_mismatches": [int(j) for j in sorted(set(bad_jobs) | set(bad_hist))[:8]]}
+    return cpu, parity
+
+
+def cpu_c3():
+    """C3 on one host thread (the reference API is one serial call)."""
+    from oracle.pyoracle import OracleLib, ORACLE_SO
+    lib, kind = ref_checker()
     eff, arr, ids, _ = (OracleLib(ORACLE_SO)).make_pool(1 << 20, 7)
     t0 = time.perf_counter()
     res = lib.batch_requests(eff, arr, ids, 128, capi.builtin_latency_model(), capi.builtin_analytic_memory_model())
     lib.offload(res["batch_id"], res["est"], np.arange(8, dtype=np.int32), [0.0] * 8)
     sec3 = time.perf_counter() - t0
-    out["scheduler_c3"] = {"value": (1 << 20) / sec3, "unit": "requests scheduled/s", "cores": 1,
-                           "kind": kind, "sample": "one batch_requests + offload of the 1M pool"}
-    return out
+    return {"value": (1 << 20) / sec3, "unit": "requests scheduled/s", "cores": 1,
+            "kind": kind, "sample": "one batch_requests + offload of the 1M pool"}
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run
+    with N ranks (the driver's own launch shape) and return its exit code."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     dist = None
     if world > 1:
         import torch

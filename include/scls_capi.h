@@ -391,6 +391,8 @@ typedef struct scls_multi scls_multi;
 scls_status scls_multi_create(int32_t n_dev, const int32_t* devices, scls_multi** out);
 void scls_multi_destroy(scls_multi* m);
 size_t scls_multi_last_error(const scls_multi* m, char* buf, size_t cap);
+/* scls_set_option on every device context of the group. */
+scls_status scls_multi_set_option(scls_multi* m, int32_t option, int64_t value);
 /* 1 when the gather runs over NCCL (distinct devices), 0 for peer copies. */
 int32_t scls_multi_uses_nccl(const scls_multi* m);
 /* results / slice_hist in host memory.  out_ms (optional, n_dev + 2 floats):

@@ -224,6 +224,28 @@ def _alloc_log(n_logged, rec_cap, mem_cap):
 class RefLib(_Checker):
     prefix = "ref_"
 
+    def run_sweep(self, specs, cfgs, lat, mem, hist_bins=16, threads=1):
+        """ref_run_sweep: the reference's sweep body for every (config, trace):
+        generate once per trace, Simulator::run + compute per config, no
+        digests.  Returns (results[c * ntr + t], hist [nc, ntr, bins])."""
+        fn = self.lib.ref_run_sweep
+        fn.restype = C.c_int32
+        fn.argtypes = [C.c_int32, C.POINTER(capi.WorkloadSpec), C.c_int32, C.POINTER(capi.SchedCfg),
+                       C.POINTER(capi.Latency), C.POINTER(capi.Memory), C.POINTER(capi.TraceResult), C.c_int32,
+                       C.POINTER(C.c_int64), C.c_int32]
+        specs = list(specs)
+        if isinstance(cfgs, capi.SchedCfg):
+            cfgs = [cfgs]
+        ntr, nc = len(specs), len(cfgs)
+        sp = (capi.WorkloadSpec * max(ntr, 1))(*specs)
+        ca = (capi.SchedCfg * nc)(*cfgs)
+        res = (capi.TraceResult * max(ntr * nc, 1))()
+        hist = np.zeros(max(ntr * nc * hist_bins, 1), np.int64)
+        st = fn(ntr, sp, nc, ca, C.byref(lat), C.byref(mem), res, hist_bins, _p(hist, C.c_int64), threads)
+        if st:
+            self._raise(st)
+        return res, hist[:ntr * nc * hist_bins].reshape(nc, ntr, hist_bins)
+
 
 class OracleLib(_Checker):
     prefix = "orc_"

@@ -137,8 +137,10 @@ S::LengthDist to_ref(const scls_length_dist& d) {
   }
 }
 
+// hash = false skips the FNV digests (h_* stay 0): what remains is one
+// counting pass over the log (completions, slice histogram, batch counters).
 void fill_result(const S::EventLog& log, scls_trace_result* r, int32_t hist_bins,
-                 int64_t* hist, scls_event_log* out_log, int64_t trace) {
+                 int64_t* hist, scls_event_log* out_log, int64_t trace, bool hash = true) {
   uint64_t hc = SCLS_FNV_OFFSET, hd = SCLS_FNV_OFFSET, ht = SCLS_FNV_OFFSET,
            hl = SCLS_FNV_OFFSET;
   int64_t nd = 0, nt = 0, pad = 0, inval = 0, bc = 0, bm = 0, er = 0, done = 0;
@@ -152,25 +154,31 @@ void fill_result(const S::EventLog& log, scls_trace_result* r, int32_t hist_bins
   }
   for (const S::EventRecord& e : log.events) {
     const int32_t kind = static_cast<int32_t>(e.kind);
+    if (hash) {
     hl = scls_hash_record(hl, kind, e.t, e.request, e.worker, e.batch, e.n, e.l_in,
                           e.planned_l_out, e.served_l_out, e.est_serve_s,
                           e.input_len, e.gen_len, e.response_s, e.slices,
                           e.next_interval_s, static_cast<int32_t>(e.members.size()));
     for (const S::MemberAccounting& m : e.members)
       hl = scls_hash_member(hl, m.request, m.effective_input, m.pad, m.gen, m.invalid);
+    }
     switch (e.kind) {
       case S::EventKind::kComplete:
-        hc = scls_fnv_bytes(hc, static_cast<uint64_t>(e.request));
-        ht = scls_fnv_bytes(ht, scls_dbits(e.t));
+        if (hash) {
+          hc = scls_fnv_bytes(hc, static_cast<uint64_t>(e.request));
+          ht = scls_fnv_bytes(ht, scls_dbits(e.t));
+        }
         ++done;
         if (hist && e.slices >= 0 && e.slices < hist_bins)
           hist[trace * hist_bins + e.slices] += 1;
         break;
       case S::EventKind::kDispatch:
-        hd = scls_fnv_bytes(hd, static_cast<uint64_t>(e.batch));
-        hd = scls_fnv_bytes(hd, static_cast<uint64_t>(static_cast<int64_t>(e.worker)));
-        hd = scls_fnv_bytes(hd, static_cast<uint64_t>(static_cast<int64_t>(e.n)));
-        hd = scls_fnv_bytes(hd, static_cast<uint64_t>(static_cast<int64_t>(e.l_in)));
+        if (hash) {
+          hd = scls_fnv_bytes(hd, static_cast<uint64_t>(e.batch));
+          hd = scls_fnv_bytes(hd, static_cast<uint64_t>(static_cast<int64_t>(e.worker)));
+          hd = scls_fnv_bytes(hd, static_cast<uint64_t>(static_cast<int64_t>(e.n)));
+          hd = scls_fnv_bytes(hd, static_cast<uint64_t>(static_cast<int64_t>(e.l_in)));
+        }
         ++nd;
         break;
       case S::EventKind::kTick: ++nt; break;
@@ -208,10 +216,10 @@ void fill_result(const S::EventLog& log, scls_trace_result* r, int32_t hist_bins
     out_log->rec_count[trace] = rec_n;
     out_log->mem_count[trace] = mem_n;
   }
-  r->h_complete_ids = hc;
-  r->h_dispatch = hd;
-  r->h_complete_t = ht;
-  r->h_log = hl;
+  r->h_complete_ids = hash ? hc : 0;
+  r->h_dispatch = hash ? hd : 0;
+  r->h_complete_t = hash ? ht : 0;
+  r->h_log = hash ? hl : 0;
   r->n_events = static_cast<int64_t>(log.events.size());
   r->n_dispatches = nd;
   r->n_ticks = nt;
@@ -404,6 +412,83 @@ scls_status ref_simulate(int32_t n_traces, const int64_t* req_offset, const doub
       } catch (...) {
         r->status = map_exception();
         r->error_request_id = g_err_request;
+      }
+    }
+  };
+  if (n_threads <= 1) {
+    worker();
+  } else {
+    std::vector<std::thread> pool;
+    for (int32_t i = 0; i < n_threads; ++i) pool.emplace_back(worker);
+    for (auto& th : pool) th.join();
+  }
+  return SCLS_OK;
+}
+
+// The reference's sweep body (experiment.cpp:62-85 / run_experiment :39-60)
+// for n_traces x n_cfgs jobs: per trace, generate(spec) once (workload.h:78),
+// then for every config Simulator::run + compute (sim_engine.h:61-67,
+// metrics.h:41) -- exactly the work of one reference sweep value -- plus one
+// digest-free counting pass over each log for the parity record.  Traces
+// are spread over n_threads host threads (independent runs may execute
+// concurrently, sim_engine.h:55-58).  Job j = c * n_traces + t.
+scls_status ref_run_sweep(int32_t n_traces, const scls_workload_spec* specs, int32_t n_cfgs,
+                          const scls_sched_cfg* cfgs, const scls_latency* lat, const scls_memory* mem,
+                          scls_trace_result* results, int32_t hist_bins, int64_t* slice_hist,
+                          int32_t n_threads) {
+  const S::LatencyModel latency = to_ref(*lat);
+  const S::MemoryModel memory = to_ref(*mem);
+  std::atomic<int32_t> next{0};
+  auto worker = [&]() {
+    for (;;) {
+      const int32_t t = next.fetch_add(1);
+      if (t >= n_traces) return;
+      std::vector<S::Request> reqs;
+      scls_status gen_status = SCLS_OK;
+      try {
+        S::WorkloadSpec w;
+        w.rate = specs[t].rate;
+        w.duration_s = specs[t].duration_s;
+        w.input_len_dist = to_ref(specs[t].input_len_dist);
+        w.gen_len_dist = to_ref(specs[t].gen_len_dist);
+        w.max_input_limit = specs[t].max_input_limit;
+        w.max_gen_limit = specs[t].max_gen_limit;
+        w.seed = specs[t].seed;
+        reqs = S::generate(w);
+      } catch (...) {
+        gen_status = map_exception();
+      }
+      for (int32_t c = 0; c < n_cfgs; ++c) {
+        const int64_t j = (int64_t)c * n_traces + t;
+        scls_trace_result* r = &results[j];
+        std::memset(r, 0, sizeof *r);
+        r->worker_count = cfgs[c].worker_count;
+        r->error_request_id = -1;
+        r->n_requests = static_cast<int64_t>(reqs.size());
+        if (slice_hist) std::fill(slice_hist + j * hist_bins, slice_hist + (j + 1) * hist_bins, 0);
+        if (gen_status != SCLS_OK) {
+          r->status = gen_status;
+          continue;
+        }
+        try {
+          S::Simulator sim(to_ref(cfgs[c]), latency, memory, cfgs[c].horizon_s);
+          auto policy = S::make_scheduler(to_ref(cfgs[c]).policy);
+          const S::EventLog elog = sim.run(reqs, *policy);
+          fill_result(elog, r, hist_bins, slice_hist, nullptr, j, false);
+          const S::MetricsReport rep = S::compute(elog);
+          r->throughput = rep.throughput;
+          r->avg_response_s = rep.avg_response_s;
+          r->p95_response_s = rep.p95_response_s;
+          r->ct_std_s = rep.ct_std_s;
+          r->avg_pad_tokens = rep.avg_pad_tokens;
+          r->avg_invalid_tokens = rep.avg_invalid_tokens;
+          r->avg_batch_size = rep.avg_batch_size;
+          r->early_return_ratio = rep.early_return_ratio;
+          r->status = SCLS_OK;
+        } catch (...) {
+          r->status = map_exception();
+          r->error_request_id = g_err_request;
+        }
       }
     }
   };

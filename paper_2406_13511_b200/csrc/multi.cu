@@ -337,6 +337,15 @@ extern "C" size_t scls_multi_last_error(const scls_multi* m, char* buf, size_t c
   return s.size();
 }
 
+extern "C" scls_status scls_multi_set_option(scls_multi* m, int32_t option, int64_t value) {
+  if (!m) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null multi context");
+  for (scls_ctx* c : m->ctx) {
+    const scls_status st = scls_set_option(c, option, value);
+    if (st) return multi_error(m, st, c->err);
+  }
+  return SCLS_OK;
+}
+
 extern "C" int32_t scls_multi_uses_nccl(const scls_multi* m) { return m && !m->comm.empty() ? 1 : 0; }
 
 namespace {

@@ -72,6 +72,7 @@ scls_multi* multi() {
       scls_multi* m = nullptr;
       if (scls_multi_create((int32_t)devs.size(), devs.data(), &m) != SCLS_OK)
         throw Error("B200 multi-GPU sweep unavailable: " + last_error(nullptr));
+      scls_multi_set_option(m, SCLS_OPT_SIM_DIGESTS, 0);  // sweeps report metrics only
       g_multi.m = m;
     }
   }

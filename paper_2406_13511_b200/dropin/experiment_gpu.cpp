@@ -184,14 +184,22 @@ std::vector<SweepRow> sweep(const RunConfig& base, const std::string& param,
           throw Error(std::string("B200 multi-GPU sweep failed: ") + buf);
         }
       } else {
-        b200::check(ctx, scls_run_experiments(ctx, static_cast<int32_t>(group.size()), gs.data(), gc.data(),
-                                              &lats[v0], &mems[v0], gr.data(), hist_bins, gh.data(), nullptr,
-                                              SCLS_MEM_HOST));
+        // metrics only (no log digests): the sweep keeps reports, not logs
+        scls_set_option(ctx, SCLS_OPT_SIM_DIGESTS, 0);
+        const scls_status st = scls_run_experiments(ctx, static_cast<int32_t>(group.size()), gs.data(), gc.data(),
+                                                    &lats[v0], &mems[v0], gr.data(), hist_bins, gh.data(), nullptr,
+                                                    SCLS_MEM_HOST);
+        scls_set_option(ctx, SCLS_OPT_SIM_DIGESTS, 1);
+        b200::check(ctx, st);
       }
     } else {
-      b200::check(ctx, scls_simulate(ctx, static_cast<int32_t>(group.size()), offs.data(), arr.data(), inp.data(),
-                                     gen.data(), static_cast<int32_t>(gc.size()), gc.data(), idx.data(), &lats[v0],
-                                     &mems[v0], gr.data(), hist_bins, gh.data(), nullptr, SCLS_MEM_HOST));
+      scls_set_option(ctx, SCLS_OPT_SIM_DIGESTS, 0);
+      const scls_status st = scls_simulate(ctx, static_cast<int32_t>(group.size()), offs.data(), arr.data(),
+                                           inp.data(), gen.data(), static_cast<int32_t>(gc.size()), gc.data(),
+                                           idx.data(), &lats[v0], &mems[v0], gr.data(), hist_bins, gh.data(), nullptr,
+                                           SCLS_MEM_HOST);
+      scls_set_option(ctx, SCLS_OPT_SIM_DIGESTS, 1);
+      b200::check(ctx, st);
     }
     for (std::size_t g = 0; g < group.size(); ++g) {
       res[group[g]] = gr[g];

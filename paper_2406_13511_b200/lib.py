@@ -37,6 +37,7 @@ EXPORTS = [
     "scls_shard_range", "scls_comm_unique_id", "scls_comm_init", "scls_comm_size", "scls_run_sweep_sharded",
     "scls_multi_create", "scls_multi_destroy", "scls_multi_last_error", "scls_multi_uses_nccl",
     "scls_multi_run_sweep", "scls_multi_run_experiments", "scls_device_count",
+    "scls_multi_set_option",
 ]
 
 
@@ -111,6 +112,7 @@ def load():
         "scls_multi_run_experiments": (i32, [vp, i32, P(capi.WorkloadSpec), S, L, M,
                                              P(capi.TraceResult), i32, vp, vp]),
         "scls_device_count": (i32, []),
+        "scls_multi_set_option": (i32, [vp, i32, i64]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -446,9 +448,13 @@ class Context:
         (results[c * ntr + t], hist[c, t])."""
         if isinstance(cfgs, capi.SchedCfg):
             cfgs = [cfgs]
-        specs = list(specs)
-        ntr, nc = len(specs), len(cfgs)
-        sp = (capi.WorkloadSpec * max(ntr, 1))(*specs)
+        if isinstance(specs, C.Array):  # a prebuilt scls_workload_spec array is passed as is
+            sp, ntr = specs, len(specs)
+        else:
+            specs = list(specs)
+            ntr = len(specs)
+            sp = (capi.WorkloadSpec * max(ntr, 1))(*specs)
+        nc = len(cfgs)
         cfg_arr = (capi.SchedCfg * nc)(*cfgs)
         res = (capi.TraceResult * max(ntr * nc, 1))()
         hist = np.zeros(max(ntr * nc * hist_bins, 1), np.int64)
@@ -509,6 +515,12 @@ class Multi:
 
     def __exit__(self, *a):
         self.close()
+
+    def set_digests(self, on):
+        """SCLS_OPT_SIM_DIGESTS on every device context (default on)."""
+        st = self.lib.scls_multi_set_option(self.h, 1, 1 if on else 0)
+        if st:
+            raise SclsError(st, "scls_multi_set_option failed")
 
     def uses_nccl(self):
         return bool(self.lib.scls_multi_uses_nccl(self.h))

@@ -42,6 +42,7 @@ def test_multi_matches_single_device(want, devices):
     specs, cfgs, w_res, w_hist = want
     with lib.Multi(devices) as m:
         assert m.uses_nccl() is False  # one device listed (possibly repeatedly)
+        m.set_digests(False)  # as `want`: the sweep reports metrics only
         res, hist, ms = m.run_sweep(specs, cfgs, capi.builtin_latency_model(), capi.builtin_memory_model(),
                                     hist_bins=16)
     assert np.array_equal(_words(res, 33), w_res)
