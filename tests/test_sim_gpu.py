@@ -155,8 +155,9 @@ def test_error_statuses(ctx, orc):
                 a, _ = ctx.simulate([trace, zero, zero, trace], capi.sched_cfg(policy=pol), lat, MEMORIES["rule"]())
                 ctx.set_digests(True)
                 assert [r.status for r in a] == [0, capi.ERR_INVALID_ARGUMENT, capi.ERR_INVALID_ARGUMENT, 0], pol
-                b, _ = orc.simulate([trace], capi.sched_cfg(policy=pol), lat, MEMORIES["rule"]())
-                assert_results_equal(a[3], b[0], pol)
+                if digests:
+                    b, _ = orc.simulate([trace], capi.sched_cfg(policy=pol), lat, MEMORIES["rule"]())
+                    assert_results_equal(a[3], b[0], pol)
     # invalid config -> Error, other traces unaffected
     a, _ = ctx.simulate([trace, trace], [capi.sched_cfg(), capi.sched_cfg(lambda_=2.0)], lat,
                         MEMORIES["rule"](), cfg_index=[0, 1])
