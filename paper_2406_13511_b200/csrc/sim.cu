@@ -254,14 +254,15 @@ __device__ __forceinline__ int argmin_event_redux(double t, unsigned long long s
   return w;
 }
 
-// Stable LSD radix sort of n (key, val) pairs on key bits [0, bits), warp-wide,
+// Stable LSD radix sort of n (key, val) pairs on key bits [lo, bits), warp-wide,
 // ping-ponging between (k, v) and (k2, v2).  Returns true when the result is
-// in (k2, v2).  bins: 256 ints of this warp's shared memory.
+// in (k2, v2).  bins: 256 ints of this warp's shared memory.  Bits below `lo`
+// ride along (a payload packed under the sort key).
 __device__ bool warp_radix_sort(int n, uint64_t* k, int32_t* v, uint64_t* k2, int32_t* v2, int bits,
-                                int lane, int32_t* bins) {
+                                int lane, int32_t* bins, int lo = 0) {
   bool swapped = false;
   const unsigned lt = (1u << lane) - 1u;
-  for (int shift = 0; shift < bits; shift += 8) {
+  for (int shift = lo; shift < bits; shift += 8) {
     const uint32_t mask = bits - shift >= 8 ? 0xffu : ((1u << (bits - shift)) - 1u);
     for (int i = lane; i < 256; i += 32) bins[i] = 0;
     __syncwarp();
@@ -439,10 +440,11 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   int32_t* gen = (int32_t*)(base + Lay.gen);
   int32_t* sl = (int32_t*)(base + Lay.sl);
   double* resp = (double*)(base + Lay.resp);
-  for (int i = lane; i < n; i += 32) {
-    gen[i] = 0;
-    sl[i] = 0;
-  }
+  if (POL != SCLS_POLICY_SCLS)
+    for (int i = lane; i < n; i += 32) {
+      gen[i] = 0;
+      sl[i] = 0;
+    }
 
   Sink<kHash, kLog> sink;
   sink.init(logging ? P.recs + (int64_t)t * P.rec_cap : nullptr,
@@ -465,13 +467,18 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   long long total_pad = 0, total_inv = 0, batch_count = 0, batch_members = 0, early = 0;
   double tick_t = dinf();
   unsigned long long tick_s = ~0ull;
-  int pool_len = 0, tl_pos = 0;
+  int pool_len = 0, tl_pos = 0, arr_lo = 0;
   int pf_head = 0, pf_tail = 0;  // SLS policy FIFO
   int err_req = -1;
   status = SCLS_OK;
 
   // Policy-specific arena views.
-  int32_t* pool = (int32_t*)(base + Lay.pool);
+  int32_t* pool = (int32_t*)(base + Lay.pool);  // SCLS pool records: id, eff, generated, true gen, slices, arrival
+  int32_t* p_eff = (int32_t*)(base + Lay.p_eff);
+  int32_t* p_g = (int32_t*)(base + Lay.p_g);
+  int32_t* p_t = (int32_t*)(base + Lay.p_t);
+  int32_t* p_s = (int32_t*)(base + Lay.p_s);
+  double* p_a = (double*)(base + Lay.p_a);
   uint64_t* sk = (uint64_t*)(base + Lay.sk);
   uint64_t* sk2 = (uint64_t*)(base + Lay.sk2);
   int32_t* sv = (int32_t*)(base + Lay.sv);
@@ -604,70 +611,94 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   // ---- the SCLS tick (sched_policies.cpp:90-147) ------------------------------------
   auto scls_tick = [&]() -> int {
     int nb = 0;
-    const int P_ = pool_len;
+    // the pool: repooled records [0, pool_len), then the arrivals since the
+    // last tick, ids [arr_lo, cur), whose state is their input row
+    const int n_rec = pool_len, a_lo = arr_lo;
+    const int P_ = pool_len + (cur - arr_lo);
+    arr_lo = cur;
     if (P_ > 0) {
-      // 1. order the pool by (eff, id); ids are arrival ranks (sim_engine.cpp:110-114)
+      // 1. order the pool by (eff, id); ids are arrival ranks (sim_engine.cpp:110-114).
+      //    key = eff << (idb + pb) | id << pb | pool slot: the slot rides under
+      //    the sort key, so the rows pass reads each request's record from the
+      //    pool (written contiguously at arrival / repooling) instead of
+      //    chasing per-request arrays by id.
       const int idb = bits_of((uint32_t)max(n - 1, 1));
+      const int pb = bits_of((uint32_t)max(P_ - 1, 1));
+      // eff <= Lmax; the slot fits under the key for any n < 2^20 (huge traces
+      // sort a slot array alongside)
+      const bool packed = idb + pb + bits_of((uint32_t)P.Lmax) <= 64;
+      const int sh = packed ? pb : 0;
+      int32_t* slot_v = segs;      // free until the backtrack
+      int32_t* slot_v2 = split_g;  // free until the DP
       uint32_t emax = 0;
-      // four rows per lane per trip, every load issued before any use: the
-      // pool and request arrays are L2 / DRAM resident, so memory-level
-      // parallelism, not issue, bounds this loop
       for (int i0 = lane; i0 < P_; i0 += 32 * kKeysU) {
-        int id[kKeysU];
-#pragma unroll
-        for (int u = 0; u < kKeysU; ++u) id[u] = i0 + 32 * u < P_ ? pool[i0 + 32 * u] : 0;
-        int ip[kKeysU], gn[kKeysU];
+        int id[kKeysU], e[kKeysU];
 #pragma unroll
         for (int u = 0; u < kKeysU; ++u) {
-          ip[u] = i0 + 32 * u < P_ ? inp[id[u]] : 0;
-          gn[u] = i0 + 32 * u < P_ ? gen[id[u]] : 0;
+          const int i = i0 + 32 * u;
+          id[u] = i < n_rec ? pool[i] : a_lo + (i - n_rec);
+          e[u] = i < n_rec ? p_eff[i] : (i < P_ ? inp[id[u]] : 0);
         }
 #pragma unroll
         for (int u = 0; u < kKeysU; ++u) {
-          if (i0 + 32 * u < P_) {
-            const uint32_t e = (uint32_t)(ip[u] + gn[u]);
-            emax = max(emax, e);
-            sk[i0 + 32 * u] = ((uint64_t)e << idb) | (uint64_t)id[u];
+          const int i = i0 + 32 * u;
+          if (i < P_) {
+            emax = max(emax, (uint32_t)e[u]);
+            sk[i] = ((uint64_t)e[u] << (idb + sh)) | ((uint64_t)id[u] << sh) | (packed ? (uint64_t)i : 0ull);
+            if (!packed) slot_v[i] = i;
           }
         }
       }
       emax = __reduce_max_sync(FULL, emax);
+      const int top = idb + sh + bits_of(emax);
       __syncwarp();
       SIM_PROF(2);
-      const bool sw = warp_radix_sort(P_, sk, nullptr, sk2, nullptr, idb + bits_of(emax), lane, bins);
+      const bool sw = packed ? warp_radix_sort(P_, sk, nullptr, sk2, nullptr, top, lane, bins, sh)
+                             : warp_radix_sort(P_, sk, slot_v, sk2, slot_v2, top, lane, bins);
       const uint64_t* keys = sw ? sk2 : sk;
+      const int32_t* slots = sw ? slot_v2 : slot_v;
       SIM_PROF(3);
+      const int kb_id = sh;  // id field position in the sorted key
       const uint64_t idmask = (1ull << idb) - 1ull;
-      // 2. rows: L, singleton feasibility (batcher.cpp:40-46)
+      const uint64_t pmask = (1ull << pb) - 1ull;
+      // 2. rows: the batched state of every member, L, K(L) and its cost row,
+      //    singleton feasibility (batcher.cpp:40-46)
       int bad = 0x7fffffff;
       for (int i0 = lane; i0 < P_; i0 += 32 * kRowsU) {  // kRowsU rows per lane per trip, loads first
         uint64_t key[kRowsU];
+        int q[kRowsU];
 #pragma unroll
-        for (int u = 0; u < kRowsU; ++u) key[u] = i0 + 32 * u < P_ ? keys[i0 + 32 * u] : 0ull;
+        for (int u = 0; u < kRowsU; ++u) {
+          const bool ok = i0 + 32 * u < P_;
+          key[u] = ok ? keys[i0 + 32 * u] : 0ull;
+          q[u] = packed ? (int)(key[u] & pmask) : (ok ? slots[i0 + 32 * u] : 0);
+        }
         int id[kRowsU], L[kRowsU], g_[kRowsU], t_[kRowsU], s_[kRowsU], k_[kRowsU];
         double a_[kRowsU];
 #pragma unroll
         for (int u = 0; u < kRowsU; ++u) {
           const bool ok = i0 + 32 * u < P_;
-          id[u] = (int)(key[u] & idmask);
-          L[u] = (int)(key[u] >> idb);
-          g_[u] = ok ? gen[id[u]] : 0;
-          t_[u] = ok ? tg[id[u]] : 0;
-          s_[u] = ok ? sl[id[u]] : 0;
-          a_[u] = ok ? arr[id[u]] : 0.0;
-          k_[u] = ok && L[u] <= P.Lmax ? Kt[L[u]] : 0;
+          id[u] = (int)((key[u] >> kb_id) & idmask);
+          L[u] = (int)(key[u] >> (kb_id + idb));
+          // a repooled record, or a fresh arrival (slot >= n_rec: its input row)
+          const bool rec = ok && q[u] < n_rec;
+          g_[u] = rec ? p_g[q[u]] : 0;
+          t_[u] = rec ? p_t[q[u]] : (ok ? tg[id[u]] : 0);
+          s_[u] = rec ? p_s[q[u]] : 0;
+          a_[u] = rec ? p_a[q[u]] : (ok ? arr[id[u]] : 0.0);
+          k_[u] = ok && L[u] <= P.Lmax ? __ldg(Kt + L[u]) : 0;
         }
 #pragma unroll
         for (int u = 0; u < kRowsU; ++u) {
           const int i = i0 + 32 * u;
           if (i < P_) {
-            const int64_t q = tl_pos + i;
-            tlog[q] = id[u];
-            tl_g[q] = g_[u];
-            tl_t[q] = t_[u];
-            tl_e[q] = L[u];
-            tl_s[q] = s_[u];
-            tl_a[q] = a_[u];
+            const int64_t qq = tl_pos + i;
+            tlog[qq] = id[u];
+            tl_g[qq] = g_[u];
+            tl_t[qq] = t_[u];
+            tl_e[qq] = L[u];
+            tl_s[qq] = s_[u];
+            tl_a[qq] = a_[u];
             sv[i] = L[u];
             if (L[u] > P.Lmax || k_[u] == 0) bad = min(bad, i);
           }
@@ -694,6 +725,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       __syncwarp();
       const double kInf = dinf();
       for (int tb = 0; tb < P_; tb += 32) {
+        SIM_PROF(5);
         const int r = tb + 1 + lane;
         const bool valid = r <= P_;
         const int L = valid ? sv[r - 1] : 0;
@@ -735,6 +767,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
             }
           }
         }
+        SIM_PROF(11);  // tile setup + far candidates (the rest of the tile goes to slot 5)
         if (C.mono) {
           // decision rounds (dp_mono.cuh): with T[0..a] final, a pending row
           // whose best candidate from sources <= a is strictly below
@@ -920,19 +953,19 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       int id = 0, eff = 0, g = 0, pad = 0, inv = 0, s1 = 0;
       double ta = 0.0;
       bool done = false;
+      int ng = 0, tgv = 0;
       if (ok) {
         const int q = bst + i;
         id = tlog[q];
-        const int gsf = tl_g[q], tgv = tl_t[q];
+        const int gsf = tl_g[q];
+        tgv = tl_t[q];
         eff = tl_e[q];
         s1 = tl_s[q] + 1;
-        if (one) ta = tl_a[q];
+        ta = tl_a[q];
         g = min(tgv - gsf, served);
         pad = lin - eff;
         inv = served - g;
-        const int ng = gsf + g;
-        gen[id] = ng;
-        sl[id] = s1;
+        ng = gsf + g;
         done = ng >= tgv || ng >= C.G;
       }
       const int cnt = min(32, bn - b0);
@@ -941,7 +974,15 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       total_inv += __reduce_add_sync(FULL, ok ? inv : 0);
       const unsigned fm = __ballot_sync(FULL, ok && done);
       const unsigned pm = __ballot_sync(FULL, ok && !done);
-      if (ok && !done) pool[pool_len + __popc(pm & lt)] = id;
+      if (ok && !done) {  // repooled in member order with its record (sched_policies.cpp:176-181)
+        const int d = pool_len + __popc(pm & lt);
+        pool[d] = id;
+        p_eff[d] = eff + g;
+        p_g[d] = ng;
+        p_t[d] = tgv;
+        p_s[d] = s1;
+        p_a[d] = ta;
+      }
       pool_len += __popc(pm);
       if (one) {
         const int cnt = __popc(fm);
@@ -1251,10 +1292,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           if (run < 32) break;
         }
         if (first_arrival == dinf()) first_arrival = arr[cur];
-        for (int c0 = 0; c0 < cnt; c0 += 32) {
-          const int i = cur + c0 + lane;
-          if (c0 + lane < cnt) pool[pool_len + c0 + lane] = i;
-        }
+
         if (kHash || kLog) {
           for (int i = 0; i < cnt; ++i) {
             const int id = cur + i;
@@ -1264,8 +1302,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           sink.n_events += cnt;
         }
         clock = arr[cur + cnt - 1];
-        pool_len += cnt;
-        cur += cnt;
+        cur += cnt;  // pooled as the id range [arr_lo, cur) until the next tick
         next_arr = cur < n ? arr[cur] : dinf();
         __syncwarp();
         SIM_PROF(1);

@@ -10,6 +10,7 @@ namespace scls {
 struct SimLayout {
   int64_t gen, sl, resp;                                  // per request
   int64_t pool, sk, sk2, sv, T, split, segs, tlog;        // SCLS tick
+  int64_t p_eff, p_g, p_t, p_s, p_a;                      // SCLS pool records
   int64_t b_start, b_n, b_lin, b_served, b_next, b_est;   // SCLS batches
   int64_t tl_g, tl_t, tl_e, tl_s, tl_a;                   // SCLS slot state
   int64_t fifo, pf_t, pf_seq, pf_w, run, ex;              // SLS / ILS
@@ -32,11 +33,21 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
   };
   const int64_t n1 = n + 1;
   const int64_t cap_w = W > 0 ? (n + W - 1) / W : 0;
-  L.gen = take(4 * n1);
-  L.sl = take(4 * n1);
+  // per-request progress; SCLS carries it in its pool records instead
+  L.gen = take(policy == SCLS_POLICY_SCLS ? 0 : 4 * n1);
+  L.sl = take(policy == SCLS_POLICY_SCLS ? 0 : 4 * n1);
   L.resp = take(8 * n1);
   if (policy == SCLS_POLICY_SCLS) {
+    // Repooled requests carry their whole record (id, effective input,
+    // generated, true gen, slices, arrival), written contiguously at batch
+    // completion, so a tick never chases per-request arrays by id; fresh
+    // arrivals are the id range since the last tick (their input rows).
     L.pool = take(4 * n1);
+    L.p_eff = take(4 * n1);
+    L.p_g = take(4 * n1);
+    L.p_t = take(4 * n1);
+    L.p_s = take(4 * n1);
+    L.p_a = take(8 * n1);
     L.sk = take(8 * n1);
     L.sk2 = take(8 * n1);
     L.sv = take(4 * n1);
