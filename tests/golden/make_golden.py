@@ -1,7 +1,8 @@
 """Generate the committed golden fixtures from the UNMODIFIED reference.
 
 Run in the build container (where /root/reference exists):
-    make -C oracle ref && python tests/golden/make_golden.py
+    make -C oracle ref && python tests/golden/make_golden.py          # golden.json
+    python tests/golden/make_golden.py --large                        # golden_large.json
 
 Every number here comes from oracle/_ref/libscls_ref.so, i.e. the reference
 core compiled from /root/reference/proj/core/src (oracle/Makefile).  The
@@ -147,5 +148,33 @@ def main():
     print("wrote", path)
 
 
+def main_large():
+    """C3-style pools beyond 2^20 (bench_batcher.cpp make_pool, seed 7, S = 128):
+    n = 2^22 and 2^24 under the analytic KV cap and the rule table, batches
+    fingerprinted, then offloaded onto 8 workers at load 0."""
+    ref = RefLib(REF_SO)
+    orc = OracleLib(ORACLE_SO)
+    lat = capi.builtin_latency_model()
+    out = {"source": "oracle/_ref/libscls_ref.so built from /root/reference/proj/core/src",
+           "pools": []}
+    for n in (1 << 22, 1 << 24):
+        eff, arr, ids, _ = orc.make_pool(n, 7)
+        for mname in ("analytic", "rule"):
+            res = ref.batch_requests(eff, arr, ids, 128, lat, MEMORIES[mname]())
+            rec = dict(n=n, seed=7, slice_len=128, memory=mname, pool=sha(eff) + sha(arr))
+            rec.update(batch_record(res))
+            ob, ow, nl = ref.offload(res["batch_id"], res["est"], np.arange(8, dtype=np.int32), [0.0] * 8)
+            rec.update(assign_batch=sha(ob), assign_worker=sha(ow), final_loads=[fx(x) for x in nl])
+            out["pools"].append(rec)
+            print("large", n, mname, rec["n_batches"], rec["sum_est_dec"], flush=True)
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_large.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote", path)
+
+
 if __name__ == "__main__":
-    main()
+    if "--large" in sys.argv:
+        main_large()
+    else:
+        main()

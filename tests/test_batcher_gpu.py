@@ -252,3 +252,29 @@ def test_decision_kernel_forced_small_windows(ctx, orc, golden):
             assert sha(res["est"].astype(np.float64)) == case["est"]
     finally:
         ctx.set_dp_kernel(0)
+
+
+@pytest.mark.gpu
+def test_golden_large_pools(ctx, orc):
+    """Pools of 2^22 and 2^24 requests (the north star's ">= 1M-request
+    pools"): batches and the 8-worker offload vs the reference's fingerprints
+    (tests/golden/golden_large.json, make_golden.py --large)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_large.json")
+    lat = capi.builtin_latency_model()
+    for case in json.load(open(path))["pools"]:
+        eff, arr, ids, _ = orc.make_pool(case["n"], case["seed"])
+        assert sha(eff) + sha(arr) == case["pool"]
+        r = ctx.schedule(eff, arr, ids, case["slice_len"], lat, MEMORIES[case["memory"]](),
+                         np.arange(8, dtype=np.int32), [0.0] * 8)
+        msg = (case["n"], case["memory"])
+        assert r["n_batches"] == case["n_batches"], msg
+        assert float(planned_total(r["est"])).hex() == case["sum_est"], msg
+        assert sha(r["seg_begin"].astype(np.int32)) == case["seg"], msg
+        assert sha(r["l_in"].astype(np.int32)) == case["l_in"], msg
+        assert sha(r["est"].astype(np.float64)) == case["est"], msg
+        assert sha(r["member_id"].astype(np.int64)) == case["member"], msg
+        assert sha(r["assign_batch"]) == case["assign_batch"], msg
+        assert sha(r["assign_worker"]) == case["assign_worker"], msg
+        assert [float(x).hex() for x in r["loads"]] == case["final_loads"], msg

@@ -490,3 +490,33 @@ def test_packed_jobs_mixed_outcomes(ctx, orc, pol):
                     assert getattr(a[c][t], f) == getattr(b[t], f), (c, t, f, getattr(a[c][t], f), getattr(b[t], f))
         assert np.array_equal(ha[c], hb), c
     assert len(statuses) >= 3, statuses  # ok, error and non-termination all occurred
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_sweep_600s_regime_vs_reference(ctx, ref):
+    """The headline's regime (bench.py / BASELINE configs[4]): 600 s traces at
+    rates 10-25 req/s, 8 instances, S = 128, generated on the device, under
+    SCLS / SLS / ILS with the metrics-only kernels the sweep uses (independent
+    ILS / SLS lanes, two-job ILS packs), against the reference's own sweep
+    body (generate + Simulator::run + compute) on the host: every job, every
+    report field, the slice histogram and the counters.  Fresh seeds (not the
+    bench's), plus 4- and 16-instance configs."""
+    import os
+    T = 384
+    specs = [capi.workload_spec(rate=(10.0, 15.0, 20.0, 25.0)[i % 4], duration_s=600.0, seed=70000 + i)
+             for i in range(T)]
+    lat, mem = capi.builtin_latency_model(), MEMORIES["rule"]()
+    cfgs = [capi.sched_cfg(policy=p, worker_count=w) for w in (8, 4, 16) for p in ("scls", "sls", "ils")]
+    ctx.set_digests(False)
+    try:
+        got, got_h = ctx.run_sweep(specs, cfgs, lat, mem, hist_bins=16)
+    finally:
+        ctx.set_digests(True)
+    want, want_h = ref.run_sweep(specs, cfgs, lat, mem, hist_bins=16, threads=os.cpu_count() or 1)
+    skip = ("sim_clock", "h_complete_ids", "h_dispatch", "h_complete_t", "h_log")
+    bad = [(j, f) for j in range(len(cfgs) * T) for f, _ in capi.TraceResult._fields_
+           if f not in skip and getattr(got[j], f) != getattr(want[j], f)]
+    assert not bad, bad[:10]
+    assert np.array_equal(got_h, want_h)
+    assert all(got[j].status == 0 for j in range(len(cfgs) * T))
