@@ -15,7 +15,10 @@
 #include "scls_capi.h"
 #include "slicesim/cost_model.h"
 #include "slicesim/errors.h"
+#include "slicesim/event_log.h"
 #include "slicesim/memory_model.h"
+#include "slicesim/metrics.h"
+#include "slicesim/request.h"
 #include "slicesim/sched_policies.h"
 
 namespace slicesim {
@@ -37,6 +40,24 @@ scls_multi* multi();
 inline void check(scls_ctx* ctx, scls_status st) {
   if (st != SCLS_OK) raise(ctx, st);
 }
+
+// One run with its full device event log (device_run.cpp): the workload is
+// generated on the device from `spec` (uniform / histogram lengths), or
+// taken from `workload`.  Throws only for C-ABI failures; the run's own
+// status is in res (raise_status maps it onto the reference's exceptions).
+struct LoggedRun {
+  std::vector<scls_event_record> recs;
+  std::vector<scls_member> mems;
+  int64_t rc = 0, mc = 0;
+  scls_trace_result res{};
+  std::vector<int64_t> hist;
+};
+LoggedRun run_logged(const scls_sched_cfg& c, const scls_latency& lat, const scls_memory& mem, int32_t hist_bins,
+                     const scls_workload_spec* spec, const std::vector<Request>* workload);
+void raise_status(const LoggedRun& r, double horizon_s);
+EventLog to_event_log(const LoggedRun& r, int worker_count);
+MetricsReport to_report(const scls_trace_result& r, const int64_t* hist, int32_t hist_bins);
+int32_t report_hist_bins(const scls_sched_cfg& c);
 
 scls_latency to_c(const LatencyModel& m);
 scls_memory to_c(const MemoryModel& m);

@@ -93,14 +93,43 @@ scls_workload_spec to_c(const WorkloadSpec& w) {
 }  // namespace
 
 RunResult run_experiment(const RunConfig& cfg) {
+  // experiment.cpp:39-60: models -> workload -> Simulator::run -> compute.
+  // Uniform / histogram workloads are generated on the device
+  // (scls_run_experiments, bit-exact with generate()); the run's event log and
+  // its MetricsReport both come from the device (metrics.cpp:30-117 computed
+  // online, bit for bit), so neither generate() nor compute() runs on the
+  // host.  Trace files and log-normal lengths are loaded / generated on the host.
   const LatencyModel latency = resolve_latency_model(cfg.latency_model_path);
   const MemoryModel memory = resolve_memory_model(cfg.memory_model_path);
-  std::vector<Request> requests = load_workload(cfg);
-  Simulator sim(cfg.sched, latency, memory, cfg.horizon_s);
-  auto policy = make_scheduler(cfg.sched.policy);
+  std::vector<Request> requests;
+  scls_workload_spec spec{};
+  const bool on_dev = device_generated(cfg);
+  if (on_dev) {
+    validate(cfg.workload);  // generate()'s own check (workload.cpp:86-98), same exception
+    spec = to_c(cfg.workload);
+  } else {
+    requests = load_workload(cfg);
+  }
+  Simulator check_cfg(cfg.sched, latency, memory, cfg.horizon_s);  // constructor validation (sim_engine.cpp:32-35)
+  const scls_sched_cfg c = b200::to_c(cfg.sched, cfg.horizon_s);
+  const int32_t bins = b200::report_hist_bins(c);
   RunResult result;
-  result.log = sim.run(std::move(requests), *policy);
-  result.report = compute(result.log);
+  if (!on_dev) {
+    // Simulator::run's own preconditions (sim_engine.cpp:102-114) on the host-built workload
+    std::stable_sort(requests.begin(), requests.end(), [](const Request& a, const Request& b) {
+      if (a.arrival_time != b.arrival_time) return a.arrival_time < b.arrival_time;
+      return a.id < b.id;
+    });
+    for (std::size_t i = 0; i < requests.size(); ++i)
+      if (requests[i].id != static_cast<RequestId>(i))
+        throw Error("workload request ids must be 0..n-1 in arrival order");
+    if (requests.empty()) throw EmptyLogError("cannot compute metrics from an empty log");
+  }
+  const b200::LoggedRun r = b200::run_logged(c, b200::to_c(latency), b200::to_c(memory), bins,
+                                             on_dev ? &spec : nullptr, on_dev ? nullptr : &requests);
+  b200::raise_status(r, cfg.horizon_s);
+  result.log = b200::to_event_log(r, cfg.sched.worker_count);
+  result.report = b200::to_report(r.res, r.hist.data(), bins);
   return result;
 }
 
@@ -210,28 +239,15 @@ std::vector<SweepRow> sweep(const RunConfig& base, const std::string& param,
   for (std::size_t v = 0; v < nv; ++v) {
     if (early[v]) std::rethrow_exception(early[v]);
     const scls_trace_result& r = res[v];
-    if (r.status == SCLS_ERR_INFEASIBLE_REQUEST)
-      throw InfeasibleRequestError(r.error_request_id, "request " + std::to_string(r.error_request_id) +
-                                                           " does not fit memory even as a singleton batch");
-    if (r.status == SCLS_ERR_NON_TERMINATION) throw NonTerminationError("simulated clock reached horizon");
-    if (r.status == SCLS_ERR_EMPTY_LOG) throw EmptyLogError("cannot compute metrics from an empty log");
-    if (r.status != SCLS_OK) throw Error("device simulation failed with status " + std::to_string(r.status));
+    if (r.status != SCLS_OK) {
+      // the failing value re-runs alone with its event log, which raises the
+      // reference's exact exception and message (sim_engine.cpp:159-163, ...)
+      (void)run_experiment(with_value(base, param, values[v]));
+      throw Error("device simulation failed with status " + std::to_string(r.status));
+    }
     SweepRow& row = rows[v];
     row.value = values[v];
-    MetricsReport& m = row.report;
-    m.throughput = r.throughput;
-    m.avg_response_s = r.avg_response_s;
-    m.p95_response_s = r.p95_response_s;
-    m.ct_std_s = r.ct_std_s;
-    m.avg_pad_tokens = r.avg_pad_tokens;
-    m.avg_invalid_tokens = r.avg_invalid_tokens;
-    m.avg_batch_size = r.avg_batch_size;
-    m.early_return_ratio = r.early_return_ratio;
-    const double completed = static_cast<double>(r.completed);
-    for (int32_t s = 0; s < hist_bins; ++s) {
-      const int64_t c = hist[v * hist_bins + s];
-      if (c > 0) m.slice_count_hist[s] = static_cast<double>(c) / completed;
-    }
+    row.report = b200::to_report(r, hist.data() + v * hist_bins, hist_bins);
   }
   return rows;
 }

@@ -109,76 +109,14 @@ EventLog Simulator::run(std::vector<Request> workload, Scheduler& policy) {
   const int64_t n = static_cast<int64_t>(workload.size());
   requests_ = workload;
   if (n == 0) return std::move(log_);
-  std::vector<double> arr(n);
-  std::vector<int32_t> inp(n), gen(n);
-  for (int64_t i = 0; i < n; ++i) {
-    arr[i] = workload[i].arrival_time;
-    inp[i] = workload[i].orig_input_len;
-    gen[i] = workload[i].true_gen_len;
-  }
-  const int64_t offs[2] = {0, n};
   const scls_latency lat = b200::to_c(latency_);
   const scls_memory mem = b200::to_c(memory_);
-  scls_ctx* ctx = b200::context();
-  int64_t rec_cap = 6 * n + 64, mem_cap = 4 * n + 64;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    std::vector<scls_event_record> recs(rec_cap);
-    std::vector<scls_member> mems(mem_cap);
-    int64_t rc = 0, mc = 0;
-    scls_event_log lg{1, rec_cap, mem_cap, recs.data(), mems.data(), &rc, &mc};
-    scls_trace_result res{};
-    b200::check(ctx, scls_simulate(ctx, 1, offs, arr.data(), inp.data(), gen.data(), 1, &c, nullptr, &lat,
-                                   &mem, &res, 0, nullptr, &lg, SCLS_MEM_HOST));
-    if (rc > rec_cap || mc > mem_cap) {  // the device counts past capacity: resize once
-      rec_cap = rc;
-      mem_cap = mc;
-      continue;
-    }
-    if (res.status != SCLS_OK && res.status != SCLS_ERR_EMPTY_LOG) {
-      if (res.status == SCLS_ERR_INFEASIBLE_REQUEST)
-        throw InfeasibleRequestError(res.error_request_id,
-                                     "request " + std::to_string(res.error_request_id) +
-                                         " does not fit memory even as a singleton batch");
-      if (res.status == SCLS_ERR_NON_TERMINATION) {
-        // sim_engine.cpp:159-163; the device log holds every record up to EndOfRun
-        int64_t done = 0;
-        for (int64_t k = 0; k < std::min(rc, rec_cap); ++k) done += recs[k].kind == 5;
-        throw NonTerminationError("simulated clock reached horizon " + std::to_string(horizon_s_) + " s with " +
-                                  std::to_string(done) + " of " + std::to_string(n) + " requests completed");
-      }
-      throw Error("device simulation failed with status " + std::to_string(res.status));
-    }
-    log_.events.clear();
-    log_.events.reserve(static_cast<std::size_t>(rc));
-    for (int64_t k = 0; k < rc; ++k) {
-      const scls_event_record& r = recs[k];
-      EventRecord e;
-      e.t = r.t;
-      e.kind = static_cast<EventKind>(r.kind);
-      e.request = r.request;
-      e.worker = r.worker;
-      e.batch = r.batch;
-      e.n = r.n;
-      e.l_in = r.l_in;
-      e.planned_l_out = r.planned_l_out;
-      e.served_l_out = r.served_l_out;
-      e.est_serve_s = r.est_serve_s;
-      e.input_len = r.input_len;
-      e.gen_len = r.gen_len;
-      e.response_s = r.response_s;
-      e.slices = r.slices;
-      e.next_interval_s = r.next_interval_s;
-      for (int32_t j = 0; j < r.member_count; ++j) {
-        const scls_member& m = mems[r.member_offset + j];
-        e.members.push_back(MemberAccounting{m.request, m.effective_input, m.pad, m.gen, m.invalid});
-      }
-      log_.add(std::move(e));
-    }
-    replay(log_, c.policy, cfg_.max_gen_limit, requests_, workers_);
-    clock_ = res.sim_clock;
-    return std::move(log_);
-  }
-  throw Error("device event log capacity could not be established");
+  const b200::LoggedRun r = b200::run_logged(c, lat, mem, 0, nullptr, &workload);
+  if (r.res.status != SCLS_ERR_EMPTY_LOG) b200::raise_status(r, horizon_s_);  // compute() raises that one
+  log_ = b200::to_event_log(r, cfg_.worker_count);
+  replay(log_, c.policy, cfg_.max_gen_limit, requests_, workers_);
+  clock_ = r.res.sim_clock;
+  return std::move(log_);
 }
 
 }  // namespace slicesim

@@ -124,3 +124,25 @@ def test_cli_sweep_sharded_byte_identical(tmp_path, devices):
         assert p.returncode == 0, (tag, p.stderr[-2000:])
         outs[tag] = (d / "s.csv").read_bytes()
     assert outs["ref"] == outs["b200"] and len(outs["ref"]) > 0
+
+
+STRICT = [c for c in CASES if not c[0].startswith("gen_")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,args,files", STRICT, ids=[c[0] for c in STRICT])
+def test_cli_device_only_path(tmp_path, name, args, files):
+    """slicesim_b200_strict: the drop-in CLI with the reference's host
+    generate() and compute() poisoned (tests/refsuite/poison_host_path.cpp
+    aborts if either runs).  `run` and `sweep` on generated workloads still
+    write byte-identical reports, logs and CSVs: the workload is generated
+    and the report computed on the device."""
+    ref, strict = _require("slicesim_ref"), _require("slicesim_b200_strict")
+    outs = {}
+    for tag, exe in (("ref", ref), ("strict", strict)):
+        d = tmp_path / tag
+        d.mkdir()
+        p = subprocess.run([exe] + args.format(d=d).split(), capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, (tag, p.stderr[-2000:])
+        outs[tag] = {f: (d / f).read_bytes() for f in files}
+    assert outs["ref"] == outs["strict"], name
