@@ -94,6 +94,16 @@ __global__ void slot_to_worker_kernel(int64_t nb, const int32_t* __restrict__ sl
 
 constexpr int kChunk = 2048;
 
+// p ? a : b as an opaque selp, so the front end cannot turn a select over an
+// unrolled register array into an indexed (local-memory) access.
+__device__ __forceinline__ double select_if(bool p, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tselp.f64 %0, %2, %3, q;\n\t}"
+      : "=d"(r)
+      : "r"((unsigned)p), "d"(a), "d"(b));
+  return r;
+}
+
 // Thread 0 runs the serial greedy chain over the sorted estimates with the W
 // loads in registers and a log2(W)-deep comparison tree; warp 1 streams the
 // next chunk of estimates into shared memory meanwhile.
@@ -139,10 +149,14 @@ __global__ void __launch_bounds__(64) greedy_small_kernel(int64_t nb, const doub
             }
           }
         }
+        // every candidate sum is formed while the tree runs; the winner's is
+        // then selected -- no indexed update, so l[] stays in registers
         const double ei = e[i];
+        double nl[W];
 #pragma unroll
-        for (int w = 0; w < W; ++w)
-          if (w == bx[0]) l[w] = __dadd_rn(l[w], ei);
+        for (int w = 0; w < W; ++w) nl[w] = __dadd_rn(l[w], ei);
+#pragma unroll
+        for (int w = 0; w < W; ++w) l[w] = select_if(bx[0] == w, nl[w], l[w]);
         out_slot[base + i] = bx[0];
       }
     }
