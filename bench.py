@@ -261,6 +261,40 @@ def bench_c3(ctx, torch, lib, capi, stream, steps, warmup):
             "gpu_launches_per_call": launches // max(steps, 1)}
 
 
+def bench_scheduler_sweep(ctx, lib):
+    """Per-call latency of batch_requests across pool sizes: the reference's
+    own microbenchmark sizes (bench_batcher.cpp:44-57: make_pool(n, 7), S =
+    128, builtin rule-table memory, n = 16..4096) and 2^14..2^20.  Device time
+    (CUDA events, inputs resident), e2e through the C-ABI with host arrays
+    (H2D + D2H inside), and the compiled reference on one host core (the
+    reference API is one serial call), every result compared."""
+    lib_ref, kind = ref_checker()
+    lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
+    rows = []
+    for n in (16, 64, 256, 1024, 4096, 1 << 14, 1 << 16, 1 << 18, 1 << 20):
+        eff, arr, ids, _ = lib.make_pool(n, 7)
+        reps = 50 if n <= 4096 else (10 if n <= 1 << 16 else 3)
+        dev, e2e = [], []
+        for _ in range(reps + 2):
+            t0 = time.perf_counter()
+            r = ctx.batch_requests(eff, arr, ids, 128, lat, mem)
+            e2e.append(time.perf_counter() - t0)
+            dev.append(ctx.timings()["total"])
+        cpu = []
+        for _ in range(max(3, reps // 5)):
+            t0 = time.perf_counter()
+            w = lib_ref.batch_requests(eff, arr, ids, 128, lat, mem)
+            cpu.append(time.perf_counter() - t0)
+        same = (r["n_batches"] == w["n_batches"] and all(np.array_equal(r[k], w[k])
+                                                          for k in ("seg_begin", "l_in", "est", "member_id")))
+        dv, ev, cv = statistics.median(dev[2:]) * 1e3, statistics.median(e2e[2:]) * 1e6, statistics.median(cpu) * 1e6
+        rows.append({"n": n, "batches": int(r["n_batches"]), "device_us": round(dv, 1), "e2e_us": round(ev, 1),
+                     "cpu_us": round(cv, 1), "e2e_speedup": round(cv / ev, 2), "parity": "ok" if same else "MISMATCH",
+                     "path": "small (4 launches)" if n <= 4096 else "multi-kernel"})
+    return {"metric": "batch_requests latency per call", "memory": "rule table (builtin_memory_model)", "S": 128,
+            "cpu": f"{kind}, 1 host core", "rows": rows}
+
+
 def bench_configs(ctx, lib, capi, steps):
     """BASELINE configs[0], [1], [3] as latency lines next to the headline:
     C1 (1 instance, rate 2, 500 s, SCLS), C2 (8 instances, rate 20, 500 s, SCLS)
@@ -476,6 +510,7 @@ def run_ours(args, rank, world, dist):
     }
     if not args.no_c3:
         line["scheduler_c3"] = bench_c3(ctx, torch, lib, capi, stream, max(2, args.steps // 2), 2)
+        line["scheduler_sweep"] = bench_scheduler_sweep(ctx, lib)
         line["configs_c1_c2_c4"] = bench_configs(ctx, lib, capi, args.steps)
     if not args.no_cpu:
         cpu, parity = cpu_reference(args, T, cfgs, lat, mem, hist_bins, grid, grid_hist)

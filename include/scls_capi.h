@@ -135,7 +135,8 @@ int64_t scls_last_launch_count(const scls_ctx* ctx);
 /* Context options.  SCLS_OPT_SIM_DIGESTS (default 1): scls_simulate fills
  * the h_* log digests of scls_trace_result; 0 skips them (the metrics are
  * computed either way, and the digests are zero). */
-enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT = 3, SCLS_OPT_ILS_KERNEL = 4 };
+enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT = 3, SCLS_OPT_ILS_KERNEL = 4,
+       SCLS_OPT_BATCH_PATH = 5 };
 /* SCLS_OPT_DP_KERNEL: 0 (default) picks the monotone decision kernel when the
  * model allows it and some window exceeds 32 rows, else the serial-chain
  * kernel; 1 forces the chain kernel; 2 forces the decision kernel when the
@@ -146,7 +147,10 @@ enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT
  * sweep.  SCLS_OPT_ILS_KERNEL
  * (default 0): metrics-only ILS and SLS run every instance / worker in its own
  * lane and merge the completions (csrc/sim_indep.cuh); 1 forces the lock-step
- * kernels that process the global event order directly (results identical). */
+ * kernels that process the global event order directly (results identical).
+ * SCLS_OPT_BATCH_PATH (default 0): batch_requests / schedule take the fused
+ * four-launch small-pool path for n <= 4096 and the multi-kernel path above;
+ * 1 forces the multi-kernel path at every size (results identical). */
 scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value);
 /* Diagnostics: enable/disable clock64 phase counters in the DP chain kernel
  * and read-and-reset them (cycles: main chain, main barrier wait, helper

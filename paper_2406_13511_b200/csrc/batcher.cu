@@ -233,6 +233,7 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
   *nb_out = 0;
   if (n == 0) return SCLS_OK;
   if (n >= 0x7fffffffLL) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "pool larger than 2^31-1");
+  if (small_pool_eligible(n) && !trace && !ctx->force_large_path) return batch_requests_small(ctx, in, out, nb_out);
   const Lat lat = make_lat(*in.lat);
   const Mem mem = make_mem(*in.mem);
   const int threads = 256;
@@ -365,7 +366,7 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
                        !std::signbit(in.lat->d3) && !std::signbit(in.lat->d4);
   auto launch = [&](auto kern, size_t bytes) -> scls_status {
     SCLS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    kern<<<1, kDpThreads, bytes, s>>>((int32_t)n, Krow, cbase, cost, T, split, ctx->dp_prof);
+    kern<<<1, kDpThreads, bytes, s>>>((int32_t)n, Krow, cbase, cost, T, split, ctx->dp_prof, nullptr, 0);
     SCLS_LAUNCHED();
     return SCLS_OK;
   };

@@ -38,6 +38,11 @@ struct BatchTrace {
 scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const BatchOutputs& out,
                                   int64_t* nb_out, BatchTrace* trace);
 
+// Pools of up to 4096 requests: the same results in four launches and one
+// host read-back (small.cu).
+bool small_pool_eligible(int64_t n);
+scls_status batch_requests_small(scls_ctx* ctx, const BatchInputs& in, const BatchOutputs& out, int64_t* nb_out);
+
 // offloader.cpp:25-54 on device arrays; loads/worker ids on device, mutated
 // in place; outputs the assignment sequence.
 scls_status offload_device(scls_ctx* ctx, int64_t nb, const int64_t* batch_id, const double* est,

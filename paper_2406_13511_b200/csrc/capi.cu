@@ -233,6 +233,10 @@ scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value) {
     ctx->ils_lockstep = value != 0;
     return SCLS_OK;
   }
+  if (option == SCLS_OPT_BATCH_PATH) {
+    ctx->force_large_path = value != 0;
+    return SCLS_OK;
+  }
   return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "unknown option");
 }
 

@@ -29,6 +29,7 @@ struct scls_ctx {
   bool sim_concurrent = true;             // scls_simulate runs its per-policy launches concurrently
   bool ils_lockstep = false;              // metrics-only ILS: the lock-step kernel instead of independent lanes
   cudaStream_t side[3] = {};              // forked streams for those launches (created on first use)
+  bool force_large_path = false;          // batch_requests: the multi-kernel path even for small pools (tests)
   void* comm = nullptr;                   // ncclComm_t of scls_comm_init (multi.cu)
   int world = 1, rank = 0;
 

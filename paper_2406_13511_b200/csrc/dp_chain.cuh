@@ -54,7 +54,11 @@ template <bool kGlobalT, bool kIntCmp>
 __global__ void __launch_bounds__(kDpThreads, 1)
     dp_chain_kernel(int32_t n, const int32_t* __restrict__ Krow, const int32_t* __restrict__ cbase,
                     const double* __restrict__ cost, double* __restrict__ T,
-                    int32_t* __restrict__ split, unsigned long long* __restrict__ prof) {
+                    int32_t* __restrict__ split, unsigned long long* __restrict__ prof,
+                    const int32_t* __restrict__ gate = nullptr, int32_t gate_id = 0) {
+  // small-pool launches (small.cu) start both DP kernels; the one the device
+  // chose runs, the other returns
+  if (gate && *gate != gate_id) return;
   extern __shared__ __align__(16) unsigned char dp_smem_raw[];
   DpSmem& sm = *reinterpret_cast<DpSmem*>(dp_smem_raw);
   constexpr int M = kDpRing - 1;

@@ -67,7 +67,9 @@ template <bool kGlobalT>
 __global__ void __launch_bounds__(kDpThreads, 1)
     dp_mono_kernel(int32_t n, const int32_t* __restrict__ Krow, const int32_t* __restrict__ cbase,
                    const double* __restrict__ cost, double* __restrict__ T, int32_t* __restrict__ split,
-                   unsigned long long* __restrict__ prof) {
+                   unsigned long long* __restrict__ prof, const int32_t* __restrict__ gate = nullptr,
+                   int32_t gate_id = 0) {
+  if (gate && *gate != gate_id) return;  // small-pool launches: the DP kernel the device did not choose
   extern __shared__ __align__(16) unsigned char dp_smem_raw[];
   DpMonoSmem& sm = *reinterpret_cast<DpMonoSmem*>(dp_smem_raw);
   constexpr int M = kDpRing - 1;

@@ -194,6 +194,10 @@ class Context:
         """SCLS_OPT_ILS_KERNEL: 1 = the lock-step metrics-only ILS kernel, 0 = independent instance lanes."""
         self._check(self.lib.scls_set_option(self.h, 4, 1 if on else 0))
 
+    def set_batch_path(self, large):
+        """SCLS_OPT_BATCH_PATH: 1 forces the multi-kernel batch_requests path for small pools too."""
+        self._check(self.lib.scls_set_option(self.h, 5, 1 if large else 0))
+
     def set_dp_kernel(self, mode):
         """SCLS_OPT_DP_KERNEL: 0 auto (monotone decision kernel when allowed), 1 chain."""
         self._check(self.lib.scls_set_option(self.h, 2, int(mode)))

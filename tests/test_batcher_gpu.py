@@ -278,3 +278,40 @@ def test_golden_large_pools(ctx, orc):
         assert sha(r["assign_batch"]) == case["assign_batch"], msg
         assert sha(r["assign_worker"]) == case["assign_worker"], msg
         assert [float(x).hex() for x in r["loads"]] == case["final_loads"], msg
+
+
+@pytest.mark.gpu
+def test_small_pool_path_matches_large_path(ctx, orc):
+    """The fused small-pool path (csrc/small.cu, n <= 4096) against the
+    multi-kernel path and the C oracle: every size class, all memory models,
+    arrival ties, negative ids, an infeasible request."""
+    rng = np.random.default_rng(5)
+    lat = capi.builtin_latency_model()
+    sizes = (1, 2, 3, 31, 32, 33, 100, 460, 1000, 1500, 2048, 4031, 4032, 4033, 4095, 4096)
+    for n in sizes:
+        eff = rng.integers(1, 2048, n).astype(np.int32)
+        arr = np.round(rng.random(n) * 20, 1)  # ties
+        ids = rng.permutation(n).astype(np.int64) - n // 3
+        for mname in ("rule", "analytic", "tight"):
+            mem = MEMORIES[mname]()
+            try:
+                want = orc.batch_requests(eff, arr, ids, 128, lat, mem)
+            except Exception as e:  # infeasible under the tight model
+                with pytest.raises(lib_error()) as ei:
+                    ctx.batch_requests(eff, arr, ids, 128, lat, mem)
+                assert ei.value.request_id == e.request_id, (n, mname)
+                continue
+            small = ctx.batch_requests(eff, arr, ids, 128, lat, mem)
+            ctx.set_batch_path(True)
+            try:
+                large = ctx.batch_requests(eff, arr, ids, 128, lat, mem)
+            finally:
+                ctx.set_batch_path(False)
+            assert_same_batches(small, want, (n, mname, "small"))
+            assert_same_batches(large, want, (n, mname, "large"))
+            assert np.array_equal(small["order"], large["order"])
+
+
+def lib_error():
+    from paper_2406_13511_b200.lib import SclsError
+    return SclsError
