@@ -1727,9 +1727,25 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
       SCLS_LAUNCHED();
       scls_status st = scan_exclusive(ctx, Lmax + 1, need, off, off + Lmax + 1);
       if (st) return st;
-      int32_t tot = 0;
+      int32_t* d_kmax = (int32_t*)ctx->buf(kSlotSim + 29, sizeof(int32_t) * 2);
+      if (!d_kmax) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
+      SCLS_CUDA(cudaMemsetAsync(d_kmax, 0, sizeof(int32_t), s));
+      max_reduce_kernel<<<std::min(div_up(Lmax + 1, 256), ctx->sm_count * 8), 256, 0, s>>>(Lmax + 1, need, d_kmax);
+      SCLS_LAUNCHED();
+      int32_t tot = 0, kmax = 0;
       SCLS_CUDA(cudaMemcpyAsync(&tot, off + Lmax + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      SCLS_CUDA(cudaMemcpyAsync(&kmax, d_kmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       SCLS_CUDA(cudaStreamSynchronize(s));
+      // Tick DP variant: when every window fits one 32-row tile and the
+      // launch holds more SCLS jobs than there are SMs (a contended sweep),
+      // the in-tile chain issues less than the decision rounds (C5 sweep:
+      // ~1.5 ms of ~37 ms); a lightly loaded GPU keeps the rounds, whose
+      // per-trace latency is lower.
+      if (kmax <= 32 && ctx->dp_mode == 0) {
+        int64_t jobs = 0;
+        for (int t = 0; t < n_traces; ++t) jobs += (cfg_index ? h_idx[t] : 0) == c;
+        if (jobs > ctx->sm_count) hc[c].mono = 0;
+      }
       if (grand + tot > (1ll << 30)) return set_error(ctx, SCLS_ERR_CAPACITY, "simulator cost tables exceed 2^30 entries");
       totals[hc[c].table] = tot;
       // c(L, k) entries are written after the buffer is sized; remember the
@@ -1738,6 +1754,8 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
       SCLS_LAUNCHED();
       grand += tot;
     }
+    // the tick-DP variant may have changed per config (above)
+    SCLS_CUDA(cudaMemcpyAsync(d_cfg, hc.data(), sizeof(SimCfg) * n_cfgs, cudaMemcpyHostToDevice, s));
     d_cost = (double*)ctx->buf(kSlotSim + 12, sizeof(double) * (size_t)std::max<int64_t>(grand, 1));
     if (!d_cost) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
     const Lat dl = make_lat(*lat);
