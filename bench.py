@@ -253,8 +253,25 @@ def bench_c3(ctx, torch, lib, capi, stream, steps, warmup):
     tot = 0.0
     for e in r["est"]:
         tot += float(e)
+    peak, _ = peaks()
+
+    def hbm(bytes_per_req, ms):
+        gbs = bytes_per_req * n / (ms / 1e3) / 1e9 if ms else None
+        return {"bytes_per_request": bytes_per_req, "ms": ms, "achieved_gbs": gbs,
+                "frac": gbs / peak if gbs else None, "peak_gbs": peak}
+
+    # the sort and the estimator are HBM-shaped (24 B/request for
+    # the sort; the estimator reads the sorted key and writes a row's L / K:
+    # 16 B/request); the DP is the serial chain, reported in ns per row against
+    # the measured DADD+DSETP+SEL dependent-step floor (25.9 cycles @ 1965 MHz,
+    # tools/ubench_chain.cu) with the committed ncu issue counters.
+    dp = issue_line("dp_mono_kernel_1m", "dp_mono_kernel", n, "rows", ph["dp"])
+    dp["ns_per_row"] = ph["dp"] * 1e6 / n
+    dp["chain_floor_ns_per_row"] = 25.9 / 1.965
     return {"metric": "requests scheduled/s", "config": "C3: make_pool(2^20, 7), analytic KV cap, S=128, 8 workers",
             "value": n / (med / 1e3), "ms_per_call": med, "phases_ms": ph,
+            "hbm": {"sort": hbm(24, ph["sort"]), "estimate": hbm(16, ph["estimate"])},
+            "issue_efficiency": {"dp": dp},
             "e2e_value": n / statistics.median(e2e), "e2e_ms": statistics.median(e2e) * 1e3,
             "n_batches": int(nb), "sum_est": repr(tot),
             "parity": "ok" if (nb == 11820 and repr(tot) == "70831.31070040006") else "MISMATCH",

@@ -416,6 +416,11 @@ scls_status scls_multi_run_experiments(scls_multi* m, int32_t n_runs, const scls
 /* Diagnostics: the device port of glibc's log (csrc/glibc_log.cuh) on n
  * inputs, for the bit-exactness check against the host libm. */
 scls_status scls_debug_log(scls_ctx* ctx, int64_t n, const double* x, double* y, int32_t mem);
+/* The same for fn = 0 log, 1 exp, 2 cos (csrc/glibc_expcos.cuh: the FMA
+ * builds of glibc's exp and cos behind the log-normal lengths,
+ * workload.cpp:112-118,136-141; cos for |x| < 105414350, exp exact for
+ * |x| < 512 and +inf / +0 beyond). */
+scls_status scls_debug_libm(scls_ctx* ctx, int32_t fn, int64_t n, const double* x, double* y, int32_t mem);
 
 /* ---- workload: workload.h:78 generate ------------------------------------
  * Host-side Poisson trace generation (mt19937_64 + glibc log, the reference's

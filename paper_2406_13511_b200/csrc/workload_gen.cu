@@ -26,8 +26,8 @@
 // then are compacted into the contiguous req_offset layout the simulator
 // reads (scls_simulate, sim_engine.cpp:102-114: ids = arrival ranks).
 //
-// Log-normal lengths (exp, cos of glibc) are not ported: such specs fail with
-// SCLS_ERR_ERROR instead of being generated inexactly.
+// Log-normal lengths (Box-Muller, two outputs per draw) use bit-exact ports of
+// glibc's FMA `exp` and `cos` (csrc/glibc_expcos.cuh).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -36,6 +36,7 @@
 #include <vector>
 
 #include "ctx.h"
+#include "glibc_expcos.cuh"
 #include "glibc_log.cuh"
 #include "scls_capi.h"
 
@@ -72,10 +73,11 @@ __device__ __forceinline__ int uniform_int(int lo, int hi, uint64_t x) {
 
 __device__ __forceinline__ int clamp_len(int v, int limit) { return v < 1 ? 1 : (v > limit ? limit : v); }
 
-// sample_length (workload.cpp:133-161) for the uniform and histogram kinds;
-// w points at this request's outputs for the distribution.
+// sample_length (workload.cpp:133-161); w points at this request's outputs
+// for the distribution.
 __device__ __forceinline__ int sample_len(const scls_length_dist& d, int limit, const uint64_t* w) {
   if (d.kind == SCLS_DIST_UNIFORM) return clamp_len(uniform_int(d.lo, d.hi, w[0]), limit);
+  if (d.kind == SCLS_DIST_LOGNORMAL) return scls_glibc::lognormal_length(d.mu, d.sigma, d.cap, limit, w[0], w[1]);
   const double u = unit(w[0]);
   double cdf = 0.0;
   int bucket = d.n_buckets - 1;
@@ -89,6 +91,8 @@ __device__ __forceinline__ int sample_len(const scls_length_dist& d, int limit, 
   return clamp_len(uniform_int(d.edges[bucket], d.edges[bucket + 1], w[1]), limit);
 }
 
+// engine outputs per draw: uniform 1; histogram (bucket, value) and
+// log-normal (Box-Muller u1, u2: workload.cpp:112-118) 2
 __device__ __forceinline__ int draws(const scls_length_dist& d) { return d.kind == SCLS_DIST_UNIFORM ? 1 : 2; }
 
 __global__ void __launch_bounds__(kGenWarps * 32)
@@ -205,9 +209,10 @@ __global__ void compact_kernel(int32_t n, const int64_t* __restrict__ cap_off, c
 }
 
 // Device copy of the ported log, for the bit-exactness test against libm.
-__global__ void log_kernel(int64_t n, const double* __restrict__ x, double* __restrict__ y) {
+// fn: 0 log, 1 exp, 2 cos (the device ports, for the bit-exactness checks)
+__global__ void libm_kernel(int32_t fn, int64_t n, const double* __restrict__ x, double* __restrict__ y) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = scls_glibc::log_fma(x[i]);
+    y[i] = fn == 0 ? scls_glibc::log_fma(x[i]) : fn == 1 ? scls_glibc::exp_fma(x[i]) : scls_glibc::cos_fma(x[i]);
 }
 
 }  // namespace
@@ -221,9 +226,6 @@ scls_status generate_device(scls_ctx* ctx, int32_t n_specs, const scls_workload_
   for (int t = 0; t < n_specs; ++t) {
     scls_status st = validate_workload_spec(ctx, specs[t]);
     if (st) return st;
-    if (specs[t].input_len_dist.kind == SCLS_DIST_LOGNORMAL || specs[t].gen_len_dist.kind == SCLS_DIST_LOGNORMAL)
-      return set_error(ctx, SCLS_ERR_ERROR,
-                       "device generator: log-normal lengths are not supported (glibc exp/cos not ported)");
     if (!(specs[t].rate * specs[t].duration_s < 1e9))
       return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "device generator: rate * duration must be < 1e9");
   }
@@ -328,9 +330,15 @@ extern "C" scls_status scls_generate_batch(scls_ctx* ctx, int32_t n_specs, const
 }
 
 extern "C" scls_status scls_debug_log(scls_ctx* ctx, int64_t n, const double* x, double* y, int32_t mem) {
+  return scls_debug_libm(ctx, 0, n, x, y, mem);
+}
+
+extern "C" scls_status scls_debug_libm(scls_ctx* ctx, int32_t fn, int64_t n, const double* x, double* y,
+                                       int32_t mem) {
   if (!ctx) return set_error(nullptr, SCLS_ERR_INVALID_ARGUMENT, "null context");
   SCLS_CUDA(cudaSetDevice(ctx->device));
-  if (n < 0 || (n > 0 && (!x || !y))) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (fn < 0 || fn > 2 || n < 0 || (n > 0 && (!x || !y)))
+    return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad arguments");
   if (n == 0) return SCLS_OK;
   cudaStream_t s = ctx->stream;
   const double* dx = x;
@@ -342,7 +350,7 @@ extern "C" scls_status scls_debug_log(scls_ctx* ctx, int64_t n, const double* x,
     dx = b;
     dy = b + n;
   }
-  log_kernel<<<std::min(div_up(n, 256), ctx->sm_count * 8), 256, 0, s>>>(n, dx, dy);
+  libm_kernel<<<std::min(div_up(n, 256), ctx->sm_count * 8), 256, 0, s>>>(fn, n, dx, dy);
   SCLS_LAUNCHED();
   if (mem == SCLS_MEM_HOST) SCLS_CUDA(cudaMemcpyAsync(y, dy, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
   SCLS_CUDA(cudaStreamSynchronize(s));

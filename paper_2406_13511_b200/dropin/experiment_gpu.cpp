@@ -4,10 +4,10 @@
 // (experiment.h:52-53) is the data-parallel entry point: instead of one run
 // after another it builds every run of the sweep and simulates all of them
 // in ONE call (one warp per trace), reading the reports the device computes
-// online (metrics.cpp:30-117, bit for bit).  Generated workloads with uniform
-// or histogram lengths are generated on the device too (scls_run_experiments,
-// bit-exact with generate()); trace files and log-normal lengths are loaded /
-// generated on the host and simulated with scls_simulate.  Errors surface in
+// online (metrics.cpp:30-117, bit for bit).  Generated workloads (uniform,
+// log-normal and histogram lengths) are generated on the device too
+// (scls_run_experiments, bit-exact with generate()); only trace files are
+// loaded on the host and simulated with scls_simulate.  Errors surface in
 // value order, as the sequential reference would raise them.
 #include <algorithm>
 #include <cmath>
@@ -57,8 +57,7 @@ RunConfig with_value(const RunConfig& base, const std::string& param, double val
 bool device_generated(const RunConfig& cfg) {
   const WorkloadSpec& w = cfg.workload;
   auto ok = [](const LengthDist& d) {
-    return d.kind == LengthDist::Kind::kUniform ||
-           (d.kind == LengthDist::Kind::kHistogram && d.weights.size() <= SCLS_MAX_BUCKETS);
+    return d.kind != LengthDist::Kind::kHistogram || d.weights.size() <= SCLS_MAX_BUCKETS;
   };
   return !cfg.workload_from_trace && ok(w.input_len_dist) && ok(w.gen_len_dist);
 }

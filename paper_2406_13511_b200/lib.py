@@ -33,7 +33,7 @@ EXPORTS = [
     "scls_batch_serve_time", "scls_would_oom", "scls_max_batch_size",
     "scls_batch_requests", "scls_offload", "scls_schedule", "scls_simulate",
     "scls_simulate_grid", "scls_generate", "scls_make_pool", "scls_debug_dp_profile", "scls_set_option",
-    "scls_run_sweep", "scls_run_experiments", "scls_generate_batch", "scls_debug_log",
+    "scls_run_sweep", "scls_run_experiments", "scls_generate_batch", "scls_debug_log", "scls_debug_libm",
     "scls_shard_range", "scls_comm_unique_id", "scls_comm_init", "scls_comm_size", "scls_run_sweep_sharded",
     "scls_multi_create", "scls_multi_destroy", "scls_multi_last_error", "scls_multi_uses_nccl",
     "scls_multi_run_sweep", "scls_multi_run_experiments", "scls_device_count",
@@ -97,6 +97,7 @@ def load():
                                        P(capi.TraceResult), i32, vp, P(capi.EventLog), i32]),
         "scls_generate_batch": (i32, [vp, i32, P(capi.WorkloadSpec), i64, vp, vp, vp, vp, i32]),
         "scls_debug_log": (i32, [vp, i64, vp, vp, i32]),
+        "scls_debug_libm": (i32, [vp, i32, i64, vp, vp, i32]),
         "scls_shard_range": (None, [i64, i32, i32, P(i64), P(i64)]),
         "scls_comm_unique_id": (i32, [vp]),
         "scls_comm_init": (i32, [vp, i32, i32, vp]),
@@ -471,6 +472,14 @@ class Context:
         x = np.ascontiguousarray(x, np.float64)
         y = np.zeros_like(x)
         self._check(self.lib.scls_debug_log(self.h, len(x), _ptr(x), _ptr(y), capi.MEM_HOST))
+        return y
+
+    def debug_libm(self, fn, x):
+        """The device port of glibc log / exp / cos (fn = "log" | "exp" | "cos") on x."""
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros_like(x)
+        code = {"log": 0, "exp": 1, "cos": 2}[fn]
+        self._check(self.lib.scls_debug_libm(self.h, code, len(x), _ptr(x), _ptr(y), capi.MEM_HOST))
         return y
 
 

@@ -68,6 +68,12 @@ CASES = [
     ("sweep_workers_wide_sls", "sweep --param workers --values 40,200 --set policy.kind=sls --set workload.rate=120 "
      "--set workload.duration=40 --out {d}/s.csv", ["s.csv"]),
     ("gen_workload", "gen-workload --set workload.duration=60 --out {d}/t.csv", ["t.csv"]),
+    # log-normal lengths: generated on the device (csrc/glibc_expcos.cuh)
+    ("run_lognormal", "run --set workload.input_dist=lognormal:6.0:0.9:3000 "
+     "--set workload.gen_dist=lognormal:5.0:1.1:1024 --set workload.duration=150 "
+     "--report {d}/r.json --event-log {d}/e.jsonl", ["r.json", "e.jsonl"]),
+    ("sweep_rate_lognormal", "sweep --param rate --values 5,15,25 --set workload.gen_dist=lognormal:4.8:1.3:2048 "
+     "--set workload.duration=120 --set policy.kind=ils --out {d}/s.csv", ["s.csv"]),
 ]
 
 

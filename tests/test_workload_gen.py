@@ -1,10 +1,12 @@
 """Device trace generation: generate() on the B200,
 bit-exact with the reference's sampler (workload.cpp:100-181).
 
-CPU tests pin the ingredient the device cannot take from the reference: the
-port of glibc 2.39's FMA-variant `log` (csrc/glibc_log.cuh, constants from
-tools/extract_glibc_log.py), compiled for the host and compared bit for bit
-with this image's libm over 30M inputs.  GPU tests compare the device port
+CPU tests pin the ingredients the device cannot take from the reference: the
+ports of glibc 2.39's FMA-variant `log` (csrc/glibc_log.cuh, constants from
+tools/extract_glibc_log.py) and `exp` / `cos` (csrc/glibc_expcos.cuh,
+tools/extract_glibc_expcos.py), compiled for the host and compared bit for
+bit with this image's libm over tens of millions of inputs, and the
+log-normal draw against the reference's expression.  GPU tests compare the device port
 with libm, scls_generate_batch with the host generator and the compiled
 reference, and scls_run_sweep with scls_simulate_grid on host-generated
 traces (every TraceResult field)."""
@@ -67,6 +69,91 @@ def _build(src, name, shared=False):
     return out
 
 
+EXPCOS_SRC = r"""
+#include "glibc_expcos.cuh"
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <numbers>
+#include <random>
+// the reference's log-normal draw (workload.cpp:112-118,136-141), on libm
+static int ref_lognormal(double mu, double sigma, int cap, int limit, std::mt19937_64& e) {
+  const double u1 = 1.0 - (double)(e() >> 11) * 0x1.0p-53;
+  const double u2 = (double)(e() >> 11) * 0x1.0p-53;
+  const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * std::numbers::pi * u2);
+  const double raw = std::exp(mu + sigma * z);
+  const long long rounded = raw > 1e18 ? (long long)1e18 : std::llround(raw);
+  const long long v = std::min<long long>(rounded, cap);
+  return v < 1 ? 1 : (v > limit ? limit : (int)v);
+}
+int main() {
+  using namespace scls_glibc;
+  std::mt19937_64 g(1);
+  long bad = 0, n = 0;
+  auto chk = [&](const char* f, double x, double a, double b) {
+    ++n;
+    if (f_bits(a) != f_bits(b) && !(std::isnan(a) && std::isnan(b))) {
+      if (bad < 5) std::printf("%s(%a) libm=%a port=%a\n", f, x, a, b);
+      ++bad;
+    }
+  };
+  auto u = [&]() { return (double)(g() >> 11) * 0x1p-53; };
+  for (int i = 0; i < 8000000; ++i) { const double x = 6.283185307179586 * u(); chk("cos", x, std::cos(x), cos_fma(x)); }
+  for (int i = 0; i < 2000000; ++i) { const double x = 0.9 * u(); chk("cos", x, std::cos(x), cos_fma(x)); }
+  for (int i = 0; i < 2000000; ++i) { const double x = 1e-6 * u(); chk("cos", x, std::cos(x), cos_fma(x)); }
+  for (int i = 0; i < 2000000; ++i) { const double x = (u() - 0.5) * 2e6; chk("cos", x, std::cos(x), cos_fma(x)); }
+  for (int i = 0; i < 8000000; ++i) { const double x = (u() - 0.5) * 100.0; chk("exp", x, std::exp(x), exp_fma(x)); }
+  for (int i = 0; i < 2000000; ++i) { const double x = (u() - 0.5) * 1023.0; chk("exp", x, std::exp(x), exp_fma(x)); }
+  for (int i = 0; i < 2000000; ++i) { const double x = (u() - 0.5) * 1e-3; chk("exp", x, std::exp(x), exp_fma(x)); }
+  for (double x : {0.0, -0.0, 1e-300, 0x1p-27, 0x1p-28, 0.855469, 2.426265, 3.14159, 6.283185307179586})
+    chk("cos", x, std::cos(x), cos_fma(x));
+  for (double x : {0.0, -0.0, 1e-300, 0x1p-54, 0x1p-55, 1.0, 41.44653167389282, 41.4465316738928, 511.9, -511.9})
+    chk("exp", x, std::exp(x), exp_fma(x));
+  // the sampler end to end: mu / sigma spread incl. raw beyond 1e18 and below 0.5
+  const double mus[] = {-2.0, 0.0, 3.0, 5.5, 6.2, 7.0, 40.0, 45.0};
+  const double sig[] = {0.1, 0.5, 1.0, 2.0, 10.0};
+  for (double mu : mus)
+    for (double s : sig) {
+      std::mt19937_64 a(123), b(123);
+      for (int i = 0; i < 100000; ++i) {
+        const int r = ref_lognormal(mu, s, 1 << 30, 1 << 30, a);
+        const uint64_t w0 = b(), w1 = b();
+        ++n;
+        if (r != lognormal_length(mu, s, 1 << 30, 1 << 30, w0, w1)) ++bad;
+      }
+    }
+  std::printf("n=%ld bad=%ld\n", n, bad);
+  return bad != 0;
+}
+"""
+
+
+def test_glibc_expcos_port_matches_libm_on_host():
+    """csrc/glibc_expcos.cuh (host build) == this image's libm exp / cos, bit
+    for bit, and the log-normal draw == the reference's expression on libm."""
+    d = tempfile.mkdtemp(prefix="scls_gexp_")
+    src, exe = os.path.join(d, "c.cpp"), os.path.join(d, "c")
+    with open(src, "w") as f:
+        f.write(EXPCOS_SRC)
+    subprocess.run(["g++", "-O2", "-std=c++20", "-ffp-contract=off", "-I", CSRC, src, "-o", exe],
+                   check=True, capture_output=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout
+    assert "bad=0" in r.stdout
+
+
+def test_expcos_tables_match_this_libm(tmp_path):
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("extract2", os.path.join(ROOT, "tools", "extract_glibc_expcos.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.OUT = str(tmp_path / "glibc_expcos_data.h")
+    mod.main()
+    want = open(os.path.join(CSRC, "glibc_expcos_data.h")).read().split("\n", 1)[1]
+    got = open(mod.OUT).read().split("\n", 1)[1]
+    assert got == want
+
+
 def test_glibc_log_port_matches_libm_on_host():
     exe = _build(CHECK_SRC, "glog_check")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
@@ -104,6 +191,13 @@ def _specs():
                                   max_input_limit=1500, max_gen_limit=300, seed=11))
     out.append(capi.workload_spec(rate=8.0, duration_s=200.0, input_dist=u, seed=2 ** 63 + 5))
     out.append(capi.workload_spec(rate=1000.0, duration_s=30.0, max_input_limit=100, max_gen_limit=50, seed=0))
+    # log-normal lengths (Box-Muller: two outputs per draw), mixed with the other kinds
+    ln = capi.lognormal_dist(5.0, 1.0, 900)
+    out.append(capi.workload_spec(rate=10.0, duration_s=100.0, gen_dist=ln, seed=21))
+    out.append(capi.workload_spec(rate=15.0, duration_s=80.0, input_dist=capi.lognormal_dist(6.0, 0.8, 2000),
+                                  gen_dist=capi.lognormal_dist(4.5, 1.5, 4096), max_gen_limit=700, seed=22))
+    out.append(capi.workload_spec(rate=12.0, duration_s=60.0, input_dist=capi.lognormal_dist(3.0, 2.5, 1 << 30),
+                                  gen_dist=u, seed=23))
     return out
 
 
@@ -123,6 +217,51 @@ def test_device_log_matches_libm(ctx):
     nan = np.isnan(want) & np.isnan(got)
     bad = (got.view(np.int64) != want.view(np.int64)) & ~nan
     assert not bad.any(), (x[bad][:5], got[bad][:5], want[bad][:5])
+
+
+@pytest.mark.gpu
+def test_device_exp_cos_match_libm(ctx):
+    """The device ports of glibc exp / cos (the log-normal draw) == libm."""
+    so = _build(LIBM_SRC + r"""
+void libm_exp(int64_t n, const double* x, double* y) { for (int64_t i = 0; i < n; ++i) y[i] = exp(x[i]); }
+void libm_cos(int64_t n, const double* x, double* y) { for (int64_t i = 0; i < n; ++i) y[i] = cos(x[i]); }
+""", "libm_ec", shared=True)
+    libm = C.CDLL(so)
+    rng = np.random.default_rng(11)
+    u = (rng.integers(0, 2 ** 53, 3_000_000, dtype=np.int64).astype(np.float64)) * 2.0 ** -53
+    cases = {"cos": np.concatenate([2 * np.pi * u, 0.9 * u[:500_000], 1e-6 * u[:200_000],
+                                    (u[:500_000] - 0.5) * 2e6, [0.0, -0.0, 2.0 ** -27, 2.0 ** -28, 0.855469, 2.426265]]),
+             "exp": np.concatenate([(u - 0.5) * 100.0, (u[:500_000] - 0.5) * 1023.0, (u[:200_000] - 0.5) * 1e-3,
+                                    [0.0, -0.0, 2.0 ** -54, 2.0 ** -55, 1.0, 41.44653167389282, 511.9, -511.9]])}
+    for fn, x in cases.items():
+        f = getattr(libm, "libm_" + fn)
+        f.argtypes = [C.c_int64, C.c_void_p, C.c_void_p]
+        want = np.zeros_like(x)
+        f(len(x), x.ctypes.data, want.ctypes.data)
+        got = ctx.debug_libm(fn, x)
+        bad = got.view(np.int64) != want.view(np.int64)
+        assert not bad.any(), (fn, x[bad][:5], got[bad][:5], want[bad][:5])
+
+
+@pytest.mark.gpu
+def test_device_lognormal_generation_large(ctx, orc):
+    """2M log-normal draws on the device (1M requests, both lengths log-normal)
+    == the compiled reference's generate(), request by request."""
+    from oracle import pyoracle
+    from paper_2406_13511_b200 import lib
+    ref = pyoracle.ref_lib()
+    specs = [capi.workload_spec(rate=1000.0, duration_s=1000.0, input_dist=capi.lognormal_dist(6.0, 1.2, 8192),
+                                gen_dist=capi.lognormal_dist(5.0, 1.0, 4096), max_input_limit=4096,
+                                max_gen_limit=2048, seed=77),
+             capi.workload_spec(rate=200.0, duration_s=500.0, input_dist=capi.lognormal_dist(44.0, 3.0, 1 << 30),
+                                gen_dist=capi.lognormal_dist(-1.0, 4.0, 1 << 30), seed=78)]
+    offs, arr, inp, gen = ctx.generate_batch(specs)
+    for t, sp in enumerate(specs):
+        want = (ref or orc).generate(sp)
+        lo, hi = offs[t], offs[t + 1]
+        assert hi - lo == len(want[0]), t
+        assert np.array_equal(arr[lo:hi].view(np.int64), np.asarray(want[0], np.float64).view(np.int64)), t
+        assert np.array_equal(inp[lo:hi], want[1]) and np.array_equal(gen[lo:hi], want[2]), t
 
 
 @pytest.mark.gpu
@@ -186,10 +325,10 @@ def test_run_sweep_errors(ctx):
     with pytest.raises(SclsError) as e:
         ctx.run_sweep([bad], [capi.sched_cfg(policy="scls")], lat, mem)
     assert e.value.name == "Error" and "rate" in str(e.value)
-    ln = capi.workload_spec(rate=5.0, duration_s=10.0, gen_dist=capi.lognormal_dist(5.0, 1.0, 1024))
+    bad = capi.workload_spec(rate=5.0, duration_s=10.0, gen_dist=capi.lognormal_dist(5.0, -1.0, 1024))
     with pytest.raises(SclsError) as e:
-        ctx.run_sweep([ln], [capi.sched_cfg(policy="scls")], lat, mem)
-    assert "log-normal" in str(e.value)
+        ctx.run_sweep([bad], [capi.sched_cfg(policy="scls")], lat, mem)
+    assert e.value.name == "Error"
 
 
 @pytest.mark.gpu
