@@ -16,7 +16,7 @@
 //
 // Per-trace state lives in a per-trace arena (sim_layout) in global memory;
 // worker state lives in the lanes' registers (W <= 32; wider configs run a
-// variant with 32 worker slots per lane, W <= 1024).  The SCLS tick runs
+// variant with ceil(W / 32) worker slots per lane in the trace's arena, any W).  The SCLS tick runs
 // the scheduling core warp-wide: LSD radix sort of the pool by
 // (eff, arrival-rank == id), the Eq. 10 DP with a per-config cost table, the
 // backtrack, the stable descending estimate order and the max-min offload.
@@ -333,10 +333,12 @@ __device__ bool warp_radix_sort(int n, uint64_t* k, int32_t* v, uint64_t* k2, in
 __device__ __forceinline__ int bits_of(uint32_t x) { return x ? 32 - __clz(x) : 0; }
 
 // Per-worker (SCLS/SLS) / per-instance (ILS) state.  Worker w lives in lane
-// w & 31, slot w >> 5 of that lane's V slots: V = 1 (W <= 32, registers) or
-// kWideV (W <= 32 * kWideV, the slots in local memory).
-constexpr int kWideV = 32;
-constexpr int kMaxWorkers = 32 * kWideV;
+// w & 31, slot w >> 5 of that lane's slots: V = 1 (W <= 32, one slot in
+// registers) or V = kWideV (any W > 32, the reference's worker_count >= 1 of
+// sched_policies.cpp:56: ceil(W / 32) slots per lane in the trace's arena,
+// slot q of lane l at index 32 q + l, so a warp's 32 lanes touch 32
+// consecutive slots).
+constexpr int kWideV = 2;  // template tag of the arena-slot variant
 struct WorkerState {
   double ev_t = dinf();  // pending BatchDone / ILS boundary
   unsigned long long ev_s = ~0ull;
@@ -349,16 +351,27 @@ struct WorkerState {
   int it_cnt = 0, next_exit = 0, mctx = 0;
   long long seg_id = -1;
 };
+static_assert(sizeof(WorkerState) <= kWorkerSlotBytes, "sim.cuh kWorkerSlotBytes");
+
+// A lane's worker slots: V = 1 one register-resident slot; otherwise nv
+// slots in the arena.
+template <int V>
+struct Slots {
+  WorkerState r;
+  WorkerState* g = nullptr;
+  int nv = 1;
+  __device__ __forceinline__ WorkerState& operator[](int q) { return V == 1 ? r : g[q * 32]; }
+};
 
 // The (t, seq)-earliest pending worker event (seqs are distinct), or -1.
 template <int V>
-__device__ __forceinline__ int argmin_worker_event(const WorkerState* ws, int W, int lane, double* bt,
+__device__ __forceinline__ int argmin_worker_event(Slots<V>& ws, int W, int lane, double* bt,
                                                    unsigned long long* bs) {
   if (V == 1) return argmin_event_redux(ws[0].ev_t, ws[0].ev_s, lane < W && ws[0].ev_t != dinf(), lane, bt, bs);
   double t = dinf();
   unsigned long long s = ~0ull;
   int v = 0;
-  for (int q = 0; q < V; ++q) {
+  for (int q = 0; q < ws.nv; ++q) {
     const bool ok = q * 32 + lane < W && ws[q].ev_t != dinf();
     if (ok && (ws[q].ev_t < t || (ws[q].ev_t == t && ws[q].ev_s < s))) {
       t = ws[q].ev_t;
@@ -372,7 +385,7 @@ __device__ __forceinline__ int argmin_worker_event(const WorkerState* ws, int W,
 
 // The worker with the minimal (load, worker id) (offloader.cpp:41-48).
 template <int V>
-__device__ __forceinline__ int argmin_worker_load(const WorkerState* ws, int W, int lane) {
+__device__ __forceinline__ int argmin_worker_load(Slots<V>& ws, int W, int lane) {
   double bt;
   unsigned long long bs;
   if (V == 1)  // loads are >= 0, so (load, lane) keys order exactly
@@ -380,7 +393,7 @@ __device__ __forceinline__ int argmin_worker_load(const WorkerState* ws, int W, 
   double ld = dinf();
   int v = 0;
   bool has = false;
-  for (int q = 0; q < V; ++q)
+  for (int q = 0; q < ws.nv; ++q)
     if (q * 32 + lane < W && (!has || ws[q].load < ld)) {  // ascending slots: ties keep the lower id
       ld = ws[q].load;
       v = q;
@@ -393,9 +406,9 @@ __device__ __forceinline__ int argmin_worker_load(const WorkerState* ws, int W, 
 
 // min over workers of load (sched_policies.cpp:134-146).
 template <int V>
-__device__ __forceinline__ double min_worker_load(const WorkerState* ws, int W, int lane) {
+__device__ __forceinline__ double min_worker_load(Slots<V>& ws, int W, int lane) {
   double ml = dinf();
-  for (int q = 0; q < V; ++q)
+  for (int q = 0; q < ws.nv; ++q)
     if (q * 32 + lane < W) ml = fmin(ml, ws[q].load);
   for (int o = 16; o; o >>= 1) ml = fmin(ml, __shfl_xor_sync(FULL, ml, o));
   return ml;
@@ -452,7 +465,12 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
             logging ? P.mem_cap : 0);
 
   // Worker / instance state: worker w in lane WL(w), slot WK(w) (see WorkerState).
-  WorkerState ws[V];
+  Slots<V> ws;
+  if (V != 1) {
+    ws.g = (WorkerState*)(base + Lay.ws) + lane;
+    ws.nv = (W + 31) >> 5;
+    for (int q = 0; q < ws.nv; ++q) ws.g[q * 32] = WorkerState();
+  }
 #define WK(w) ws[V == 1 ? 0 : ((w) >> 5)]
 #define WL(w) (V == 1 ? (w) : ((w) & 31))
 #define MINE(w) (lane == WL(w))
@@ -1648,8 +1666,6 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   int32_t Gmax = 1;
   for (int c = 0; c < n_cfgs; ++c) {
     const scls_sched_cfg& x = cfgs[c];
-    if (x.worker_count > kMaxWorkers && validate_cfg_host(x) == SCLS_OK)
-      return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "device simulator supports worker_count <= 1024");
     hok[c] = model_ok && validate_cfg_host(x) == SCLS_OK;
     hc[c] = SimCfg{x.policy, x.slice_len, x.max_gen_limit, x.fixed_batch_size, x.max_concurrent,
                    x.worker_count, x.lambda, x.gamma, x.horizon_s, -1, mono && ctx->dp_mode != 1};

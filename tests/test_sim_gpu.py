@@ -397,13 +397,13 @@ def test_randomized_metrics_only_sweep_vs_reference(ctx, orc):
 @pytest.mark.parametrize("digests", [True, False])
 def test_wide_worker_counts_vs_oracle(ctx, orc, digests):
     """More than 32 workers / instances (the reference allows any count,
-    sched_policies.cpp:56): the wide lock-step variant (32 worker slots per
-    lane) against the oracle, mixed with narrow configs in one launch, with
+    sched_policies.cpp:56): the wide lock-step variant (ceil(W/32) worker
+    slots per lane in the trace's arena, any W) against the oracle, mixed with narrow configs in one launch, with
     and without digests (without: the metrics-only launch path)."""
     lat = capi.builtin_latency_model()
     rng = np.random.default_rng(33)
     cfgs, traces, idx = [], [], []
-    for i, w in enumerate((33, 40, 64, 100, 257, 1024, 8)):
+    for i, w in enumerate((33, 40, 64, 100, 257, 1024, 1025, 3000, 8)):
         for pol in ("scls", "sls", "ils"):
             cfgs.append(capi.sched_cfg(policy=pol, worker_count=w, slice_len=int(rng.choice([16, 64, 128])),
                                        max_gen_limit=512, fixed_batch_size=int(rng.integers(1, 12)),
@@ -442,11 +442,25 @@ def test_wide_worker_event_logs(ctx, orc):
             assert max(r[0][7] for r in ra) >= 33  # workers above 32 were used (record field `worker`)
 
 
-def test_worker_count_limit(ctx, orc):
+def test_worker_counts_beyond_1024(ctx, orc):
+    """Any worker_count >= 1 (sched_policies.cpp:56): 1,500 / 5,000 workers,
+    every policy, event logs record by record and the report."""
     lat = capi.builtin_latency_model()
-    trace = orc.generate(capi.workload_spec(rate=5.0, duration_s=5.0))
-    with pytest.raises(Exception, match="1024"):
-        ctx.simulate([trace], capi.sched_cfg(worker_count=1025), lat, MEMORIES["rule"]())
+    traces = [orc.generate(capi.workload_spec(rate=2000.0, duration_s=3.0, seed=97 + i)) for i in range(2)]
+    for w in (1500, 5000):
+        for pol in ("scls", "sls", "ils"):
+            cfg = capi.sched_cfg(policy=pol, worker_count=w, slice_len=64, max_concurrent=3, fixed_batch_size=3)
+            a, _, la = ctx.simulate(traces, cfg, lat, MEMORIES["rule"](), n_logged=2, rec_cap=200000,
+                                    mem_cap=200000)
+            b, _, lb = orc.simulate(traces, cfg, lat, MEMORIES["rule"](), n_logged=2, rec_cap=200000,
+                                    mem_cap=200000)
+            for t in range(2):
+                assert_results_equal(a[t], b[t], (w, pol, t))
+                ra, ma = _log_rows(la, t)
+                rb, mb = _log_rows(lb, t)
+                assert ra == rb and ma == mb, (w, pol, t)
+                if pol != "scls":  # round-robin assignment reaches every worker
+                    assert max(r[0][7] for r in ra) >= 1024, (w, pol)
 
 
 @pytest.mark.parametrize("pol", ["ils", "sls"])
