@@ -136,7 +136,7 @@ int64_t scls_last_launch_count(const scls_ctx* ctx);
  * the h_* log digests of scls_trace_result; 0 skips them (the metrics are
  * computed either way, and the digests are zero). */
 enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT = 3, SCLS_OPT_ILS_KERNEL = 4,
-       SCLS_OPT_BATCH_PATH = 5 };
+       SCLS_OPT_BATCH_PATH = 5, SCLS_OPT_DP_CLUSTER = 6 };
 /* SCLS_OPT_DP_KERNEL: 0 (default) picks the monotone decision kernel when the
  * model allows it and some window exceeds 32 rows, else the serial-chain
  * kernel; 1 forces the chain kernel; 2 forces the decision kernel when the
@@ -150,7 +150,13 @@ enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT
  * kernels that process the global event order directly (results identical).
  * SCLS_OPT_BATCH_PATH (default 0): batch_requests / schedule take the fused
  * four-launch small-pool path for n <= 4096 and the multi-kernel path above;
- * 1 forces the multi-kernel path at every size (results identical). */
+ * 1 forces the multi-kernel path at every size (results identical).
+ * SCLS_OPT_DP_CLUSTER (default 1): the monotone DP kernel runs as a
+ * thread-block cluster of this many CTAs (1, 2 or 4): the older far
+ * candidates go to the peer CTAs, exchanged over distributed shared memory
+ * (results identical).  Measured slower than one CTA on the C3 pool (2: 58,
+ * 4: 70 vs 51 ms: the per-tile DSMEM handshake costs more than the far scan
+ * it moves), so 1 is the default. */
 scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value);
 /* Diagnostics: enable/disable clock64 phase counters in the DP chain kernel
  * and read-and-reset them (cycles: main chain, main barrier wait, helper

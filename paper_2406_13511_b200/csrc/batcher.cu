@@ -377,8 +377,40 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
   const bool monotone = int_cmp && scls_validate_memory(in.mem) == SCLS_OK && ctx->dp_mode != 1 &&
                         (k_max > 32 || ctx->dp_mode == 2);
   ctx->dp_last_mono = monotone;
+  // A thread-block cluster spreads the far candidates over kC SMs
+  // (dp_mono.cuh); SCLS_OPT_DP_CLUSTER picks kC (1 = one CTA).
+  auto launch_cluster = [&](auto kern, int csize, size_t bytes) -> bool {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csize);
+    cfg.blockDim = dim3(kDpThreads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, (int32_t)n, (const int32_t*)Krow, (const int32_t*)cbase, (const double*)cost, T,
+                           split, ctx->dp_prof, (const int32_t*)nullptr, (int32_t)0) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    SCLS_LAUNCHED();
+    return true;
+  };
   if (monotone) {
-    stt = global_t ? launch(dp_mono_kernel<true>, sizeof(DpMonoSmem)) : launch(dp_mono_kernel<false>, sizeof(DpMonoSmem));
+    bool done = false;
+    if (!global_t && ctx->dp_cluster == 4) done = launch_cluster(dp_mono_kernel<false, 4>, 4, sizeof(DpMonoSmemT<4>));
+    if (!global_t && ctx->dp_cluster == 2) done = launch_cluster(dp_mono_kernel<false, 2>, 2, sizeof(DpMonoSmemT<2>));
+    if (!done)
+      stt = global_t ? launch(dp_mono_kernel<true>, sizeof(DpMonoSmem)) : launch(dp_mono_kernel<false>, sizeof(DpMonoSmem));
+    ctx->dp_last_cluster = done ? ctx->dp_cluster : 1;
   } else if (global_t) {
     stt = int_cmp ? launch(dp_chain_kernel<true, true>, smem) : launch(dp_chain_kernel<true, false>, smem);
   } else {

@@ -229,6 +229,11 @@ scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value) {
     ctx->sim_concurrent = value != 0;
     return SCLS_OK;
   }
+  if (option == SCLS_OPT_DP_CLUSTER) {
+    if (value != 1 && value != 2 && value != 4) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "DP cluster size must be 1, 2 or 4");
+    ctx->dp_cluster = (int)value;
+    return SCLS_OK;
+  }
   if (option == SCLS_OPT_ILS_KERNEL) {
     ctx->ils_lockstep = value != 0;
     return SCLS_OK;

@@ -24,6 +24,8 @@ struct scls_ctx {
   int sm_count = 148;
   unsigned long long* dp_prof = nullptr;  // device counters when profiling is on
   bool sim_digests = true;                // scls_simulate computes the log digests
+  int dp_cluster = 1;                     // CTAs per monotone-DP cluster (1, 2 or 4)
+  int dp_last_cluster = 1;                // what the last monotone DP launch used
   int dp_mode = 0;                        // 0 auto, 1 force the chain kernel (tests)
   bool dp_last_mono = false;              // the last DP ran the monotone decision kernel
   bool sim_concurrent = true;             // scls_simulate runs its per-policy launches concurrently

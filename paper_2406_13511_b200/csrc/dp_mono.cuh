@@ -41,29 +41,100 @@
 
 namespace scls {
 
-constexpr int kMonoSegs = kDpHelpers;  // 12 k-segments per row
+constexpr int kMonoSegs = kDpHelpers;  // 12 k-segments per row per CTA
+constexpr int kDpMaxCluster = 4;       // CTAs per DP cluster (dp_mono_kernel<., kC>)
 #ifndef SCLS_DP_FAR_TOP
 #define SCLS_DP_FAR_TOP 48
 #endif
 constexpr int kFarTop = SCLS_DP_FAR_TOP;  // far k's near the window, split finer
 
-struct DpMonoSmem {
-  double ring[kDpRing];          // 32 KB of recent T
-  double cs[3][kDpStageK][32];   // 48 KB staged c(L_r, 1..64), +INF past W_r
-  double Pv[2][kMonoSegs][32];   // far partial minima per segment
+// Shared memory of dp_mono_kernel<., kC>.  kC > 1 stages 96 costs per row
+// (the near-far band k <= 95 of CTA 0's helpers) and holds the peers'
+// far-far partials in a 3-deep ring (Q).
+template <int kC>
+struct DpMonoSmemT {
+  static constexpr int kStage = kC > 1 ? 96 : kDpStageK;
+  double ring[kDpRing];              // 32 KB of recent T
+  double cs[3][kStage][32];          // staged c(L_r, 1..kStage), +INF past W_r
+  double Pv[2][kMonoSegs][32];       // CTA 0 helpers' partial minima per segment
   int32_t Pk[2][kMonoSegs][32];
-  double Fv[2][32];              // merged far minimum per row
+  double Qv[3][32];                  // a peer's merged far-far minimum per row (kC > 1)
+  int32_t Qk[3][32];
+  unsigned long long tiles_done;     // CTA 0: tiles whose T is final (read by the peers)
+  unsigned long long far_done;       // a peer: far-far tiles whose Q entry is final (read by CTA 0)
+  double Fv[2][32];                  // merged far minimum per row
   int32_t Fk[2][32];
   int32_t W[4][32];
   int32_t CB[4][32];
 };
+using DpMonoSmem = DpMonoSmemT<1>;
+
+// ---- thread-block-cluster primitives (DSMEM stores, counters at cluster scope)
+__device__ __forceinline__ uint32_t dp_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t dp_mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint32_t dp_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void dp_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Monotone counters at cluster scope.  A writer orders its CTA's earlier
+// shared-memory writes (made visible to it by a CTA barrier) before the
+// counter with a cumulative release fence; readers poll with acquire loads,
+// so no phase aliasing however far one side runs ahead.
+__device__ __forceinline__ void dp_fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+__device__ __forceinline__ void dp_st_count(unsigned long long* c, unsigned long long v) {
+  asm volatile("st.relaxed.cluster.shared::cta.u64 [%0], %1;" ::"r"(dp_smem_u32(c)), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long dp_ld_acquire(uint32_t cluster_addr) {
+  unsigned long long v;
+  asm volatile("ld.acquire.cluster.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ double dp_ld_remote(uint32_t a) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int32_t dp_ld_remote_s32(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+// Polls a (local or remote) counter until it reaches target; a bounded spin
+// turns a protocol error into a trap (a launch error) instead of a hung GPU.
+__device__ __forceinline__ void dp_wait_count(uint32_t cluster_addr, unsigned long long target) {
+  for (uint32_t it = 0;; ++it) {
+    if (dp_ld_acquire(cluster_addr) >= target) return;
+    if (it > (1u << 27)) __trap();
+    __nanosleep(20);
+  }
+}
 
 // (v, k) lexicographic "a before b": smaller value, ties to the smaller k.
 __device__ __forceinline__ bool lex_lt(double va, int ka, double vb, int kb) {
   return va < vb || (va == vb && ka < kb);
 }
 
-template <bool kGlobalT>
+// kC > 1 (a thread-block cluster of kC CTAs, !kGlobalT): CTA 0 runs the
+// kernel below; CTAs 1..kC-1 are far-candidate helpers only.  Their 12
+// helper warps take far segments 12 rank .. 12 rank + 11 of every row (the
+// 12 kC segments split the k range as the 12 did), read T from their own ring
+// -- after each tile's barrier an idle warp of CTA 0 publishes tiles_done
+// (release fence + store); a peer's helper warp 0 polls it (acquire) and
+// copies the tile's 32 T values out of CTA 0's ring over DSMEM.  Every
+// exchange is a pull of data the owner finished in its own shared memory:
+// the owner publishes a monotone counter after a release fence, the reader
+// polls it with acquire loads and then loads over DSMEM.
+// Pv/Pk are double-buffered by tile parity: a peer writes far(u) only after
+// tile u-2 is final, and CTA 0 merged far(u-2) before finishing tile u-3.
+template <bool kGlobalT, int kC = 1>
 __global__ void __launch_bounds__(kDpThreads, 1)
     dp_mono_kernel(int32_t n, const int32_t* __restrict__ Krow, const int32_t* __restrict__ cbase,
                    const double* __restrict__ cost, double* __restrict__ T, int32_t* __restrict__ split,
@@ -71,7 +142,9 @@ __global__ void __launch_bounds__(kDpThreads, 1)
                    int32_t gate_id = 0) {
   if (gate && *gate != gate_id) return;  // small-pool launches: the DP kernel the device did not choose
   extern __shared__ __align__(16) unsigned char dp_smem_raw[];
-  DpMonoSmem& sm = *reinterpret_cast<DpMonoSmem*>(dp_smem_raw);
+  using Smem = DpMonoSmemT<kC>;
+  Smem& sm = *reinterpret_cast<Smem*>(dp_smem_raw);
+  constexpr int kStage = Smem::kStage;
   constexpr int M = kDpRing - 1;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -79,6 +152,12 @@ __global__ void __launch_bounds__(kDpThreads, 1)
   const int h = warp - 1 - (warp >> 2);  // helper index 0..11
   const int ht = h * 32 + lane;
   const int ntiles = (n + 31) >> 5;
+  static_assert(kC >= 1 && kC <= kDpMaxCluster && (kC == 1 || !kGlobalT), "cluster variant: T in the ring");
+  // kC == 1: the 12 helper warps split every row's far k range.  kC > 1: the
+  // peers' 12 (kC - 1) warps split the far-far range (sources <= 32(u-2)).
+  constexpr int kSegs = kC > 1 ? kMonoSegs * (kC - 1) : kMonoSegs;
+  const int rank = kC > 1 ? (int)dp_cluster_rank() : 0;
+  const int g = kC > 1 ? h + kMonoSegs * (rank - 1) : h;  // this helper warp's far segment
 
   auto load_meta = [&](int u) {
     if (h == 0 && u < ntiles) {
@@ -90,7 +169,7 @@ __global__ void __launch_bounds__(kDpThreads, 1)
   // Staging c(L_r, 1..64) of tile u: stage_load issues the global loads
   // into registers, stage_store writes them (+INF past W_r) to shared
   // memory — far() runs in between so the loads' latency is hidden.
-  constexpr int kPer = (32 * kDpStageK + kDpHelperThreads - 1) / kDpHelperThreads;
+  constexpr int kPer = (32 * kStage + kDpHelperThreads - 1) / kDpHelperThreads;
   auto stage_load = [&](int u, double* v) {
 #pragma unroll
     for (int i = 0; i < kPer; ++i) v[i] = kInf;
@@ -100,7 +179,7 @@ __global__ void __launch_bounds__(kDpThreads, 1)
     for (int i = 0; i < kPer; ++i) {
       const int e = ht + i * kDpHelperThreads;
       const int k = 1 + (e >> 5);
-      if (e < 32 * kDpStageK && k <= W) v[i] = cost[CB + k];
+      if (e < 32 * kStage && k <= W) v[i] = cost[CB + k];
     }
   };
   auto stage_store = [&](int u, const double* v) {
@@ -109,7 +188,7 @@ __global__ void __launch_bounds__(kDpThreads, 1)
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int e = ht + i * kDpHelperThreads;
-      if (e < 32 * kDpStageK) sm.cs[b][e >> 5][e & 31] = v[i];
+      if (e < 32 * kStage) sm.cs[b][e >> 5][e & 31] = v[i];
     }
   };
   auto stage_costs = [&](int u) {
@@ -117,35 +196,29 @@ __global__ void __launch_bounds__(kDpThreads, 1)
     stage_load(u, v);
     stage_store(u, v);
   };
-  // Far candidates of tile u (sources j <= 32(u-1)): helper h scans the h-th
-  // k-segment of row m = lane, then (after a helper-only barrier) helper 0
-  // merges the segments in ascending k.
-  auto far = [&](int u) {
-    if (u >= ntiles) return;
-    const int jmax = (u - 1) << 5;
+  // This warp's segment g of the far candidates of row r (lane) over the
+  // sources j <= jtop (k >= r - jtop): (value, k) lexicographic minimum.
+  auto seg_scan = [&](int u, int jtop, int W, int cb, double& best, int& bk) {
     const int r = (u << 5) + 1 + lane;
-    const int W = sm.W[u & 3][lane];
-    const int cb = sm.CB[u & 3][lane];
+    const int jmax = jtop;
     const int kmin = r - jmax;
     const int span = W - kmin + 1;
-    double best = kInf;
-    int bk = 0;
     if (span > 0) {
       // Two tiers: the top kFarTop k's (the batch sizes near the window, where
       // the minimum of these monotone costs lives and pruning rarely holds)
       // in kMonoSegs/2 short segments, the rest in the other half (mostly
       // pruned by the bound below) -- the helpers' work evens out.
-      constexpr int kHalf = kMonoSegs / 2;
+      constexpr int kHalf = kSegs / 2;
       const int top = min(span, kFarTop);
       const int rest = span - top;
       int k0, k1;
-      if (h < kHalf) {
+      if (g < kHalf) {
         const int len = (rest + kHalf - 1) / kHalf;
-        k0 = kmin + h * len;
+        k0 = kmin + g * len;
         k1 = min(kmin + rest - 1, k0 + len - 1);
       } else {
         const int len = (top + kHalf - 1) / kHalf;
-        k0 = kmin + rest + (h - kHalf) * len;
+        k0 = kmin + rest + (g - kHalf) * len;
         k1 = min(W, k0 + len - 1);
       }
       // Exact segment pruning (monotone T and c): every candidate of the
@@ -189,34 +262,147 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         bk = k2;
       }
     }
+  };
+  // merge of 12 partials (per-warp loads, then a tree); folds into (fv, fk2)
+  auto merge12 = [&](const double (*Pv_)[32], const int32_t (*Pk_)[32], double& fv, int& fk2) {
+    double v[kMonoSegs];
+    int k[kMonoSegs];
+#pragma unroll
+    for (int s2 = 0; s2 < kMonoSegs; ++s2) {
+      v[s2] = Pv_[s2][lane];
+      k[s2] = Pk_[s2][lane];
+    }
+#pragma unroll
+    for (int span2 = 1; span2 < kMonoSegs; span2 <<= 1) {
+#pragma unroll
+      for (int s2 = 0; s2 + span2 < kMonoSegs; s2 += 2 * span2) {
+        if (lex_lt(v[s2 + span2], k[s2 + span2], v[s2], k[s2])) {
+          v[s2] = v[s2 + span2];
+          k[s2] = k[s2 + span2];
+        }
+      }
+    }
+    if (lex_lt(v[0], k[0], fv, fk2)) {
+      fv = v[0];
+      fk2 = k[0];
+    }
+  };
+  // Far candidates of tile u (sources j <= 32(u-1)), merged into Fv/Fk by
+  // helper 0 of CTA 0.  kC == 1: the 12 helpers' k-segments of every row.
+  // kC > 1: CTA 0's helpers take the near-far band (the 32 sources of tile
+  // u-2, costs from the staged cs block) and merge it with the peers'
+  // far-far segments of tile u (Q ring, delivered over DSMEM).
+  auto far = [&](int u) {
+    if (u >= ntiles) return;
+    double best = kInf;
+    int bk = 0;
+    if (kC == 1) {
+      seg_scan(u, (u - 1) << 5, sm.W[u & 3][lane], sm.CB[u & 3][lane], best, bk);
+    } else {
+      const int r = (u << 5) + 1 + lane;
+      const int lo = r - sm.W[u & 3][lane];
+      const int jn0 = max(0, ((u - 2) << 5) + 1), jn1 = (u - 1) << 5;
+      const int cb3 = u % 3;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int j = jn0 + h + q * kMonoSegs;
+        if (j <= jn1 && j >= lo && r <= n) {
+          const int k = r - j;  // 1 + lane .. 64 + lane, staged (+INF past W_r)
+          const double cand = __dadd_rn(sm.ring[j & M], sm.cs[cb3][k - 1][lane]);
+          if (lex_lt(cand, k, best, bk)) {
+            best = cand;
+            bk = k;
+          }
+        }
+      }
+    }
     sm.Pv[u & 1][h][lane] = best;
     sm.Pk[u & 1][h][lane] = bk;
     asm volatile("bar.sync 1, %0;" ::"n"(kDpHelperThreads));
     if (h == 0) {
-      // merge the 12 segments (ascending k): all loads first, then a tree of
-      // (value, k) lexicographic minima — ties go to the smaller k.
-      double v[kMonoSegs];
-      int k[kMonoSegs];
-#pragma unroll
-      for (int s2 = 0; s2 < kMonoSegs; ++s2) {
-        v[s2] = sm.Pv[u & 1][s2][lane];
-        k[s2] = sm.Pk[u & 1][s2][lane];
-      }
-#pragma unroll
-      for (int span2 = 1; span2 < kMonoSegs; span2 <<= 1) {
-#pragma unroll
-        for (int s2 = 0; s2 + span2 < kMonoSegs; s2 += 2 * span2) {
-          if (lex_lt(v[s2 + span2], k[s2 + span2], v[s2], k[s2])) {
-            v[s2] = v[s2 + span2];
-            k[s2] = k[s2 + span2];
+      double fv = kInf;
+      int fk2 = 0;
+      merge12(sm.Pv[u & 1], sm.Pk[u & 1], fv, fk2);
+      if (kC > 1) {
+        // each peer's merged far-far minima of tile u, pulled over DSMEM once
+        // the peer has published them (acquire)
+#pragma unroll 1
+        for (int p = 1; p < kC; ++p) {
+          dp_wait_count(dp_mapa(dp_smem_u32(&sm.far_done), p), (unsigned long long)u);
+          const double qv = dp_ld_remote(dp_mapa(dp_smem_u32(&sm.Qv[u % 3][lane]), p));
+          const int qk = dp_ld_remote_s32(dp_mapa(dp_smem_u32(&sm.Qk[u % 3][lane]), p));
+          if (lex_lt(qv, qk, fv, fk2)) {
+            fv = qv;
+            fk2 = qk;
           }
         }
       }
-      sm.Fv[u & 1][lane] = v[0];
-      sm.Fk[u & 1][lane] = k[0];
+      sm.Fv[u & 1][lane] = fv;
+      sm.Fk[u & 1][lane] = fk2;
     }
   };
-
+  // A peer's far-far segments of tile u (sources j <= 32(u-2)): its 12
+  // helper warps' partials (Pv, local), merged by its helper 0 into Q[u % 3],
+  // then published (warp-wide release fence, far_done = u) for CTA 0 to pull.
+  // Q[u % 3] is rewritten for tile u + 3 only after tiles_done >= u + 1,
+  // i.e. after CTA 0 consumed it while finishing tile u - 1.
+  auto far_far = [&](int u, int W, int cb) {
+    double best = kInf;
+    int bk = 0;
+    if (u >= 2) seg_scan(u, (u - 2) << 5, W, cb, best, bk);
+    sm.Pv[u & 1][h][lane] = best;
+    sm.Pk[u & 1][h][lane] = bk;
+    asm volatile("bar.sync 1, %0;" ::"n"(kDpHelperThreads));
+    if (h == 0) {
+      double fv = kInf;
+      int fk2 = 0;
+      merge12(sm.Pv[u & 1], sm.Pk[u & 1], fv, fk2);
+      sm.Qv[u % 3][lane] = fv;
+      sm.Qk[u % 3][lane] = fk2;
+      __syncwarp();
+      dp_fence_cluster();
+      if (lane == 0) dp_st_count(&sm.far_done, (unsigned long long)u);
+    }
+  };
+  if (kC > 1) {
+    if (tid == 0) {
+      sm.ring[0] = 0.0;
+      sm.tiles_done = 0;
+      sm.far_done = 0;
+    }
+    dp_cluster_sync();
+    if (rank != 0) {
+      // peer: far_far(u) (sources <= 32(u-2)) once tiles 0..u-3 are final --
+      // helper warp 0 polls CTA 0's tiles_done and copies tile u-3's T into
+      // this CTA's ring; CTA 0 needs the result only at the end of tile u-1,
+      // two tiles later
+      if (helper) {
+        int Wn = 0, CBn = 0;
+        auto meta = [&](int u, int& W_, int& CB_) {
+          const int r = (u << 5) + 1 + lane;
+          W_ = u < ntiles && r <= n ? Krow[r - 1] : 0;
+          CB_ = u < ntiles && r <= n ? cbase[r - 1] : 0;
+        };
+        meta(1, Wn, CBn);
+        const uint32_t done0 = dp_mapa(dp_smem_u32(&sm.tiles_done), 0);
+        for (int u = 1; u < ntiles; ++u) {
+          const int Wc = Wn, CBc = CBn;
+          meta(u + 1, Wn, CBn);
+          if (u >= 3) {
+            if (h == 0) {
+              dp_wait_count(done0, (unsigned long long)(u - 2));
+              const int r = ((u - 3) << 5) + 1 + lane;
+              if (r <= n) sm.ring[r & M] = dp_ld_remote(dp_mapa(dp_smem_u32(&sm.ring[r & M]), 0));
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kDpHelperThreads));
+          }
+          far_far(u, Wc, CBc);
+        }
+      }
+      dp_cluster_sync();  // keep this CTA's shared memory alive until CTA 0 is done
+      return;
+    }
+  }
   if (tid == 0) {
     sm.ring[0] = 0.0;
     T[0] = 0.0;
@@ -353,6 +539,10 @@ __global__ void __launch_bounds__(kDpThreads, 1)
       t2 = prof ? clock64() : 0;
     }
     __syncthreads();
+    if (kC > 1 && warp == 4 && lane == 0) {  // off the main warp's path: publish tile t
+      dp_fence_cluster();
+      dp_st_count(&sm.tiles_done, (unsigned long long)(t + 1));
+    }
     if (prof) {
       const long long t3 = clock64();
       if (warp == 0) {
@@ -378,6 +568,7 @@ __global__ void __launch_bounds__(kDpThreads, 1)
       atomicAdd(&prof[5], 1ull);
     }
   }
+  if (kC > 1) dp_cluster_sync();  // the peers' shared memory stays valid until CTA 0 is done
 }
 
 }  // namespace scls

@@ -199,6 +199,10 @@ class Context:
         """SCLS_OPT_BATCH_PATH: 1 forces the multi-kernel batch_requests path for small pools too."""
         self._check(self.lib.scls_set_option(self.h, 5, 1 if large else 0))
 
+    def set_dp_cluster(self, ctas):
+        """SCLS_OPT_DP_CLUSTER: CTAs per monotone-DP cluster (1, 2 or 4; default 1)."""
+        self._check(self.lib.scls_set_option(self.h, 6, int(ctas)))
+
     def set_dp_kernel(self, mode):
         """SCLS_OPT_DP_KERNEL: 0 auto (monotone decision kernel when allowed), 1 chain."""
         self._check(self.lib.scls_set_option(self.h, 2, int(mode)))

@@ -315,3 +315,33 @@ def test_small_pool_path_matches_large_path(ctx, orc):
 def lib_error():
     from paper_2406_13511_b200.lib import SclsError
     return SclsError
+
+
+@pytest.mark.parametrize("ctas", [1, 2, 4])
+def test_dp_cluster_sizes_bit_exact(ctx, orc, golden, ctas):
+    """The monotone DP as one CTA or a 2 / 4-CTA cluster (far candidates over
+    DSMEM): the reference's fingerprints on the 2^20 goldens and the oracle on
+    pools whose windows exceed a tile (the analytic and tight KV caps)."""
+    lat = capi.builtin_latency_model()
+    ctx.set_dp_cluster(ctas)
+    try:
+        for case in golden["batcher"]:
+            if case["memory"] == "rule" or case["n"] < 8192:
+                continue
+            eff, arr, ids, _ = orc.make_pool(case["n"], case["seed"])
+            res = ctx.batch_requests(eff, arr, ids, case["slice_len"], lat, MEMORIES[case["memory"]]())
+            msg = (ctas, case["n"], case["slice_len"], case["memory"])
+            assert res["n_batches"] == case["n_batches"], msg
+            assert sha(res["seg_begin"].astype(np.int32)) == case["seg"], msg
+            assert sha(res["est"].astype(np.float64)) == case["est"], msg
+        rng = np.random.default_rng(5 + ctas)
+        for n in (4097, 9000, 33333):
+            eff = rng.integers(1, 3000, n).astype(np.int32)
+            arr = rng.random(n) * 50
+            ids = rng.permutation(n).astype(np.int64)
+            for mname in ("analytic", "tight"):
+                a = ctx.batch_requests(eff, arr, ids, 128, lat, MEMORIES[mname]())
+                b = orc.batch_requests(eff, arr, ids, 128, lat, MEMORIES[mname]())
+                assert_same_batches(a, b, (ctas, n, mname))
+    finally:
+        ctx.set_dp_cluster(1)

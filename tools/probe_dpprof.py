@@ -20,5 +20,14 @@ for name, mem in (("analytic", capi.builtin_analytic_memory_model()), ("rule", c
               p[0] / tiles, p[6] / tiles, p[7] / tiles, p[1] / tiles, p[2] / tiles / nh, p[3] / tiles / nh,
               p[4] / tiles / nh))
 ctx.dp_profile(False)
+eff, arr, ids, _ = lib.make_pool(n, 7)
+for ctas in (1, 2, 4):
+    ctx.set_dp_cluster(ctas)
+    ts = []
+    for _ in range(3):
+        r = ctx.batch_requests(eff, arr, ids, 128, lat, capi.builtin_analytic_memory_model())
+        ts.append(ctx.timings()["dp"])
+    print("analytic dp cluster", ctas, "ms", [round(x, 2) for x in ts], r["n_batches"])
+ctx.set_dp_cluster(1)
 r = ctx.batch_requests(eff, arr, ids, 128, lat, capi.builtin_memory_model())
 print("unprofiled rule dp ms %.2f" % ctx.timings()["dp"])
