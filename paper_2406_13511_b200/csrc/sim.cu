@@ -840,13 +840,18 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         // T[tb+s-1] arrives; step s offers k = lane + 2 - s to this lane
         double Tj = T[tb];
         const int rows = min(32, P_ - tb);
-        auto kval = [&](int s) { return s >= 2 && s <= rows && lane + 2 - s >= 1 && lane + 2 - s <= Wr; };
+        // step s is valid for this lane iff 2 <= s <= rows and 1 <= k <= Wr,
+        // i.e. s in [s_lo, s_lo + cnt): one unsigned compare per step
+        const int s_lo = max(2, lane + 2 - Wr);
+        const int cnt = max(0, min(rows, lane + 1) - s_lo + 1);
+        auto kval = [&](int s) { return (unsigned)(s - s_lo) < (unsigned)cnt; };
+        const double* __restrict__ cp = crow + lane;       // c(L_r, lane + 2 - s) = cp[2 - s]
         double c1 = 0.0;                                   // step s (never valid at s = 1)
-        double c2 = kval(2) ? __ldg(crow + lane) : 0.0;    // step s + 1
+        double c2 = kval(2) ? __ldg(cp) : 0.0;             // step s + 1
         for (int s = 1; s <= rows; ++s) {
           const double c0 = c1;
           c1 = c2;
-          c2 = kval(s + 2) ? __ldg(crow + lane - s) : 0.0;  // k = lane + 2 - (s + 2)
+          c2 = kval(s + 2) ? __ldg(cp - s) : 0.0;  // k = lane + 2 - (s + 2)
           if (kval(s)) {
             const double cand = __dadd_rn(Tj, c0);
             if (cand <= acc) {
