@@ -1,3 +1,6 @@
+# ncu captures behind profiles/ncu_summary.json (run under gpurun, one GPU):
+#   bash tools/gpu_profile.sh   -> gpurun_out/prof_*_r02b.ncu-rep, r02b_*.log
+# then: python tools/summarize_ncu.py report gpurun_out/<rep> <kernel-substring>=<name>
 set -x
 NCU="ncu --set full --import-source on --clock-control none -c 1"
 $NCU -k regex:sim_ils_indep -o gpurun_out/prof_ils_r02b python tools/probe.py one ils 4096 > gpurun_out/r02b_ils.log 2>&1
