@@ -515,6 +515,9 @@ def run_ours(args, rank, world, dist):
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(ncu_name),
                      "peak_source": peak_src, "bytes_per_launch": bytes_per_launch,
                      "launch_ms": pol_ms[dom],
+                     # the bound that applies: warp-issue slots (ncu smsp__issue_active of the
+                     # committed capture of this kernel on the current build)
+                     "issue_frac": ((ncu_row(ncu_name) or {}).get("issue_active_pct") or 0.0) / 100.0 or None,
                      "note": "the simulators are event-chain (issue / latency) bound, not HBM bound: "
                              "algorithmic bytes = 16 B/request in + result records out; the issue efficiency "
                              "the north star asks for is in `issue_efficiency`"},

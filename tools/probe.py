@@ -3,6 +3,7 @@
   python tools/probe.py sweep [traces]     per-policy kernel ms of the C5 sweep shape
   python tools/probe.py scls-dp [traces]   SCLS kernel ms per tick-DP mode (auto / chain)
   python tools/probe.py one <policy> [traces] one device-generated sweep of one policy (ncu target)
+  python tools/probe.py c4                 every C4 job alone, device ms next to the reference (1 thread)
   python tools/probe.py scls-prof [traces] [rates]
                                            per-phase clock64 split of the SCLS kernel
                                            (needs SCLS_B200_LIB = a -DSCLS_SIM_PROF build)
@@ -43,6 +44,28 @@ def main():
                 ctx.set_dp_kernel(mode)
                 print("dp mode", mode, "sweep", kernel_ms(ctx, specs(T), capi.sched_cfg()),
                       "one rate-25 trace", kernel_ms(ctx, specs(1, (25.0,)), capi.sched_cfg()))
+        elif cmd == "c4":  # every C4 job alone: device ms (and the compiled reference, 1 thread)
+            from oracle.pyoracle import ref_lib
+            ref = ref_lib()
+            import time
+            for pol in ("scls", "sls", "ils"):
+                for S in (32, 64, 128, 256):
+                    for G in (256, 512, 1024):
+                        if S > G:
+                            continue
+                        sp = capi.workload_spec(rate=20.0, duration_s=5000.0, seed=42, max_gen_limit=G)
+                        cfg = capi.sched_cfg(policy=pol, slice_len=S, max_gen_limit=G)
+                        ts = []
+                        for _ in range(2):
+                            ctx.run_experiments([sp], [cfg], LAT, MEM, hist_bins=16)
+                            ts.append(ctx.timings()["total"])
+                        cpu = None
+                        if ref is not None:
+                            tr = [ref.generate(sp)]
+                            t0 = time.perf_counter()
+                            ref.simulate(tr, [cfg], LAT, MEM, cfg_index=[0], hist_bins=16)
+                            cpu = (time.perf_counter() - t0) * 1e3
+                        print(pol, S, G, "device ms %.1f" % min(ts), "cpu ms %.1f" % cpu if cpu else "")
         elif cmd == "one":
             T = int(sys.argv[3]) if len(sys.argv) > 3 else 4096
             ctx.run_sweep(specs(T), [capi.sched_cfg(policy=sys.argv[2])], LAT, MEM, hist_bins=16)
