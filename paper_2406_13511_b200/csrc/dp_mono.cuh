@@ -21,6 +21,11 @@
 // the reference's full scan returns.  Row a+1 itself is always final (all its
 // sources are <= a).
 //
+// Warp roles (16 warps, warp w on SMSP w % 4): warp 0 = main (rows of the
+// current tile), warps 4 / 8 / 12 = stagers (row metadata 3 tiles ahead and
+// c(L, 1..64) once per run of equal L in the tile, 2 tiles ahead: ~1 load per
+// stager thread per tile instead of 2,048 per-row cost loads on the
+// helpers), the other 12 = helpers (far candidates one tile ahead).
 // Per tile of 32 rows (lane m of warp 0 <-> row 32t+1+m):
 //   far   sources j <= 32(t-1): helper warps one tile ahead; each of the 12
 //         helper warps scans one k-segment of every row (lane m <-> row m),
@@ -55,7 +60,11 @@ template <int kC>
 struct DpMonoSmemT {
   static constexpr int kStage = kC > 1 ? 96 : kDpStageK;
   double ring[kDpRing];              // 32 KB of recent T
-  double cs[3][kStage][32];          // staged c(L_r, 1..kStage), +INF past W_r
+  double cs[kC > 1 ? 3 : 1][kStage][32];   // kC > 1: staged c(L_r, 1..kStage), +INF past W_r
+  double cr[kC > 1 ? 1 : 3][32][64];      // kC == 1: c(L, 1..64) per run of equal L in the tile,
+                                          // +INF past the run's K(L) (W_r = min(K, r) adds only
+                                          // k <= r, which j >= 0 already enforces)
+  int32_t rs[3][32];                      // kC == 1: the run slot of each row
   double Pv[2][kMonoSegs][32];       // CTA 0 helpers' partial minima per segment
   int32_t Pk[2][kMonoSegs][32];
   double Qv[3][32];                  // a peer's merged far-far minimum per row (kC > 1)
@@ -159,8 +168,19 @@ __global__ void __launch_bounds__(kDpThreads, 1)
   const int rank = kC > 1 ? (int)dp_cluster_rank() : 0;
   const int g = kC > 1 ? h + kMonoSegs * (rank - 1) : h;  // this helper warp's far segment
 
+#ifndef SCLS_DP_STAGERS
+#define SCLS_DP_STAGERS 1
+#endif
+  // kC == 1: warps 4, 8, 12 (idle otherwise: SMSP 0 is left to the main
+  // warp) load the row metadata and stage the cost block, so the 12 helper
+  // warps only scan far candidates.
+  constexpr bool kStagers = SCLS_DP_STAGERS && kC == 1;
+  constexpr int kStThreads = 96;
+  const bool stager = kStagers && warp != 0 && (warp & 3) == 0;
+  const int sidx = ((warp >> 2) - 1) * 32 + lane;  // 0..95 in the stager warps
+  const bool meta_thread = kStagers ? (stager && sidx < 32) : (helper && h == 0);
   auto load_meta = [&](int u) {
-    if (h == 0 && u < ntiles) {
+    if (meta_thread && u < ntiles) {
       const int r = (u << 5) + 1 + lane;
       sm.W[u & 3][lane] = r <= n ? Krow[r - 1] : 0;
       sm.CB[u & 3][lane] = r <= n ? cbase[r - 1] : 0;
@@ -195,6 +215,31 @@ __global__ void __launch_bounds__(kDpThreads, 1)
     double v[kPer];
     stage_load(u, v);
     stage_store(u, v);
+  };
+  constexpr int kPerS = (32 * kStage + kStThreads - 1) / kStThreads;
+  auto stage_costs_st = [&](int u) {  // the stager warps' staging of tile u, one row per run
+    if (u >= ntiles) return;
+    const int r = (u << 5) + 1 + lane;
+    const bool okr = r <= n;
+    const int CBm = sm.CB[u & 3][lane];
+    const unsigned heads = __ballot_sync(0xffffffffu, okr && (lane == 0 || sm.CB[u & 3][lane - 1] != CBm));
+    const int last = 31 - __clz(__ballot_sync(0xffffffffu, okr));
+    const int nrun = __popc(heads);
+    const int b = u % 3;
+    if (sidx < 32) sm.rs[b][lane] = okr ? __popc(heads & ((2u << lane) - 1u)) - 1 : 0;
+    for (int e = sidx; e < nrun * 64; e += kStThreads) {
+      const int q = e >> 6, k = (e & 63) + 1;
+      const int h0 = __fns(heads, 0, q + 1);                       // the run's first row
+      const unsigned after = heads & ~((2u << h0) - 1u);
+      const int h1 = after ? __ffs(after) - 2 : last;              // its last row: the largest window
+      const int kq = sm.W[u & 3][h1];
+      sm.cr[b][q][k - 1] = k <= kq ? cost[sm.CB[u & 3][h0] + k] : kInf;
+    }
+  };
+  // c(L_r, k) of this lane's row in tile buffer b (k <= 64); rsl = sm.rs[b][lane]
+  auto csv = [&](int b, int rsl, int k) -> double {
+    if (kStagers) return sm.cr[b][rsl][k - 1];
+    return sm.cs[b][k - 1][lane];
   };
   // This warp's segment g of the far candidates of row r (lane) over the
   // sources j <= jtop (k >= r - jtop): (value, k) lexicographic minimum.
@@ -408,15 +453,21 @@ __global__ void __launch_bounds__(kDpThreads, 1)
     T[0] = 0.0;
     split[0] = 0;
   }
-  if (helper) {
+  if (kStagers ? stager : helper) {
     load_meta(0);
     load_meta(1);
     load_meta(2);
   }
   __syncthreads();
+  if (kStagers && stager) {
+    stage_costs_st(0);
+    stage_costs_st(1);
+  }
   if (helper) {
-    stage_costs(0);
-    stage_costs(1);
+    if (!kStagers) {
+      stage_costs(0);
+      stage_costs(1);
+    }
     for (int m = ht; m < 32; m += kDpHelperThreads) {
       sm.Fv[0][m] = kInf;
       sm.Fk[0][m] = 0;
@@ -431,6 +482,7 @@ __global__ void __launch_bounds__(kDpThreads, 1)
     long long t1 = t0, t2 = t0;
     if (warp == 0) {
       const int cbuf = t % 3;
+      const int rsl = kStagers ? sm.rs[cbuf][lane] : 0;
       const int r = tB + 1 + lane;
       // mid: sources j = tB-31 .. tB (k = lane+32-jj), 4 interleaved chains
       double va[8] = {kInf, kInf, kInf, kInf, kInf, kInf, kInf, kInf};
@@ -442,7 +494,7 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         for (int i = 0; i < 8; ++i) {
           const int jj = c * 8 + i;
           tv[i] = sm.ring[(tB - 31 + jj) & M];
-          cv[i] = sm.cs[cbuf][lane + 31 - jj][lane];
+          cv[i] = csv(cbuf, rsl, lane + 32 - jj);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -467,7 +519,7 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         }
       // rounds
       if (prof) c_mid += clock64() - t0;
-      const double c1 = sm.cs[cbuf][0][lane];
+      const double c1 = csv(cbuf, rsl, 1);
       int p0 = 0;  // first pending lane; frontier a = tB + p0
       const int rows = min(32, n - tB);
       double Ta = sm.ring[tB & M];
@@ -492,7 +544,7 @@ __global__ void __launch_bounds__(kDpThreads, 1)
             const int i = min(i0 + q, p1 - 1);
             tv[q] = sm.ring[(tB + 1 + i) & M];
             const int k = lane - i;
-            cv[q] = sm.cs[cbuf][k >= 1 ? k - 1 : 0][lane];
+            cv[q] = csv(cbuf, rsl, k >= 1 ? k : 1);
           }
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -529,13 +581,21 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         sm.ring[r & M] = acc;
       }
       t1 = t2 = prof ? clock64() : 0;
-    } else if (helper) {
+    } else if (kStagers && stager) {
       load_meta(t + 3);
-      double sv[kPer];
-      stage_load(t + 2, sv);
-      t1 = prof ? clock64() : 0;
-      far(t + 1);
-      stage_store(t + 2, sv);
+      stage_costs_st(t + 2);
+    } else if (helper) {
+      if (kStagers) {
+        t1 = prof ? clock64() : 0;
+        far(t + 1);
+      } else {
+        load_meta(t + 3);
+        double sv[kPer];
+        stage_load(t + 2, sv);
+        t1 = prof ? clock64() : 0;
+        far(t + 1);
+        stage_store(t + 2, sv);
+      }
       t2 = prof ? clock64() : 0;
     }
     __syncthreads();
