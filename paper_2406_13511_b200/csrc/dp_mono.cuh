@@ -174,9 +174,12 @@ __global__ void __launch_bounds__(kDpThreads, 1)
   // kC == 1: warps 4, 8, 12 (idle otherwise: SMSP 0 is left to the main
   // warp) load the row metadata and stage the cost block, so the 12 helper
   // warps only scan far candidates.
+#ifndef SCLS_DP_STAGER_WARPS
+#define SCLS_DP_STAGER_WARPS 3
+#endif
   constexpr bool kStagers = SCLS_DP_STAGERS && kC == 1;
-  constexpr int kStThreads = 96;
-  const bool stager = kStagers && warp != 0 && (warp & 3) == 0;
+  constexpr int kStThreads = 32 * SCLS_DP_STAGER_WARPS;  // warps 4 (, 8, 12)
+  const bool stager = kStagers && warp != 0 && (warp & 3) == 0 && (warp >> 2) <= SCLS_DP_STAGER_WARPS;
   const int sidx = ((warp >> 2) - 1) * 32 + lane;  // 0..95 in the stager warps
   const bool meta_thread = kStagers ? (stager && sidx < 32) : (helper && h == 0);
   auto load_meta = [&](int u) {
