@@ -24,7 +24,7 @@ s = s[:a] + f"""## The bench line ({tag})
 | C5 sweep, traces/s, e2e (host specs in, host results out) | {d['e2e']['value']:,.0f} |
 | CPU reference (oracle/_ref, {cb['cores']} host threads, generate + 3 policies) | {cb['value']:,.0f} |
 | per-policy kernels alone: SCLS / ILS / SLS (they run concurrently in the step) | {k['scls']:.1f} / {k['ils']:.1f} / {k['sls']:.1f} ms |
-| device generation of 43.0M requests | {d['generate_ms_per_step']:.1f} ms |
+| device generation of 43.0M requests | {d.get('generate_ms_per_shard', d.get('generate_ms_per_step')):.1f} ms |
 | C3 requests scheduled/s (1M pool, analytic) | {s3['value'] / 1e6:.2f}M device (DP {s3['phases_ms']['dp']:.1f} ms); CPU reference {cb['scheduler_c3']['value'] / 1e6:.2f}M (1 thread) |
 | C1 (1,010 requests, 1 instance) / C2 (10,053 requests, 8 instances), one trace | {c['C1']['device_ms']:.2f} / {c['C2']['device_ms']:.1f} ms device vs {c['C1']['cpu_reference_ms']:.1f} / {c['C2']['cpu_reference_ms']:.1f} ms CPU (1 thread): a single trace is one serial event chain, on par with one host core |
 | C4 (100,219 requests x 36 configs) | {c['C4']['device_ms']:.0f} ms device vs {c['C4']['cpu_reference_ms']:.0f} ms CPU ({c['C4']['cpu_cores']} threads) |
@@ -35,7 +35,7 @@ open(p, "w").write(s)
 p = os.path.join(ROOT, "DESIGN.md")
 s = open(p).read()
 a, b = s.index("## 8. Measured"), s.index("A single trace is one serial event chain")
-s = s[:a] + f"""## 8. Measured (round 1, 1× B200, 1965 MHz, no throttle reasons)
+s = s[:a] + f"""## 8. Measured (round 2, 1× B200, 1965 MHz, no throttle reasons)
 
 `profiles/{tag}` (full default `python bench.py`), details and kernel
 evidence in `profiles/README.md`:
@@ -43,7 +43,7 @@ evidence in `profiles/README.md`:
 | quantity | B200 | CPU reference, same box |
 |---|---|---|
 | **C5 sweep, simulated traces/s** (4096 traces generated + 3 policies) | **{d['value']:,.0f}** (value, {d['ms_per_step']:.1f} ms/step), **{d['e2e']['value']:,.0f} e2e** | {cb['value']:,.0f} ({cb['cores']} host threads) |
-| per-policy kernels alone, 4096 traces | SCLS {k['scls']:.1f} ms, ILS {k['ils']:.1f} ms, SLS {k['sls']:.1f} ms (concurrent in the step); generation {d['generate_ms_per_step']:.1f} ms | — |
+| per-policy kernels alone, 4096 traces | SCLS {k['scls']:.1f} ms, ILS {k['ils']:.1f} ms, SLS {k['sls']:.1f} ms (concurrent in the step); generation {d.get('generate_ms_per_shard', d.get('generate_ms_per_step')):.1f} ms | — |
 | **C3, requests scheduled/s** (1M pool, analytic) | **{s3['value'] / 1e6:.1f} M** device ({s3['ms_per_call']:.0f} ms: sort {s3['phases_ms']['sort']}, est {s3['phases_ms']['estimate']}, DP {s3['phases_ms']['dp']}, backtrack {s3['phases_ms']['backtrack']}, offload {s3['phases_ms']['offload']}), {s3['e2e_value'] / 1e6:.1f} M e2e | {cb['scheduler_c3']['value'] / 1e6:.2f} M (1 thread, the reference API) |
 | C3 rule table | DP 39 ms | 0.74 s |
 | C1 / C2, one trace | {c['C1']['device_ms']:.2f} / {c['C2']['device_ms']:.1f} ms | {c['C1']['cpu_reference_ms']:.1f} / {c['C2']['cpu_reference_ms']:.1f} ms (1 thread) |
