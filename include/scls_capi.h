@@ -150,7 +150,9 @@ enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT
  * kernels that process the global event order directly (results identical).
  * SCLS_OPT_BATCH_PATH (default 0): batch_requests / schedule take the fused
  * four-launch small-pool path for n <= 4096 and the multi-kernel path above;
- * 1 forces the multi-kernel path at every size (results identical).
+ * 1 forces the multi-kernel path at every size; 2 does that and sorts with
+ * the 8-bit LSD radix sort instead of the eff-bucket sort (results
+ * identical).
  * SCLS_OPT_DP_CLUSTER (default 1): the monotone DP kernel runs as a
  * thread-block cluster of this many CTAs (1, 2 or 4): the older far
  * candidates go to the peer CTAs, exchanged over distributed shared memory

@@ -47,7 +47,7 @@ struct KeyStats {
   int first_infeasible;                 // sorted position, INT_MAX if none
   int k_max;                            // max window over rows
   int n_runs;
-  int pad_;
+  int bucket_overflow;                  // the eff-bucket sort met a bucket above kBucketCap
   long long cost_entries;
 };
 
@@ -71,7 +71,19 @@ __global__ void key_stats_kernel(int64_t n, const int32_t* __restrict__ eff,
     imn = min(imn, __shfl_xor_sync(~0u, imn, o)); imx = max(imx, __shfl_xor_sync(~0u, imx, o));
     amn = min(amn, __shfl_xor_sync(~0u, amn, o)); amx = max(amx, __shfl_xor_sync(~0u, amx, o));
   }
+  // one set of atomics per block (per-warp atomics on six addresses contend)
+  __shared__ uint64_t red[6][32];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
+    red[0][w] = emn; red[1][w] = emx; red[2][w] = imn; red[3][w] = imx; red[4][w] = amn; red[5][w] = amx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < nw; ++q) {
+      emn = min(emn, red[0][q]); emx = max(emx, red[1][q]);
+      imn = min(imn, red[2][q]); imx = max(imx, red[3][q]);
+      amn = min(amn, red[4][q]); amx = max(amx, red[5][q]);
+    }
     atomicMin(&st->eff_min, emn); atomicMax(&st->eff_max, emx);
     atomicMin(&st->id_min, imn); atomicMax(&st->id_max, imx);
     atomicMin(&st->arr_min, amn); atomicMax(&st->arr_max, amx);
@@ -84,6 +96,7 @@ __global__ void init_stats_kernel(KeyStats* st) {
   st->first_infeasible = 0x7fffffff;
   st->k_max = 0;
   st->n_runs = 0;
+  st->bucket_overflow = 0;
   st->cost_entries = 0;
 }
 
@@ -253,52 +266,67 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
   SCLS_CUDA(cudaStreamSynchronize(s));
   const KeyStats ks = *hst;
 
-  // ---- 2. stable LSD sort by (eff, arrival, id)
+  // ---- 2. sort by (eff, arrival, id): eff buckets sorted in shared memory,
+  //         or the stable LSD radix sort field by field
   uint64_t* keys = (uint64_t*)ctx->buf(kSlotKeys, sizeof(uint64_t) * n);
   uint64_t* keys2 = (uint64_t*)ctx->buf(kSlotKeysAlt, sizeof(uint64_t) * n);
   int32_t* vals = (int32_t*)ctx->buf(kSlotVals, sizeof(int32_t) * n);
   int32_t* vals2 = (int32_t*)ctx->buf(kSlotValsAlt, sizeof(int32_t) * n);
   if (!keys || !keys2 || !vals || !vals2) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
-  bool identity = true;
-  struct FieldPlan {
-    Field f;
-    uint64_t lo, hi;
-  } plan[3] = {{kFieldId, ks.id_min, ks.id_max},
-               {kFieldArrival, ks.arr_min, ks.arr_max},
-               {kFieldEff, ks.eff_min, ks.eff_max}};
-  for (const FieldPlan& fp : plan) {
-    const int bits = bit_width(fp.hi - fp.lo);
-    if (bits == 0) continue;
-    switch (fp.f) {
-      case kFieldId:
-        gather_key_kernel<kFieldId><<<grid_n, threads, 0, s>>>(n, vals, in.eff, in.id, in.arrival,
-                                                               fp.lo, keys, identity, vals);
-        break;
-      case kFieldArrival:
-        gather_key_kernel<kFieldArrival><<<grid_n, threads, 0, s>>>(n, vals, in.eff, in.id,
-                                                                    in.arrival, fp.lo, keys,
-                                                                    identity, vals);
-        break;
-      default:
-        gather_key_kernel<kFieldEff><<<grid_n, threads, 0, s>>>(n, vals, in.eff, in.id, in.arrival,
-                                                                fp.lo, keys, identity, vals);
-        break;
+  auto lsd_sort = [&]() -> scls_status {
+    bool identity = true;
+    struct FieldPlan {
+      Field f;
+      uint64_t lo, hi;
+    } plan[3] = {{kFieldId, ks.id_min, ks.id_max},
+                 {kFieldArrival, ks.arr_min, ks.arr_max},
+                 {kFieldEff, ks.eff_min, ks.eff_max}};
+    for (const FieldPlan& fp : plan) {
+      const int bits = bit_width(fp.hi - fp.lo);
+      if (bits == 0) continue;
+      switch (fp.f) {
+        case kFieldId:
+          gather_key_kernel<kFieldId><<<grid_n, threads, 0, s>>>(n, vals, in.eff, in.id, in.arrival,
+                                                                 fp.lo, keys, identity, vals);
+          break;
+        case kFieldArrival:
+          gather_key_kernel<kFieldArrival><<<grid_n, threads, 0, s>>>(n, vals, in.eff, in.id,
+                                                                      in.arrival, fp.lo, keys,
+                                                                      identity, vals);
+          break;
+        default:
+          gather_key_kernel<kFieldEff><<<grid_n, threads, 0, s>>>(n, vals, in.eff, in.id, in.arrival,
+                                                                  fp.lo, keys, identity, vals);
+          break;
+      }
+      SCLS_LAUNCHED();
+      identity = false;
+      bool swapped = false;
+      scls_status stt = radix_sort_pairs(ctx, n, keys, vals, keys2, vals2, 0, bits, &swapped);
+      if (stt) return stt;
+      if (swapped) {
+        std::swap(keys, keys2);
+        std::swap(vals, vals2);
+      }
     }
-    SCLS_LAUNCHED();
-    identity = false;
-    bool swapped = false;
-    scls_status stt = radix_sort_pairs(ctx, n, keys, vals, keys2, vals2, 0, bits, &swapped);
-    if (stt) return stt;
-    if (swapped) {
-      std::swap(keys, keys2);
-      std::swap(vals, vals2);
+    if (identity) {
+      // Every key field constant: the order is the input order.
+      gather_key_kernel<kFieldEff><<<grid_n, threads, 0, s>>>(n, vals, in.eff, in.id, in.arrival, 0,
+                                                              keys, true, vals);
+      SCLS_LAUNCHED();
     }
-  }
-  if (identity) {
-    // Every key field constant: the order is the input order.
-    gather_key_kernel<kFieldEff><<<grid_n, threads, 0, s>>>(n, vals, in.eff, in.id, in.arrival, 0,
-                                                            keys, true, vals);
-    SCLS_LAUNCHED();
+    return SCLS_OK;
+  };
+  const uint64_t erange = ks.eff_max - ks.eff_min;
+  const bool bucketed = !ctx->force_lsd_sort && erange < (uint64_t)kBucketMaxBins;
+  if (bucketed) {
+    const int32_t emin = (int32_t)((uint32_t)ks.eff_min ^ 0x80000000u);
+    scls_status stt0 = bucket_sort_perm(ctx, n, in.eff, in.arrival, in.id, emin, (int32_t)erange + 1, vals,
+                                        &st->bucket_overflow);
+    if (stt0) return stt0;
+  } else {
+    scls_status stt0 = lsd_sort();
+    if (stt0) return stt0;
   }
   const int32_t* perm = vals;
   SCLS_CUDA(cudaEventRecord(ctx->ev[1], s));
@@ -309,12 +337,27 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
   int32_t* flag = (int32_t*)ctx->buf(kSlotFlag, sizeof(int32_t) * n);
   int32_t* run_excl = (int32_t*)ctx->buf(kSlotRunIdx, sizeof(int32_t) * n);
   if (!Lrow || !Krow || !flag || !run_excl) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
-  rows_kernel<<<grid_n, threads, 0, s>>>(n, perm, in.eff, in.slice_len, mem, Lrow, Krow, flag, st);
-  SCLS_LAUNCHED();
-  scls_status stt = scan_exclusive(ctx, n, flag, run_excl, &st->n_runs);
+  auto rows_pass = [&]() -> scls_status {
+    rows_kernel<<<grid_n, threads, 0, s>>>(n, perm, in.eff, in.slice_len, mem, Lrow, Krow, flag, st);
+    SCLS_LAUNCHED();
+    scls_status st2 = scan_exclusive(ctx, n, flag, run_excl, &st->n_runs);
+    if (st2) return st2;
+    SCLS_CUDA(cudaMemcpyAsync(hst, st, sizeof(KeyStats), cudaMemcpyDeviceToHost, s));
+    SCLS_CUDA(cudaStreamSynchronize(s));
+    return SCLS_OK;
+  };
+  scls_status stt = rows_pass();
   if (stt) return stt;
-  SCLS_CUDA(cudaMemcpyAsync(hst, st, sizeof(KeyStats), cudaMemcpyDeviceToHost, s));
-  SCLS_CUDA(cudaStreamSynchronize(s));
+  if (bucketed && hst->bucket_overflow) {
+    // an eff bucket beyond kBucketCap: redo the order with the LSD sort
+    init_stats_kernel<<<1, 1, 0, s>>>(st);
+    SCLS_LAUNCHED();
+    stt = lsd_sort();
+    if (stt) return stt;
+    perm = vals;
+    stt = rows_pass();
+    if (stt) return stt;
+  }
   if (hst->first_infeasible != 0x7fffffff) {
     // batcher.cpp:40-46: InfeasibleRequestError for the first offender.
     int32_t idx = 0;

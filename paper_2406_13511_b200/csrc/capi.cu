@@ -240,6 +240,7 @@ scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value) {
   }
   if (option == SCLS_OPT_BATCH_PATH) {
     ctx->force_large_path = value != 0;
+    ctx->force_lsd_sort = value == 2;
     return SCLS_OK;
   }
   return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "unknown option");

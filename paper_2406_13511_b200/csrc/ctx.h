@@ -32,6 +32,7 @@ struct scls_ctx {
   bool ils_lockstep = false;              // metrics-only ILS: the lock-step kernel instead of independent lanes
   cudaStream_t side[3] = {};              // forked streams for those launches (created on first use)
   bool force_large_path = false;          // batch_requests: the multi-kernel path even for small pools (tests)
+  bool force_lsd_sort = false;            // batch_requests: the LSD radix sort instead of the eff-bucket sort
   void* comm = nullptr;                   // ncclComm_t of scls_comm_init (multi.cu)
   int world = 1, rank = 0;
 
@@ -56,6 +57,7 @@ namespace scls {
 enum ScratchSlot : int {
   kSlotRadixCounts = 30,
   kSlotRadixOffs = 31,
+  kSlotBucket = 32,   // 32..35: eff-bucket sort
   kSlotScan = 40,     // 40..55: two per recursion level
   kSlotStage = 60,    // 60..79: host<->device staging of entry-point arguments
   kSlotSim = 80,      // 80..109: simulator

@@ -7,6 +7,7 @@
 // (per-warp smem counters) + earlier peers in the round; warps are then
 // prefixed per digit.  Tile = 8 warps x 256 = 2048 elements.
 #include "radix.cuh"
+#include "scls_common.cuh"
 
 namespace scls {
 namespace {
@@ -151,6 +152,180 @@ __global__ void total_kernel(const int32_t* __restrict__ in, const int32_t* __re
   *total = n ? ex[n - 1] + in[n - 1] : 0;
 }
 
+
+// ---- eff-bucket sort ------------------------------------------------------
+
+__device__ __forceinline__ uint64_t eb_bias64(int64_t x) { return (uint64_t)x ^ 0x8000000000000000ull; }
+
+// Histogram of eff - emin.  Small bin counts (<= kEbSmemBins): a shared
+// histogram per block of kEbChunk elements, then one global add per bin per
+// block; larger ranges: warp-aggregated global adds.
+constexpr int kEbSmemBins = 8192;
+constexpr int kEbChunk = 16384;
+__global__ void __launch_bounds__(512) ebucket_hist_kernel(int64_t n, const int32_t* __restrict__ eff, int32_t emin,
+                                                           int32_t nbins, int32_t* __restrict__ counts) {
+  __shared__ int32_t h[kEbSmemBins];
+  const int64_t lo = (int64_t)blockIdx.x * kEbChunk, hi = min(n, lo + kEbChunk);
+  if (nbins <= kEbSmemBins) {
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&h[eff[i] - emin], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+      if (h[b]) atomicAdd(&counts[b], h[b]);
+    return;
+  }
+  for (int64_t base = lo; base < hi; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool ok = i < hi;
+    const int b = ok ? eff[i] - emin : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    if (ok && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[b], __popc(peers));
+  }
+}
+
+// One CTA: exclusive offsets of <= kBucketMaxBins counts, a cursor copy, and
+// the overflow flag for buckets beyond kBucketCap.
+__global__ void __launch_bounds__(1024) ebucket_scan_kernel(int32_t nbins, const int32_t* __restrict__ counts,
+                                                            int32_t* __restrict__ offs,
+                                                            int32_t* __restrict__ cursor,
+                                                            int32_t* __restrict__ overflow) {
+  __shared__ int32_t ws[32];
+  const int per = (nbins + 1023) / 1024;
+  const int b0 = threadIdx.x * per;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int sum = 0, mx = 0;
+  for (int q = 0; q < per; ++q) {
+    const int b = b0 + q;
+    if (b < nbins) {
+      const int c = counts[b];
+      sum += c;
+      mx = max(mx, c);
+    }
+  }
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) ws[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const int v = ws[lane];
+    int vi = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, vi, o);
+      if (lane >= o) vi += y;
+    }
+    ws[lane] = vi - v;
+  }
+  __syncthreads();
+  int run = ws[w] + incl - sum;
+  for (int q = 0; q < per; ++q) {
+    const int b = b0 + q;
+    if (b < nbins) {
+      offs[b] = run;
+      cursor[b] = run;
+      run += counts[b];
+    }
+  }
+  if (mx > kBucketCap) *overflow = 1;
+}
+
+// Scatter positions into their eff buckets.  Small bin counts: a block
+// reserves each bin's range for its kEbChunk elements with one global add,
+// then ranks locally in shared memory (the order inside a bucket does not
+// matter: the bucket sort's last key is the position).
+__global__ void __launch_bounds__(512) ebucket_scatter_kernel(int64_t n, const int32_t* __restrict__ eff, int32_t emin,
+                                                              int32_t nbins, int32_t* __restrict__ cursor,
+                                                              int32_t* __restrict__ idx) {
+  __shared__ int32_t h[kEbSmemBins];
+  const int64_t lo = (int64_t)blockIdx.x * kEbChunk, hi = min(n, lo + kEbChunk);
+  const int lane = threadIdx.x & 31;
+  if (nbins <= kEbSmemBins) {
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&h[eff[i] - emin], 1);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+      if (h[b]) h[b] = atomicAdd(&cursor[b], h[b]);
+    __syncthreads();
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) idx[atomicAdd(&h[eff[i] - emin], 1)] = (int32_t)i;
+    return;
+  }
+  for (int64_t base = lo; base < hi; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool ok = i < hi;
+    const int b = ok ? eff[i] - emin : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    const int leader = __ffs(peers) - 1;
+    int at = 0;
+    if (ok && lane == leader) at = atomicAdd(&cursor[b], __popc(peers));
+    at = __shfl_sync(0xffffffffu, at, leader);
+    if (ok) idx[at + __popc(peers & ((1u << lane) - 1u))] = (int32_t)i;
+  }
+}
+
+// One CTA per bucket (grid-stride): gather (ordered_bits(arrival),
+// bias64(id), position), bitonic sort in shared memory, write the positions.
+constexpr int kEbThreads = 512;
+__global__ void __launch_bounds__(kEbThreads) ebucket_sort_kernel(int32_t nbins, const int32_t* __restrict__ counts,
+                                                                  const int32_t* __restrict__ offs,
+                                                                  const int32_t* __restrict__ idx,
+                                                                  const double* __restrict__ arr,
+                                                                  const int64_t* __restrict__ id,
+                                                                  int32_t* __restrict__ perm) {
+  __shared__ uint64_t ka[kBucketCap], ki[kBucketCap];
+  __shared__ uint32_t kx[kBucketCap];
+  const int tid = threadIdx.x;
+  for (int b = blockIdx.x; b < nbins; b += gridDim.x) {
+    const int c = counts[b];
+    if (c == 0 || c > kBucketCap) continue;
+    const int o = offs[b];
+    if (c == 1) {
+      if (tid == 0) perm[o] = idx[o];
+      continue;
+    }
+    int P = 2;
+    while (P < c) P <<= 1;
+    for (int q = tid; q < P; q += kEbThreads) {
+      if (q < c) {
+        const int x = idx[o + q];
+        ka[q] = ordered_bits(arr[x]);
+        ki[q] = eb_bias64(id[x]);
+        kx[q] = (uint32_t)x;
+      } else {
+        ka[q] = ki[q] = ~0ull;
+        kx[q] = ~0u;
+      }
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = tid; t < (P >> 1); t += kEbThreads) {
+          const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), h = i + j;  // j is a power of two
+          const uint64_t a0 = ka[i], a1 = ka[h], i0 = ki[i], i1 = ki[h];
+          const uint32_t x0 = kx[i], x1 = kx[h];
+          const bool gt = a0 > a1 || (a0 == a1 && (i0 > i1 || (i0 == i1 && x0 > x1)));
+          if (gt == ((i & k) == 0)) {  // ascending blocks swap a greater first element
+            ka[i] = a1;
+            ka[h] = a0;
+            ki[i] = i1;
+            ki[h] = i0;
+            kx[i] = x1;
+            kx[h] = x0;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int q = tid; q < c; q += kEbThreads) perm[o + q] = (int32_t)kx[q];
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 static scls_status scan_level(scls_ctx* ctx, int64_t n, const int32_t* in, int32_t* out,
@@ -209,6 +384,30 @@ scls_status radix_sort_pairs(scls_ctx* ctx, int64_t n, uint64_t* keys, int32_t* 
     int32_t* tv = vi; vi = vo; vo = tv;
     *swapped = !*swapped;
   }
+  return SCLS_OK;
+}
+
+scls_status bucket_sort_perm(scls_ctx* ctx, int64_t n, const int32_t* eff, const double* arr,
+                             const int64_t* id, int32_t eff_min, int32_t nbins, int32_t* perm,
+                             int32_t* d_overflow) {
+  if (nbins < 1 || nbins > kBucketMaxBins) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "eff range");
+  cudaStream_t s = ctx->stream;
+  int32_t* counts = (int32_t*)ctx->buf(kSlotBucket + 0, sizeof(int32_t) * nbins);
+  int32_t* offs = (int32_t*)ctx->buf(kSlotBucket + 1, sizeof(int32_t) * nbins);
+  int32_t* cursor = (int32_t*)ctx->buf(kSlotBucket + 2, sizeof(int32_t) * nbins);
+  int32_t* idx = (int32_t*)ctx->buf(kSlotBucket + 3, sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1));
+  if (!counts || !offs || !cursor || !idx) return set_error(ctx, SCLS_ERR_CUDA, "scratch allocation failed");
+  SCLS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * nbins, s));
+  const int grid = (int)div_up(n, kEbChunk);
+  ebucket_hist_kernel<<<grid, 512, 0, s>>>(n, eff, eff_min, nbins, counts);
+  SCLS_LAUNCHED();
+  ebucket_scan_kernel<<<1, 1024, 0, s>>>(nbins, counts, offs, cursor, d_overflow);
+  SCLS_LAUNCHED();
+  ebucket_scatter_kernel<<<grid, 512, 0, s>>>(n, eff, eff_min, nbins, cursor, idx);
+  SCLS_LAUNCHED();
+  ebucket_sort_kernel<<<std::min(nbins, ctx->sm_count * 8), kEbThreads, 0, s>>>(nbins, counts, offs, idx, arr, id,
+                                                                                perm);
+  SCLS_LAUNCHED();
   return SCLS_OK;
 }
 

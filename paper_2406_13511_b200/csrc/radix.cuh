@@ -18,6 +18,19 @@ scls_status radix_sort_pairs(scls_ctx* ctx, int64_t n, uint64_t* keys, int32_t* 
 scls_status scan_exclusive(scls_ctx* ctx, int64_t n, const int32_t* in, int32_t* out,
                            int32_t* d_total);
 
+// Sort permutation of a pool by (eff, arrival, id) -- the order of the stable
+// LSD path on (bias32(eff), ordered_bits(arrival), bias64(id)), input position
+// last -- through eff buckets: a counting scatter by eff (one histogram, one
+// scan, one scatter), then one CTA per bucket sorting (arrival, id, position)
+// bitonically in shared memory.  For eff ranges of at most kBucketMaxBins
+// values.  A bucket larger than kBucketCap sets *d_overflow (device int) and
+// leaves its part of perm unwritten; the caller then uses the LSD sort.
+constexpr int kBucketMaxBins = 1 << 16;
+constexpr int kBucketCap = 2048;
+scls_status bucket_sort_perm(scls_ctx* ctx, int64_t n, const int32_t* eff, const double* arr,
+                             const int64_t* id, int32_t eff_min, int32_t nbins, int32_t* perm,
+                             int32_t* d_overflow);
+
 // Number of significant bits of v (0 for v == 0).
 inline int bit_width(uint64_t v) { return v ? 64 - __builtin_clzll(v) : 0; }
 

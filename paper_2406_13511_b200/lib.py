@@ -196,8 +196,9 @@ class Context:
         self._check(self.lib.scls_set_option(self.h, 4, 1 if on else 0))
 
     def set_batch_path(self, large):
-        """SCLS_OPT_BATCH_PATH: 1 forces the multi-kernel batch_requests path for small pools too."""
-        self._check(self.lib.scls_set_option(self.h, 5, 1 if large else 0))
+        """SCLS_OPT_BATCH_PATH: 1 forces the multi-kernel batch_requests path for small pools too;
+        2 also replaces the eff-bucket sort by the LSD radix sort."""
+        self._check(self.lib.scls_set_option(self.h, 5, int(large) if not isinstance(large, bool) else int(large)))
 
     def set_dp_cluster(self, ctas):
         """SCLS_OPT_DP_CLUSTER: CTAs per monotone-DP cluster (1, 2 or 4; default 1)."""

@@ -345,3 +345,37 @@ def test_dp_cluster_sizes_bit_exact(ctx, orc, golden, ctas):
                 assert_same_batches(a, b, (ctas, n, mname))
     finally:
         ctx.set_dp_cluster(1)
+
+
+def test_bucket_sort_matches_lsd_sort(ctx, orc):
+    """The eff-bucket sort (default for eff ranges <= 2^16) and the LSD radix
+    sort (SCLS_OPT_BATCH_PATH 2) give the same batches as the oracle:
+    uniform and skewed eff, a bucket above the shared-memory cap (the
+    overflow fallback), eff ranges beyond 2^16 (LSD directly), equal and
+    +-0.0 arrivals, duplicate and negative ids."""
+    lat = capi.builtin_latency_model()
+    rng = np.random.default_rng(17)
+    cases = []
+    n = 50000
+    cases.append((rng.integers(1, 1025, n), rng.random(n) * 100, rng.permutation(n)))           # C3-like
+    e = rng.integers(1, 1025, n)
+    e[: n // 5] = 77                                                                              # 10k in one bucket
+    cases.append((e, rng.random(n) * 100, rng.permutation(n)))
+    cases.append((rng.integers(1, 200000, n), rng.random(n) * 100, rng.permutation(n)))       # range > 2^16
+    a = np.round(rng.random(n) * 10, 1)
+    a[::7] = 0.0
+    a[1::7] = -0.0
+    cases.append((rng.integers(1, 300, n), a, rng.integers(-50, 50, n)))                      # ties, dup ids
+    for i, (eff, arr, ids) in enumerate(cases):
+        eff = eff.astype(np.int32)
+        arr = np.asarray(arr, np.float64)
+        ids = np.asarray(ids, np.int64)
+        want = orc.batch_requests(eff, arr, ids, 128, lat, MEMORIES["rule"]())
+        for path in (0, 2):
+            ctx.set_batch_path(path)
+            try:
+                got = ctx.batch_requests(eff, arr, ids, 128, lat, MEMORIES["rule"]())
+            finally:
+                ctx.set_batch_path(0)
+            assert_same_batches(got, want, (i, path))
+            assert np.array_equal(ids[got["order"]], got["member_id"])
