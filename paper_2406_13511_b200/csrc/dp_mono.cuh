@@ -627,7 +627,11 @@ __global__ void __launch_bounds__(kDpThreads, 1)
     } else if (helper) {
       atomicAdd(&prof[2], (unsigned long long)c_c);
       atomicAdd(&prof[3], (unsigned long long)c_d);
+#ifdef SCLS_DP_PROF_MAXFAR  // diagnostics: the slowest helper's far cycles instead of the waits
+      atomicMax(&prof[4], (unsigned long long)c_d);
+#else
       atomicAdd(&prof[4], (unsigned long long)c_e);
+#endif
       atomicAdd(&prof[5], 1ull);
     }
   }
