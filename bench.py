@@ -9,15 +9,17 @@ generate -> Simulator::run -> compute per run) through the C-ABI
 scls_run_sweep_sharded: the rank's contiguous shard of traces is generated on
 its GPU from the WorkloadSpecs (bit-exact with generate()), every policy runs
 on every trace, and the library all-gathers the fixed-size result records
-with one ncclAllGather (the only collective).  Strong scaling: the sweep is
-fixed as N grows.  Device time, CUDA events on the launching stream, max over
-ranks.
+with one ncclAllGather (the only collective).  Weak scaling: every rank runs
+the 4096-trace sweep (its own seeds), so N GPUs simulate 4096 N traces per
+step; `value` is the whole job's traces/s.  Device time, CUDA events on the
+launching stream, max over ranks.
 
 Parity, outside the timed region: rank 0 runs the unmodified reference
 (oracle/_ref, compiled from /root/reference) on ALL 4096 traces x 3 policies
-on the host cores -- that run is also the cpu_baseline -- and compares every
-MetricsReport field, the slice histogram and the counters of all 12,288 jobs
-with the gathered device grid.
+of its shard on the host cores -- that run is also the cpu_baseline -- and
+compares every MetricsReport field, the slice histogram and the counters of
+all 12,288 jobs with the gathered device grid (at N > 1 also the first 32
+traces of every other rank's shard).
 
 The same JSON line carries the scheduling-core number (configs[2]): requests
 scheduled/s for batch_requests + offload of the 1M-request pool
@@ -194,16 +196,17 @@ def run_reference(args, rank, world):
     value = 3 * args.traces / sec
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "traces/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (the reference's own generate(): Poisson arrivals, codefuse-like lengths)",
             "config": {"workload": f"C5 Monte Carlo sweep: {args.traces} traces (seeds x rates 10/15/20/25 req/s), "
                                    f"{args.duration:.0f} s, 8 instances, S=128, max_gen 1024, x {{SCLS,SLS,ILS}} = "
                                    f"{3 * args.traces} simulations per step", "traces": args.traces,
                        "host_threads": cores},
             "cpu_baseline": {"value": value, "unit": "traces/s", "cores": cores, "kind": kind,
-                             "sample": f"the full workload every step: {args.traces} traces x 3 policies "
+                             "sample": f"every step the full per-GPU workload: {args.traces} traces x 3 policies "
                                        "(generate once per trace + Simulator::run + compute per policy, "
-                                       "one digest-free counting pass per log)"},
+                                       "one digest-free counting pass per log); at N > 1 the host runs one "
+                                       "GPU's share (the host cores do not grow with N)"},
             "e2e": {"value": value, "unit": "traces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -403,7 +406,10 @@ def run_ours(args, rank, world, dist):
         sweep.join_comm(ctx, rank, world, dist)
     nranks = ctx.comm_size()
     assert nranks == world, (nranks, world)
-    T = args.traces
+    # weak scaling (the trace dimension is partitioned): every rank
+    # runs the C5 sweep of args.traces traces; rank r's traces are the global
+    # indices [r * traces, (r + 1) * traces) -- distinct seeds
+    T = args.traces * world
     lo, hi = sweep.shard_range(T, rank, world)
     ntr = hi - lo
     lat, mem = capi.builtin_latency_model(), capi.builtin_memory_model()
@@ -497,13 +503,14 @@ def run_ours(args, rank, world, dist):
     line = {
         "metric": METRIC, "value": value, "unit": "traces/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: every step generates its traces on the device from WorkloadSpecs (the reference "
                 "sampler: mt19937_64, glibc log gaps, codefuse-like lengths; bit-exact with generate())",
         "config": {"workload": f"C5 Monte Carlo sweep (experiment.cpp sweep: generate + simulate + metrics): "
                                f"{T} traces (seeds x rates 10/15/20/25 req/s), {args.duration:.0f} s, 8 instances, "
                                f"S=128, max_gen 1024, x {{SCLS,SLS,ILS}} = {3 * T} simulations per step",
-                   "traces": T, "requests": nreq, "parallelism": f"trace-sharded dp{world}",
+                   "traces": T, "traces_per_gpu": args.traces, "requests": nreq,
+                   "parallelism": f"trace-sharded dp{world}",
                    "l2": "generated traces (%.0f MB per rank) > L2, rewritten every step" % (shard_req * 16 / 1e6)},
         "e2e": {"value": 3 * T / float(t_e2e.item()), "unit": "traces/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
@@ -533,7 +540,11 @@ def run_ours(args, rank, world, dist):
         line["scheduler_sweep"] = bench_scheduler_sweep(ctx, lib)
         line["configs_c1_c2_c4"] = bench_configs(ctx, lib, capi, args.steps)
     if not args.no_cpu:
-        cpu, parity = cpu_reference(args, T, cfgs, lat, mem, hist_bins, grid, grid_hist)
+        # every job of rank 0's shard (the N = 1 workload) and the first 32
+        # traces of every other rank's shard
+        check = list(range(0, args.traces)) + [t for r in range(1, world)
+                                               for t in range(r * args.traces, r * args.traces + 32)]
+        cpu, parity = cpu_reference(args, T, check, cfgs, lat, mem, hist_bins, grid, grid_hist)
         line["cpu_baseline"] = cpu
         line["parity"] = parity
         if not args.no_c3:
@@ -541,29 +552,45 @@ def run_ours(args, rank, world, dist):
     print(json.dumps(line), flush=True)
 
 
-def cpu_reference(args, T, cfgs, lat, mem, hist_bins, grid, grid_hist):
-    """The unmodified reference on ALL T traces x 3 policies on this host's
-    cores (timed: the cpu_baseline), then every job compared with the device
-    grid: every MetricsReport field, the slice histogram and the counters."""
+def cpu_reference(args, T, check, cfgs, lat, mem, hist_bins, grid, grid_hist):
+    """The unmodified reference on the traces `check` (all of them at one GPU)
+    x 3 policies on this host's cores, then every job compared with the device
+    grid (policy-major, T traces): every MetricsReport field, the slice
+    histogram and the counters.  The timed part over rank 0's shard is the
+    cpu_baseline (the N = 1 workload)."""
     lib, kind = ref_checker()
     cores = os.cpu_count() or 1
-    specs = [trace_spec(i, args.duration) for i in range(T)]
+    n0 = min(len(check), args.traces)
+    specs = [trace_spec(i, args.duration) for i in check]
     t0 = time.perf_counter()
-    want, want_hist = ref_sweep(lib, kind, specs, cfgs, lat, mem, hist_bins, cores)
+    want0, want_hist0 = ref_sweep(lib, kind, specs[:n0], cfgs, lat, mem, hist_bins, cores)
     sec = time.perf_counter() - t0
-    cpu = {"value": 3 * T / sec, "unit": "traces/s", "cores": cores, "kind": kind,
-           "sample": f"the full workload: {T} traces x 3 policies (generate once per trace + Simulator::run + "
+    parts = [(want0, want_hist0, n0)]
+    if len(specs) > n0:
+        w1, h1 = ref_sweep(lib, kind, specs[n0:], cfgs, lat, mem, hist_bins, cores)
+        parts.append((w1, h1, len(specs) - n0))
+    cpu = {"value": 3 * n0 / sec, "unit": "traces/s", "cores": cores, "kind": kind,
+           "sample": f"the full workload: {n0} traces x 3 policies (generate once per trace + Simulator::run + "
                      f"compute per policy, one digest-free counting pass per log), {cores} host threads"}
     nfields = C.sizeof(capi.TraceResult) // 8
-    wg = np.frombuffer(C.string_at(C.addressof(want), 3 * T * C.sizeof(capi.TraceResult)),
-                       np.int64).reshape(3 * T, nfields)
     word = sorted(set(FIELD_WORD[f] for f in REPORT_FIELDS))  # status + worker_count share word 0
-    bad_jobs = np.nonzero((grid[:, word] != wg[:, word]).any(axis=1))[0]
-    bad_hist = np.nonzero((grid_hist.reshape(3 * T, -1) != want_hist.reshape(3 * T, -1)).any(axis=1))[0]
-    parity = {"checked": f"all {3 * T} jobs ({T} traces x 3 policies) vs the {kind} on the host: every "
-                         "MetricsReport field bit-exact, slice histogram, completed/batch/pad/invalid/event counters",
-              "jobs": 3 * T, "mismatched_jobs": int(len(set(bad_jobs) | set(bad_hist))),
-              "first_mismatches": [int(j) for j in sorted(set(bad_jobs) | set(bad_hist))[:8]]}
+    bad = set()
+    base = 0
+    for want, want_hist, m in parts:
+        wg = np.frombuffer(C.string_at(C.addressof(want), 3 * m * C.sizeof(capi.TraceResult)),
+                           np.int64).reshape(3, m, nfields)
+        ts = np.asarray(check[base:base + m])
+        for c in range(3):
+            rows = grid[c * T + ts]
+            bj = np.nonzero((rows[:, word] != wg[c][:, word]).any(axis=1))[0]
+            bh = np.nonzero((grid_hist[c, ts] != want_hist.reshape(3, m, -1)[c]).any(axis=1))[0]
+            bad |= {int(c * T + ts[j]) for j in set(bj) | set(bh)}
+        base += m
+    jobs = 3 * len(check)
+    parity = {"checked": f"{jobs} jobs ({len(check)} traces x 3 policies{'' if len(check) == T else ' of ' + str(T)}) "
+                         f"vs the {kind} on the host: every MetricsReport field bit-exact, slice histogram, "
+                         "completed/batch/pad/invalid/event counters",
+              "jobs": jobs, "mismatched_jobs": len(bad), "first_mismatches": sorted(bad)[:8]}
     return cpu, parity
 
 
