@@ -167,6 +167,22 @@ scls_status scls_debug_dp_profile(scls_ctx* ctx, int32_t enable, uint64_t out[8]
 
 /* ---- validation (host only; mirrors the reference validators) ----------- */
 scls_status scls_validate_latency(const scls_latency* m);   /* cost_model.cpp:70-87    */
+/* cost_model.h:45-50 ProfileSample (phase 0 = prefill, 1 = decode). */
+typedef struct scls_profile_sample {
+  int32_t phase;
+  int32_t batch_size;
+  int32_t length;
+  int32_t pad_;
+  double latency_s;
+} scls_profile_sample;
+/* cost_model.cpp:96-160 fit (cost_model.h:80): least squares of the prefill
+ * and decode surfaces c1*n*l + c2*n + c3*l + c4 by column-pivoting Householder
+ * QR, rmse per phase, then validate.  Host computation (a 4-parameter
+ * problem).  SCLS_ERR_INSUFFICIENT_SAMPLES with the reference's messages
+ * (fewer than 4 samples / 2 sizes / 2 lengths in a phase, or rank < 4);
+ * SCLS_ERR_DEGENERATE_MODEL when the fitted model fails validate. */
+scls_status scls_fit_latency(const scls_profile_sample* samples, int64_t n, int32_t n_cap, int32_t l_cap,
+                             scls_latency* out);
 scls_status scls_validate_memory(const scls_memory* m);     /* memory_model.cpp:92-120 */
 scls_status scls_validate_sched(const scls_sched_cfg* cfg); /* sched_policies.cpp:45-57 */
 

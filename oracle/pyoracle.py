@@ -247,6 +247,25 @@ class RefLib(_Checker):
         return res, hist[:ntr * nc * hist_bins].reshape(nc, ntr, hist_bins)
 
 
+def _ref_fit(self, samples, n_cap=64, l_cap=4096):
+    """ref_fit_latency: the reference's own fit (cost_model.cpp:140-160)."""
+    fn = self.lib.ref_fit_latency
+    fn.restype = C.c_int32
+    rows = list(samples)
+    arr = (capi.ProfileSample * max(len(rows), 1))()
+    for i, (ph, n, l, t) in enumerate(rows):
+        arr[i].phase = {"prefill": 0, "decode": 1}.get(ph, ph)
+        arr[i].batch_size, arr[i].length, arr[i].latency_s = n, l, t
+    out = capi.Latency()
+    st = fn(arr, C.c_int64(len(rows)), n_cap, l_cap, C.byref(out))
+    if st:
+        self._raise(st)
+    return out
+
+
+RefLib.fit_latency = _ref_fit
+
+
 class OracleLib(_Checker):
     prefix = "orc_"
 

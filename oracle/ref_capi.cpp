@@ -269,6 +269,27 @@ double ref_next_interval(double lambda, double gamma, double min_load) {
   return S::next_interval(lambda, gamma, min_load);
 }
 
+// cost_model.cpp:140-160 fit, the reference's own (built here against the
+// Eigen stand-in of oracle/ref_shims): the checker of scls_fit_latency.
+scls_status ref_fit_latency(const scls_profile_sample* s, int64_t n, int32_t n_cap, int32_t l_cap,
+                            scls_latency* out) {
+  try {
+    std::vector<S::ProfileSample> v(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      v[i].phase = s[i].phase == 0 ? S::Phase::kPrefill : S::Phase::kDecode;
+      v[i].batch_size = s[i].batch_size;
+      v[i].length = s[i].length;
+      v[i].latency_s = s[i].latency_s;
+    }
+    const S::LatencyModel m = S::fit(v, n_cap, l_cap);
+    *out = scls_latency{m.p1, m.p2, m.p3, m.p4, m.d1, m.d2, m.d3, m.d4, m.rmse_prefill, m.rmse_decode,
+                        m.n_cap, m.l_cap};
+    return SCLS_OK;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
 scls_status ref_validate_latency(const scls_latency* m) {
   try { S::validate(to_ref(*m)); return SCLS_OK; } catch (...) { return map_exception(); }
 }

@@ -59,6 +59,12 @@ class Latency(C.Structure):
         ("n_cap", C.c_int32), ("l_cap", C.c_int32)]
 
 
+class ProfileSample(C.Structure):
+    """cost_model.h:45-50 (phase 0 prefill, 1 decode)."""
+    _fields_ = [("phase", C.c_int32), ("batch_size", C.c_int32), ("length", C.c_int32), ("pad_", C.c_int32),
+                ("latency_s", C.c_double)]
+
+
 class Memory(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n_rules", C.c_int32),
                 ("m_cap", C.c_double), ("m_model", C.c_double),

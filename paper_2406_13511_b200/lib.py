@@ -37,7 +37,7 @@ EXPORTS = [
     "scls_shard_range", "scls_comm_unique_id", "scls_comm_init", "scls_comm_size", "scls_run_sweep_sharded",
     "scls_multi_create", "scls_multi_destroy", "scls_multi_last_error", "scls_multi_uses_nccl",
     "scls_multi_run_sweep", "scls_multi_run_experiments", "scls_device_count",
-    "scls_multi_set_option",
+    "scls_multi_set_option", "scls_fit_latency",
 ]
 
 
@@ -88,6 +88,7 @@ def load():
         "scls_simulate_grid": (i32, [vp, i32, vp, vp, vp, vp, i32, S, L, M,
                                      P(capi.TraceResult), i32, vp, P(capi.EventLog), i32]),
         "scls_generate": (i32, [P(capi.WorkloadSpec), i64, P(i64), vp, vp, vp]),
+        "scls_fit_latency": (i32, [vp, i64, i32, i32, P(capi.Latency)]),
         "scls_make_pool": (i32, [i64, C.c_uint64, vp, vp, vp, vp]),
         "scls_debug_dp_profile": (i32, [vp, i32, vp]),
         "scls_set_option": (i32, [vp, i32, i64]),
@@ -613,6 +614,24 @@ def generate(spec):
     if st:
         raise SclsError(st, "generate failed")
     return arr[:k], inp[:k], gen[:k]
+
+
+def fit_latency(samples, n_cap=64, l_cap=4096):
+    """cost_model.cpp:140-160 fit: samples = [(phase 0|1 or "prefill"|"decode",
+    batch_size, length, latency_s)] -> capi.Latency (host computation)."""
+    lib = load()
+    rows = list(samples)
+    arr = (capi.ProfileSample * max(len(rows), 1))()
+    for i, (ph, n, l, t) in enumerate(rows):
+        arr[i].phase = {"prefill": 0, "decode": 1}.get(ph, ph)
+        arr[i].batch_size, arr[i].length, arr[i].latency_s = n, l, t
+    out = capi.Latency()
+    st = lib.scls_fit_latency(arr, len(rows), n_cap, l_cap, C.byref(out))
+    if st:
+        buf = C.create_string_buffer(4096)
+        lib.scls_last_error(None, buf, 4096)
+        raise SclsError(st, buf.value.decode())
+    return out
 
 
 def make_pool(n, seed=7):
