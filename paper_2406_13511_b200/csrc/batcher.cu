@@ -318,7 +318,10 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
     return SCLS_OK;
   };
   const uint64_t erange = ks.eff_max - ks.eff_min;
-  const bool bucketed = !ctx->force_lsd_sort && erange < (uint64_t)kBucketMaxBins;
+  // buckets that fit the shared-memory sort on average (a skewed pool still
+  // falls back after the fact, below)
+  const bool bucketed = !ctx->force_lsd_sort && erange < (uint64_t)kBucketMaxBins &&
+                        n <= (int64_t)(erange + 1) * (kBucketCap * 3 / 4);
   if (bucketed) {
     const int32_t emin = (int32_t)((uint32_t)ks.eff_min ^ 0x80000000u);
     scls_status stt0 = bucket_sort_perm(ctx, n, in.eff, in.arrival, in.id, emin, (int32_t)erange + 1, vals,
