@@ -366,6 +366,13 @@ __global__ void __launch_bounds__(kDpThreads, 1)
     }
     sm.Pv[u & 1][h][lane] = best;
     sm.Pk[u & 1][h][lane] = bk;
+#ifndef SCLS_DP_MAIN_MERGE
+#define SCLS_DP_MAIN_MERGE 1
+#endif
+    // kC == 1: the main warp merges the 12 partials itself at the start of
+    // tile u (after the tile barrier), so the helpers' barrier and helper 0's
+    // merge leave the helpers' path
+    if (kC == 1 && SCLS_DP_MAIN_MERGE) return;
     asm volatile("bar.sync 1, %0;" ::"n"(kDpHelperThreads));
     if (h == 0) {
       double fv = kInf;
@@ -475,6 +482,10 @@ __global__ void __launch_bounds__(kDpThreads, 1)
       sm.Fv[0][m] = kInf;
       sm.Fk[0][m] = 0;
     }
+    for (int e = ht; e < kMonoSegs * 32; e += kDpHelperThreads) {  // tile 0 has no far sources
+      sm.Pv[0][e >> 5][e & 31] = kInf;
+      sm.Pk[0][e >> 5][e & 31] = 0;
+    }
   }
   __syncthreads();
 
@@ -487,6 +498,16 @@ __global__ void __launch_bounds__(kDpThreads, 1)
       const int cbuf = t % 3;
       const int rsl = kStagers ? sm.rs[cbuf][lane] : 0;
       const int r = tB + 1 + lane;
+      // far: the helpers' 12 partial minima (kC == 1) or their merge, first
+      // -- independent of the ring loads below
+      double acc = kInf;
+      int kb = 0;
+      if (kC == 1 && SCLS_DP_MAIN_MERGE) {
+        merge12(sm.Pv[t & 1], sm.Pk[t & 1], acc, kb);
+      } else {
+        acc = sm.Fv[t & 1][lane];
+        kb = sm.Fk[t & 1][lane];
+      }
       // mid: sources j = tB-31 .. tB (k = lane+32-jj), 4 interleaved chains
       double va[8] = {kInf, kInf, kInf, kInf, kInf, kInf, kInf, kInf};
       int ka[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -512,8 +533,6 @@ __global__ void __launch_bounds__(kDpThreads, 1)
           }
         }
       }
-      double acc = sm.Fv[t & 1][lane];
-      int kb = sm.Fk[t & 1][lane];
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         if (lex_lt(va[q], ka[q], acc, kb)) {
