@@ -66,7 +66,16 @@ constexpr int kEmitU = SCLS_EMIT_U;  // tick emit: served l_out scan unroll
 #ifndef SCLS_PUSH_U
 #define SCLS_PUSH_U 4
 #endif
-constexpr int kPushU = SCLS_PUSH_U;  // tick DP decision rounds: final sources pushed per trip
+constexpr int kPushU = SCLS_PUSH_U;
+#ifndef SCLS_DP_BRANCHFREE
+#define SCLS_DP_BRANCHFREE 0  // tick DP: clamped loads + selects instead of divergent branches
+#endif
+#ifndef SCLS_DP_SELECT_ACCEPT
+#define SCLS_DP_SELECT_ACCEPT 1  // tick DP chain: the accept as a select (loads stay conditional)
+#endif
+#ifndef SCLS_DP_SELECT_FAR
+#define SCLS_DP_SELECT_FAR 1  // tick DP far candidates: the accept as a select
+#endif  // tick DP decision rounds: final sources pushed per trip
 
 struct SimCfg {
   int32_t policy, S, G, B, MC, W;
@@ -754,6 +763,35 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         const int wmax = __reduce_max_sync(FULL, Wr);
         // candidates with j <= tb, ascending j (k descending)
         int j = max(0, tb + 1 - wmax);
+#if SCLS_DP_BRANCHFREE
+        {
+          // k = r - j >= 1 here (j <= tb < r); loads from min(k, Wr), selects
+          const int kcap = max(Wr, 1);
+          for (; j + kFarU - 1 <= tb; j += kFarU) {
+            double tv[kFarU], cv[kFarU];
+#pragma unroll
+            for (int u = 0; u < kFarU; ++u) {
+              tv[u] = T[j + u];
+              cv[u] = __ldg(crow + min(r - (j + u), kcap));
+            }
+#pragma unroll
+            for (int u = 0; u < kFarU; ++u) {
+              const int k = r - (j + u);
+              const double cand = __dadd_rn(tv[u], cv[u]);
+              const bool tk = k <= Wr && cand <= acc;
+              acc = tk ? cand : acc;
+              kb = tk ? k : kb;
+            }
+          }
+          for (; j <= tb; ++j) {
+            const int k = r - j;
+            const double cand = __dadd_rn(T[j], __ldg(crow + min(k, kcap)));
+            const bool tk = k <= Wr && cand <= acc;
+            acc = tk ? cand : acc;
+            kb = tk ? k : kb;
+          }
+        }
+#else
         for (; j + kFarU - 1 <= tb; j += kFarU) {
           double tv[kFarU], cv[kFarU];
 #pragma unroll
@@ -765,6 +803,12 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
 #pragma unroll
           for (int u = 0; u < kFarU; ++u) {
             const int k = r - (j + u);
+#if SCLS_DP_SELECT_FAR
+            const double cand = __dadd_rn(tv[u], cv[u]);
+            const bool tk = k <= Wr && cand <= acc;
+            acc = tk ? cand : acc;
+            kb = tk ? k : kb;
+#else
             if (k <= Wr) {
               const double cand = __dadd_rn(tv[u], cv[u]);
               if (cand <= acc) {
@@ -772,6 +816,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
                 kb = k;
               }
             }
+#endif
           }
         }
         for (; j <= tb; ++j) {
@@ -785,6 +830,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
             }
           }
         }
+#endif
         SIM_PROF(11);  // tile setup + far candidates (the rest of the tile goes to slot 5)
         if (C.mono) {
           // decision rounds (dp_mono.cuh): with T[0..a] final, a pending row
@@ -845,6 +891,25 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         const int s_lo = max(2, lane + 2 - Wr);
         const int cnt = max(0, min(rows, lane + 1) - s_lo + 1);
         auto kval = [&](int s) { return (unsigned)(s - s_lo) < (unsigned)cnt; };
+#if SCLS_DP_BRANCHFREE
+        // branch-free steps: every step loads a cost from a clamped, always
+        // valid k and selects; the accept is a select, not a divergent branch
+        const int kcap = max(Wr, 1);
+        auto ck = [&](int k) { return __ldg(crow + min(max(k, 1), kcap)); };
+        double c1 = 0.0;                                   // step s (never valid at s = 1)
+        double c2 = kval(2) ? ck(lane) : 0.0;              // step s + 1
+        for (int s = 1; s <= rows; ++s) {
+          const double c0 = c1;
+          c1 = c2;
+          const double cl = ck(lane - s);  // k = lane + 2 - (s + 2)
+          c2 = kval(s + 2) ? cl : 0.0;
+          const double cand = __dadd_rn(Tj, c0);
+          const bool tk = kval(s) && cand <= acc;
+          acc = tk ? cand : acc;
+          kb = tk ? lane + 2 - s : kb;
+          Tj = shfl_d(acc, s - 1);
+        }
+#else
         const double* __restrict__ cp = crow + lane;       // c(L_r, lane + 2 - s) = cp[2 - s]
         double c1 = 0.0;                                   // step s (never valid at s = 1)
         double c2 = kval(2) ? __ldg(cp) : 0.0;             // step s + 1
@@ -852,6 +917,12 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           const double c0 = c1;
           c1 = c2;
           c2 = kval(s + 2) ? __ldg(cp - s) : 0.0;  // k = lane + 2 - (s + 2)
+#if SCLS_DP_SELECT_ACCEPT
+          const double cand = __dadd_rn(Tj, c0);
+          const bool tk = kval(s) && cand <= acc;
+          acc = tk ? cand : acc;
+          kb = tk ? lane + 2 - s : kb;
+#else
           if (kval(s)) {
             const double cand = __dadd_rn(Tj, c0);
             if (cand <= acc) {
@@ -859,8 +930,10 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
               kb = lane + 2 - s;
             }
           }
+#endif
           Tj = shfl_d(acc, s - 1);
         }
+#endif
         if (valid) {
           T[r] = acc;
           split[r] = r - kb;
