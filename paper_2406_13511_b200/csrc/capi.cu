@@ -235,7 +235,8 @@ scls_status scls_set_option(scls_ctx* ctx, int32_t option, int64_t value) {
     return SCLS_OK;
   }
   if (option == SCLS_OPT_ILS_KERNEL) {
-    ctx->ils_lockstep = value != 0;
+    ctx->ils_lockstep = value == 1;
+    ctx->ils_split = value != 2;
     return SCLS_OK;
   }
   if (option == SCLS_OPT_BATCH_PATH) {

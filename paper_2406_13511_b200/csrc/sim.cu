@@ -1984,8 +1984,9 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
       const int ci = cfg_index ? h_idx[t] : 0;
       const SimCfg& c = hc[ci];
       int G = std::max(1, 32 / std::max(c.W, 1));
-      if (ils) G = std::max(1, std::min(G, kPackSlots / std::max(1, c.W * std::max(c.MC, 1))));
-      if (ils) G = std::min(G, kIlsPackMax);
+      if (ils) G = std::max(1, std::min(G, (ctx->ils_split ? kPackSlotsSplit : kPackSlots) /
+                                              std::max(1, c.W * std::max(c.MC, 1))));
+      if (ils) G = std::min(G, ctx->ils_split ? kIlsPackMaxSplit : kIlsPackMax);
       open[ci].push_back(t);
       if ((int)open[ci].size() == G) {
         packs.push_back(std::move(open[ci]));
@@ -2084,10 +2085,19 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
       // are re-run by the lock-step kernel from a device-side list
       SCLS_CUDA(cudaMemsetAsync(d_fb_ils, 0, sizeof(int32_t), ls));
       const int32_t npk = (int32_t)pk_off[pol].size() - 1;
-      SCLS_CUDA(cudaFuncSetAttribute(sim_ils_indep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kIlsPackSmem));
-      sim_ils_indep_kernel<<<div_up(npk, wpb), wpb * 32, kIlsPackSmem, ls>>>(p, d_pk[pol], d_pk[pol] + npk + 1, npk, d_fb_ils,
-                                                                  d_fb_ils + 1);
+      if (ctx->ils_split) {
+        SCLS_CUDA(cudaFuncSetAttribute(sim_ils_indep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kIlsPackSmemSplit));
+        sim_ils_indep_kernel<true><<<div_up(npk, wpb), wpb * 32, kIlsPackSmemSplit, ls>>>(
+            p, d_pk[pol], d_pk[pol] + npk + 1, npk, d_fb_ils, d_fb_ils + 1);
+        SCLS_LAUNCHED();
+        sim_ils_merge_kernel<<<grid, wpb * 32, 0, ls>>>(p, l, cnt, d_fb_ils, d_fb_ils + 1);
+      } else {
+        SCLS_CUDA(cudaFuncSetAttribute(sim_ils_indep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kIlsPackSmem));
+        sim_ils_indep_kernel<false><<<div_up(npk, wpb), wpb * 32, kIlsPackSmem, ls>>>(
+            p, d_pk[pol], d_pk[pol] + npk + 1, npk, d_fb_ils, d_fb_ils + 1);
+      }
       SCLS_LAUNCHED();
       sim_ils_lean_kernel<<<grid, wpb * 32, 0, ls>>>(p, d_fb_ils + 1, cnt, d_fb_ils);
     }

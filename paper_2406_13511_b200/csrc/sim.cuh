@@ -15,6 +15,7 @@ struct SimLayout {
   int64_t tl_g, tl_t, tl_e, tl_s, tl_a;                   // SCLS slot state
   int64_t fifo, pf_t, pf_seq, pf_w, run, ex;              // SLS / ILS
   int64_t ct, cp, cr, ra, cn;                             // ILS / SLS completion records, slot arrivals
+  int64_t isum;                                           // ILS: per-instance phase-1 summaries (split kernels)
   int64_t ws;                                             // worker slots (W > 32)
   int64_t total;
 };
@@ -93,6 +94,7 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
     L.cp = take(8 * (W * cap_w + 1));
     L.cr = take(8 * (W * cap_w + 1));
     L.ra = take(8 * ((int64_t)W * mc + 1));
+    L.isum = take(48 * ((int64_t)W + 1));
   }
   L.ws = take(W > 32 ? kWorkerSlotBytes * 32 * (((int64_t)W + 31) / 32) : 0);
   L.total = o;

@@ -184,6 +184,21 @@ constexpr int kIlsPackMax = SCLS_ILS_PACK_MAX;  // jobs per pack (their merges r
 // dynamic shared memory of sim_ils_indep_kernel: per warp, the running slots
 // (int4), their arrival times (double) and a boundary's join inputs (int)
 constexpr size_t kIlsPackSmem = (size_t)kSimWarps * kPackSlots * (sizeof(int4) + sizeof(double) + sizeof(int32_t));
+// Split mode (SCLS_OPT ILS split, default on): the simulation kernel packs up
+// to 32 / W jobs per warp (all lanes busy) and writes each instance's phase-1
+// summary next to its completion records; a second kernel merges and reports
+// every job with a warp of its own, so the merges no longer run in series
+// behind a pack.
+constexpr int kIlsPackMaxSplit = 4;
+constexpr int kPackSlotsSplit = 2 * kPackSlots;
+constexpr size_t kIlsPackSmemSplit =
+    (size_t)kSimWarps * kPackSlotsSplit * (sizeof(int4) + sizeof(double) + sizeof(int32_t));
+struct IlsSum {  // one instance's phase-1 totals (48 B, sim_layout isum)
+  int32_t comp, stuck, n_disp, batch_count;
+  long long n_ev, batch_members;
+  double last_comp, last_end;
+};
+static_assert(sizeof(IlsSum) == 48, "sim.cuh isum region");
 
 // Packs.  A warp takes a pack of up to min(kIlsPackMax = 2, 32 / W,
 // kPackSlots / (W * MC)) jobs of one config (host: pack_off / jobs); in phase 1 lane gi * W + w simulates instance w of job
@@ -234,30 +249,80 @@ __device__ unsigned pack_validate(const SimParams& P, const int32_t* jobs, int n
   return ok;
 }
 
+// Phase 2 of one ILS job (lanes < W hold its instances' phase-1 totals):
+// the completions in the reference's global order, then the report.
+__device__ void ils_finish_job(const SimParams& P, int t, int W, int MC, int lane, const IlsSum& s, uint64_t* wt,
+                               double* wr, uint32_t* wq, int32_t* bins, int32_t* fb_count, int32_t* fb_list) {
+  const bool in = lane < W;
+  int c = in ? s.comp : 0, st = in ? s.stuck : 0, nd = in ? s.n_disp : 0, bc = in ? s.batch_count : 0;
+  long long ne = in ? s.n_ev : 0, bm = in ? s.batch_members : 0;
+  double lc = in ? s.last_comp : -dinf(), le = in ? s.last_end : 0.0;
+  const PackJob J = pack_job(P, t, W, SCLS_POLICY_ILS, MC);
+  scls_trace_result* R = &P.res[J.t];
+  int64_t* hist = P.hist ? P.hist + (int64_t)J.t * P.hist_bins : nullptr;
+  if (__any_sync(FULL, st)) {
+    finish_report(lane, R, SCLS_ERR_NON_TERMINATION, J.n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0,
+                  0, 0.0);
+    return;
+  }
+  const int completed = __reduce_add_sync(FULL, c);
+  const long long n_events = J.n + __reduce_add_sync(FULL, (unsigned)ne);  // per-instance counts fit 32 bits
+  const int n_disp_all = __reduce_add_sync(FULL, nd);
+  const int batch_all = __reduce_add_sync(FULL, bc);
+  for (int o = 16; o; o >>= 1) bm += __shfl_xor_sync(FULL, bm, o);
+  double last_completion = lc;
+  for (int o = 16; o; o >>= 1) last_completion = fmax(last_completion, __shfl_xor_sync(FULL, last_completion, o));
+  double* resp = (double*)(J.base + J.Lay.resp);
+  const bool tie = merge_completions(lane, W, c, completed, last_completion, J.cap_w,
+                                     (const double*)(J.base + J.Lay.ct), (const double*)(J.base + J.Lay.cp),
+                                     (const double*)(J.base + J.Lay.cr), nullptr, resp, wt, wr, wq, nullptr);
+  if (tie) {  // the exact lock-step kernel re-runs this job
+    if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = J.t;
+    return;
+  }
+  __syncwarp();
+  if (hist && P.hist_bins > 1 && lane == 0) hist[1] = completed;
+  finish_report(lane, R, SCLS_OK, J.n, W, completed, J.n > 0 ? J.arr[0] : dinf(), last_completion, resp, bins, le,
+                0, 0, batch_all, bm, 0, n_events, n_disp_all, 0, last_completion);
+}
+
+template <bool kSplit>
 __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
     sim_ils_indep_kernel(SimParams P, const int32_t* __restrict__ pack_off, const int32_t* __restrict__ jobs,
                          int32_t count, int32_t* __restrict__ fb_count, int32_t* __restrict__ fb_list) {
-  __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
-  __shared__ double swin_r[kSimWarps][kMergeWin];
-  __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
+  constexpr int kSlots = kSplit ? kPackSlotsSplit : kPackSlots;
+  __shared__ uint64_t swin_t[kSplit ? 1 : kSimWarps][kSplit ? 1 : kMergeWin];
+  __shared__ double swin_r[kSplit ? 1 : kSimWarps][kSplit ? 1 : kMergeWin];
+  __shared__ uint32_t swin_q[kSplit ? 1 : kSimWarps][kSplit ? 1 : kMergeWin];
+  __shared__ int32_t sbins_split[kSplit ? kSimWarps : 1][kSplit ? 256 : 1];
   extern __shared__ __align__(16) unsigned char ils_dyn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int4* srun = (int4*)ils_dyn + warp * kPackSlots;  // running slots
-  double* sra = (double*)(ils_dyn + (size_t)kSimWarps * kPackSlots * sizeof(int4)) + warp * kPackSlots;
-  int32_t* sjin = (int32_t*)(ils_dyn + (size_t)kSimWarps * kPackSlots * (sizeof(int4) + sizeof(double))) +
-                  warp * kPackSlots;
+  int4* srun = (int4*)ils_dyn + warp * kSlots;  // running slots
+  double* sra = (double*)(ils_dyn + (size_t)kSimWarps * kSlots * sizeof(int4)) + warp * kSlots;
+  int32_t* sjin = (int32_t*)(ils_dyn + (size_t)kSimWarps * kSlots * (sizeof(int4) + sizeof(double))) +
+                  warp * kSlots;
   const int g = blockIdx.x * (blockDim.x >> 5) + warp;  // launches use 1 or kSimWarps warps per CTA
   if (g >= count) return;
   const int p0 = pack_off[g], np = pack_off[g + 1] - p0;
   if (np <= 0) return;  // an empty slot (small launches: one pack per CTA)
   const int32_t* pj = jobs + p0;
-  int32_t* bins = (int32_t*)swin_t[warp];  // p95 bins (after the merge)
+  int32_t* bins = kSplit ? sbins_split[warp] : (int32_t*)swin_t[warp];  // p95 bins (after the merge)
   const int ci = P.cfg_index ? P.cfg_index[pj[0]] : 0;  // one config per pack
   const int W = P.cfgs[ci].W, MC = P.cfgs[ci].MC, G = P.cfgs[ci].G;
   const double horizon = P.cfgs[ci].horizon;
   const Lat& lat = P.lat;
   unsigned okm = pack_validate(P, pj, np, ci, W, lane, bins);
-  if (okm && np * W * MC > kPackSlots) {  // running slots do not fit this warp's shared memory (np == 1)
+  if (kSplit) {  // jobs reported here (invalid) or handed to the fallback: the merge kernel skips them
+    const bool fits = np * W * MC <= kSlots;
+    if (lane == 0)
+      for (int q = 0; q < np; ++q)
+        if (!((okm >> q) & 1u) || !fits) {
+          const PackJob Jq = pack_job(P, pj[q], W, SCLS_POLICY_ILS, MC);
+          ((IlsSum*)(Jq.base + Jq.Lay.isum))->stuck = -1;
+        }
+    __syncwarp();
+  }
+  if (okm && np * W * MC > kSlots) {  // running slots do not fit this warp's shared memory (np == 1)
     if (lane == 0)
       for (int q = 0; q < np; ++q)
         if ((okm >> q) & 1u) fb_list[atomicAdd(fb_count, 1)] = pj[q];
@@ -440,6 +505,15 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
     stuck = comp < n_mine;
   }
 
+  if (kSplit) {  // the merge kernel takes it from here
+    const int gi = lane / W, w = lane - gi * W;
+    if (gi < np && ((okm >> gi) & 1u)) {
+      const PackJob J = pack_job(P, pj[gi], W, SCLS_POLICY_ILS, MC);
+      IlsSum* sp = (IlsSum*)(J.base + J.Lay.isum) + w;
+      *sp = IlsSum{comp, stuck, n_disp, batch_count, n_ev, batch_members, last_comp, last_end};
+    }
+    return;
+  }
   // ---- phase 2, job by job: the completions in the reference's global order ----------
   for (int q = 0; q < np; ++q) {
     if (!((okm >> q) & 1u)) continue;
@@ -486,6 +560,29 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
   }
 }
 
+
+// The split ILS's phase 2: one warp per job (list order, longest first).
+__global__ void __launch_bounds__(kSimWarps * 32) sim_ils_merge_kernel(SimParams P, const int32_t* __restrict__ list,
+                                                                      int32_t count, int32_t* __restrict__ fb_count,
+                                                                      int32_t* __restrict__ fb_list) {
+  __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
+  __shared__ double swin_r[kSimWarps][kMergeWin];
+  __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (g >= count) return;
+  const int t = list[g];
+  if (t < 0) return;
+  const int ci = P.cfg_index ? P.cfg_index[t] : 0;
+  const int W = P.cfgs[ci].W, MC = P.cfgs[ci].MC;
+  const PackJob J = pack_job(P, t, W, SCLS_POLICY_ILS, MC);
+  const IlsSum* sp = (const IlsSum*)(J.base + J.Lay.isum);
+  if (__shfl_sync(FULL, lane == 0 ? sp[0].stuck : 0, 0) == -1) return;  // reported / re-run elsewhere
+  IlsSum s{};
+  if (lane < W) s = sp[lane];
+  ils_finish_job(P, t, W, MC, lane, s, swin_t[warp], swin_r[warp], swin_q[warp], (int32_t*)swin_t[warp], fb_count,
+                 fb_list);
+}
 
 // ---- SLS with independent worker lanes ------------------------------------------------
 // SLS workers never interact either: arrivals go round-robin in id order

@@ -196,6 +196,11 @@ class Context:
         """SCLS_OPT_ILS_KERNEL: 1 = the lock-step metrics-only ILS kernel, 0 = independent instance lanes."""
         self._check(self.lib.scls_set_option(self.h, 4, 1 if on else 0))
 
+    def set_ils_kernel(self, mode):
+        """SCLS_OPT_ILS_KERNEL: 0 independent lanes, simulation and merge kernels split (default);
+        1 lock-step; 2 independent lanes in one kernel (packs of two jobs, merges in series)."""
+        self._check(self.lib.scls_set_option(self.h, 4, int(mode)))
+
     def set_batch_path(self, large):
         """SCLS_OPT_BATCH_PATH: 1 forces the multi-kernel batch_requests path for small pools too;
         2 also replaces the eff-bucket sort by the LSD radix sort."""
