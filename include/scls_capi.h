@@ -146,11 +146,11 @@ enum { SCLS_OPT_SIM_DIGESTS = 1, SCLS_OPT_DP_KERNEL = 2, SCLS_OPT_SIM_CONCURRENT
  * longest first, so the policies' tails overlap: 65.8 vs 70.1 ms on the C5
  * sweep.  SCLS_OPT_ILS_KERNEL
  * (default 0): metrics-only ILS and SLS run every instance / worker in its own
- * lane and merge the completions (csrc/sim_indep.cuh; ILS as a simulation
+ * lane and merge the completions (csrc/sim_indep.cuh; each as a simulation
  * kernel packing 32 / W jobs per warp plus a merge kernel with a warp per
  * job); 1 forces the lock-step kernels that process the global event order
- * directly; 2 runs ILS in one kernel, packs of two jobs whose merges follow
- * in series (results identical).
+ * directly; 2 runs each policy in one kernel (ILS: packs of two jobs whose
+ * merges follow in series; SLS: one job per warp) (results identical).
  * SCLS_OPT_BATCH_PATH (default 0): batch_requests / schedule take the fused
  * four-launch small-pool path for n <= 4096 and the multi-kernel path above;
  * 1 forces the multi-kernel path at every size; 2 does that and sorts with

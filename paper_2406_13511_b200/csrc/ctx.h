@@ -29,7 +29,7 @@ struct scls_ctx {
   int dp_mode = 0;                        // 0 auto, 1 force the chain kernel (tests)
   bool dp_last_mono = false;              // the last DP ran the monotone decision kernel
   bool sim_concurrent = true;             // scls_simulate runs its per-policy launches concurrently
-  bool ils_split = true;                  // metrics-only ILS: simulation kernel (4 jobs / warp) + merge kernel
+  bool ils_split = true;                  // metrics-only ILS / SLS: simulation kernel (32 / W jobs per warp) + merge kernel
   bool ils_lockstep = false;              // metrics-only ILS: the lock-step kernel instead of independent lanes
   cudaStream_t side[3] = {};              // forked streams for those launches (created on first use)
   bool force_large_path = false;          // batch_requests: the multi-kernel path even for small pools (tests)

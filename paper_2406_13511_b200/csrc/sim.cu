@@ -2010,8 +2010,9 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   const bool indep = !want_log && !hash;
   std::vector<int32_t> pk_off[3], pk_jobs[3];
   int32_t* d_pk[3] = {nullptr, nullptr, nullptr};
-  for (int pol : {SCLS_POLICY_ILS}) {
+  for (int pol : {SCLS_POLICY_ILS, SCLS_POLICY_SLS}) {
     if (!indep || ctx->ils_lockstep || lists[pol].empty()) continue;
+    if (pol == SCLS_POLICY_SLS && !ctx->ils_split) continue;  // SLS packs only in split mode
     make_packs(lists[pol], pol == SCLS_POLICY_ILS, pk_off[pol], pk_jobs[pol]);
     const size_t m = pk_off[pol].size() + pk_jobs[pol].size();
     d_pk[pol] = (int32_t*)ctx->buf(kSlotSim + 26 + pol, sizeof(int32_t) * m);
@@ -2074,7 +2075,14 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
     else if (pol == SCLS_POLICY_SLS && !want_log && !hash && !ctx->ils_lockstep) {
       // independent worker lanes; exact cross-worker ties re-run in lock step
       SCLS_CUDA(cudaMemsetAsync(d_fb_sls, 0, sizeof(int32_t), ls));
-      sim_sls_indep_kernel<<<grid, wpb * 32, 0, ls>>>(p, l, cnt, d_fb_sls, d_fb_sls + 1);
+      if (ctx->ils_split) {  // packs of 32 / W jobs simulate, then a warp per job merges
+        const int32_t npk = (int32_t)pk_off[pol].size() - 1;
+        sim_sls_pack_kernel<<<div_up(npk, wpb), wpb * 32, 0, ls>>>(p, d_pk[pol], d_pk[pol] + npk + 1, npk);
+        SCLS_LAUNCHED();
+        sim_sls_merge_kernel<<<grid, wpb * 32, 0, ls>>>(p, l, cnt, d_fb_sls, d_fb_sls + 1);
+      } else {
+        sim_sls_indep_kernel<<<grid, wpb * 32, 0, ls>>>(p, l, cnt, d_fb_sls, d_fb_sls + 1);
+      }
       SCLS_LAUNCHED();
       sim_kernel<SCLS_POLICY_SLS, false, false><<<grid, wpb * 32, 0, ls>>>(p, d_fb_sls + 1, cnt, d_fb_sls);
     }

@@ -86,6 +86,7 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
     L.cp = take(8 * (W * cap_w + 1));
     L.cr = take(8 * (W * cap_w + 1));
     L.cn = take(4 * (W * cap_w + 1));
+    L.isum = take(64 * ((int64_t)W + 1));
   } else {
     L.fifo = take(4 * (W * cap_w + 1));
     L.run = take(16 * ((int64_t)W * mc + 1));

@@ -597,6 +597,186 @@ __global__ void __launch_bounds__(kSimWarps * 32) sim_ils_merge_kernel(SimParams
 #ifndef SCLS_SLS_INDEP_MINB
 #define SCLS_SLS_INDEP_MINB 7  // one wave of 4096 traces (7.3 ms vs 8.8 ms at 4)
 #endif
+// Split mode (like ILS): the simulation kernel packs 32 / W jobs of one
+// config per warp and writes each worker's totals (64 B, sim_layout isum);
+// sim_sls_merge_kernel merges and reports a job per warp.
+struct SlsSum {
+  int32_t comp, stuck, n_disp, batch_count;
+  long long n_ev, batch_members, total_pad, total_inv;
+  double last_comp, last_end;
+};
+static_assert(sizeof(SlsSum) == 64, "sim.cuh isum region (SLS)");
+
+// Phase 2 of one SLS job (lanes < W hold its workers' totals).
+__device__ void sls_finish_job(const SimParams& P, int t, int W, int lane, const SlsSum& s, uint64_t* wt,
+                               double* wr, uint32_t* wq, uint8_t* wn, int32_t* bins, int32_t* fb_count,
+                               int32_t* fb_list) {
+  const int ts = P.src ? P.src[t] : t;
+  const int64_t r0 = P.req_off[ts];
+  const int n = (int)(P.req_off[ts + 1] - r0);
+  const double* __restrict__ arr = P.arr + r0;
+  scls_trace_result* R = &P.res[t];
+  int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
+  char* base = P.arena + P.trace_base[t];
+  const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_SLS, P.trace_cap[t], 1);
+  double* resp = (double*)(base + Lay.resp);
+  const int64_t cap_w = (n + W - 1) / W;
+  const bool in = lane < W;
+  const int comp = in ? s.comp : 0, stuck = in ? s.stuck : 0;
+  long long n_ev = in ? s.n_ev : 0, batch_members = in ? s.batch_members : 0;
+  long long total_pad = in ? s.total_pad : 0, total_inv = in ? s.total_inv : 0;
+  const int n_disp = in ? s.n_disp : 0, batch_count = in ? s.batch_count : 0;
+  const double last_comp = in ? s.last_comp : -dinf(), last_end0 = in ? s.last_end : 0.0;
+  if (__any_sync(FULL, stuck)) {
+    finish_report(lane, R, SCLS_ERR_NON_TERMINATION, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0,
+                  0.0);
+    return;
+  }
+  const int completed = __reduce_add_sync(FULL, comp);
+  const long long n_events = n + __reduce_add_sync(FULL, (unsigned)n_ev);
+  const int n_disp_all = __reduce_add_sync(FULL, n_disp);
+  const int batch_all = __reduce_add_sync(FULL, batch_count);
+  double last_end = last_end0;
+  for (int o = 16; o; o >>= 1) {
+    batch_members += __shfl_xor_sync(FULL, batch_members, o);
+    total_pad += __shfl_xor_sync(FULL, total_pad, o);
+    total_inv += __shfl_xor_sync(FULL, total_inv, o);
+  }
+  double last_completion = last_comp;
+  for (int o = 16; o; o >>= 1) last_completion = fmax(last_completion, __shfl_xor_sync(FULL, last_completion, o));
+  bool tie = false;
+  if (W == 1) {  // one list: already in completion order
+    const double* cr = (const double*)(base + Lay.cr);
+    __syncwarp();
+    for (int i = lane; i < completed; i += 32) resp[i] = cr[i];
+  } else {
+    tie = merge_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),
+                            (const double*)(base + Lay.cp), (const double*)(base + Lay.cr),
+                            (const int32_t*)(base + Lay.cn), resp, wt, wr, wq, wn);
+  }
+  if (tie) {  // the exact lock-step kernel re-runs this job
+    if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
+    return;
+  }
+  __syncwarp();
+  if (hist && P.hist_bins > 1 && lane == 0) hist[1] = completed;
+  finish_report(lane, R, SCLS_OK, n, W, completed, n > 0 ? arr[0] : dinf(), last_completion, resp, bins, last_end,
+                total_pad, total_inv, batch_all, batch_members, 0, n_events, n_disp_all, 0, last_completion);
+}
+
+// Phase 1 of SLS for worker w of job t (this lane), into *out.
+__device__ __forceinline__ void sls_simulate_worker(const SimParams& P, int t, int W, int w, bool active, SlsSum* out) {
+  const int ts = P.src ? P.src[t] : t;
+  const int64_t r0 = P.req_off[ts];
+  const int n = (int)(P.req_off[ts + 1] - r0);
+  const double* __restrict__ arr = P.arr + r0;
+  const int32_t* __restrict__ inp = P.inp + r0;
+  const int32_t* __restrict__ tg = P.tg + r0;
+  const int ci = P.cfg_index ? P.cfg_index[t] : 0;
+  const int B = P.cfgs[ci].B, G = P.cfgs[ci].G;
+  const double horizon = P.cfgs[ci].horizon;
+  const Lat& lat = P.lat;
+  char* base = P.arena + P.trace_base[t];
+  const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_SLS, P.trace_cap[t], 1);
+  const int64_t cap_w = (n + W - 1) / W;
+  int comp = 0, batch_count = 0, n_disp = 0;
+  long long batch_members = 0, n_ev = 0, total_pad = 0, total_inv = 0;
+  double last_end = 0.0, last_comp = -dinf();
+  double* rt = (double*)(base + Lay.ct) + w * cap_w;
+  double* rp = (double*)(base + Lay.cp) + w * cap_w;
+  double* rr = (double*)(base + Lay.cr) + w * cap_w;
+  int32_t* rn = (int32_t*)(base + Lay.cn) + w * cap_w;
+  const int n_mine = active && w < n ? (n - 1 - w) / W + 1 : 0;  // requests w, w + W, ...
+  int f_head = 0, f_tail = 0;  // dispatched / arrived (FIFO as counters)
+  bool busy = false;
+  int b_head = 0, b_n = 0, b_lin = 0, b_lout = 0;  // in-flight batch: FIFO positions [b_head, b_head + b_n)
+  double done_t = dinf(), b_start = 0.0;
+  double next_arr = n_mine > 0 ? arr[w] : dinf();
+  double next_arr2 = n_mine > 1 ? arr[w + W] : dinf();
+  bool live = n_mine > 0;
+  // try_dispatch at `now` (sched_policies.cpp:207-243): FCFS batch of <= B
+  // from the FIFO, started at once (enqueue_batch + start_next_batch)
+  auto dispatch = [&](double now) {
+    const int take = min(B, f_tail - f_head);
+    int lin = 0, lout = 0;
+    long long so = 0, sg = 0;
+    for (int j0 = 0; j0 < take; j0 += 4) {  // four members per trip, loads first
+      int o[4], gm[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int id = w + (f_head + j0 + u) * W;
+        o[u] = j0 + u < take ? inp[id] : 0;
+        gm[u] = j0 + u < take ? min(tg[id], G) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        lin = max(lin, o[u]);
+        lout = max(lout, gm[u]);
+        so += o[u];
+        sg += gm[u];
+      }
+    }
+    // batch_end accounting (sched_policies.cpp:255-266): pad = l_in - orig,
+    // invalid = served - min(gen, G), summed over members
+    total_pad += (long long)take * lin - so;
+    total_inv += (long long)take * lout - sg;
+    b_head = f_head;
+    b_n = take;
+    b_lin = lin;
+    b_lout = lout;
+    f_head += take;
+    busy = true;
+    b_start = now;
+    done_t = __dadd_rn(now, batch_serve_time(lat, take, lin, lout));
+    n_disp += 1;
+    n_ev += 2;  // dispatch + batch_start
+  };
+  for (;;) {
+    const bool arrive = live && next_arr <= done_t && next_arr <= horizon;  // arrivals first at an instant
+    const bool done = live && !arrive && busy && done_t < next_arr && done_t < horizon;
+    if (!__any_sync(FULL, arrive || done)) break;
+    if (arrive) {
+      // on_arrival (sched_policies.cpp:194-201) + its policy event, which runs
+      // after every arrival of this instant
+      const double now = next_arr;
+      ++f_tail;
+      next_arr = next_arr2;
+      next_arr2 = f_tail + 1 < n_mine ? arr[w + (f_tail + 1) * W] : dinf();
+      if (!busy && next_arr != now) dispatch(now);
+    } else if (done) {
+      // BatchDone (sim_engine.cpp:151-158, sched_policies.cpp:245-273)
+      const double now = done_t;
+      ++batch_count;
+      batch_members += b_n;
+      last_end = fmax(last_end, now);
+      for (int j0 = 0; j0 < b_n; j0 += 4) {  // four members per trip, loads first
+        double av[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) av[u] = j0 + u < b_n ? arr[w + (b_head + j0 + u) * W] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u;
+          if (j < b_n) {
+            rt[comp + j] = now;
+            rp[comp + j] = b_start;
+            rr[comp + j] = now - av[u];
+            rn[comp + j] = j == 0 ? b_n : 0;
+          }
+        }
+      }
+      comp += b_n;
+      n_ev += 1 + b_n;  // batch_end + completions
+      last_comp = now;
+      busy = false;
+      done_t = dinf();
+      if (f_tail > f_head) dispatch(now);
+    }
+    live = live && comp < n_mine;
+  }
+  *out = SlsSum{comp, comp < n_mine ? 1 : 0, n_disp, batch_count, n_ev, batch_members, total_pad, total_inv,
+                last_comp, last_end};
+}
+
 __global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
     sim_sls_indep_kernel(SimParams P, const int32_t* __restrict__ list, int32_t count, int32_t* __restrict__ fb_count,
                          int32_t* __restrict__ fb_list) {
@@ -610,166 +790,76 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
   const int t = list[g];
   if (t < 0) return;  // an empty slot (small launches: one job per CTA)
   int32_t* bins = (int32_t*)swin_t[warp];  // p95 bins (after the merge)
-  const int ts = P.src ? P.src[t] : t;
-  const int64_t r0 = P.req_off[ts];
-  const int n = (int)(P.req_off[ts + 1] - r0);
-  const double* __restrict__ arr = P.arr + r0;
-  const int32_t* __restrict__ inp = P.inp + r0;
-  const int32_t* __restrict__ tg = P.tg + r0;
   const int ci = P.cfg_index ? P.cfg_index[t] : 0;
-  const int W = P.cfgs[ci].W, B = P.cfgs[ci].B, G = P.cfgs[ci].G;
-  const double horizon = P.cfgs[ci].horizon;
-  const Lat& lat = P.lat;
-  scls_trace_result* R = &P.res[t];
-  int64_t* hist = P.hist ? P.hist + (int64_t)t * P.hist_bins : nullptr;
-
-  int status = P.cfg_ok[ci] ? SCLS_OK : SCLS_ERR_ERROR;
-  if (status == SCLS_OK) status = trace_input_status(arr, inp, tg, n, lane);
-  if (hist)
-    for (int i = lane; i < P.hist_bins; i += 32) hist[i] = 0;
-  if (status != SCLS_OK) {
-    finish_report(lane, R, status, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0);
-    return;
-  }
-  char* base = P.arena + P.trace_base[t];
-  const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_SLS, P.trace_cap[t], 1);
-  double* resp = (double*)(base + Lay.resp);
-  const int64_t cap_w = (n + W - 1) / W;
-
-  int comp = 0, batch_count = 0, n_disp = 0, stuck = 0;
-  long long batch_members = 0, n_ev = 0, total_pad = 0, total_inv = 0;
-  double last_end = 0.0, last_comp = -dinf();
-  {
-    const int w = lane;
-    double* rt = (double*)(base + Lay.ct) + w * cap_w;
-    double* rp = (double*)(base + Lay.cp) + w * cap_w;
-    double* rr = (double*)(base + Lay.cr) + w * cap_w;
-    int32_t* rn = (int32_t*)(base + Lay.cn) + w * cap_w;
-    const int n_mine = lane < W && w < n ? (n - 1 - w) / W + 1 : 0;  // requests w, w + W, ...
-    int f_head = 0, f_tail = 0;  // dispatched / arrived (FIFO as counters)
-    bool busy = false;
-    int b_head = 0, b_n = 0, b_lin = 0, b_lout = 0;  // in-flight batch: FIFO positions [b_head, b_head + b_n)
-    double done_t = dinf(), b_start = 0.0;
-    double next_arr = n_mine > 0 ? arr[w] : dinf();
-    double next_arr2 = n_mine > 1 ? arr[w + W] : dinf();
-    bool live = n_mine > 0;
-    // try_dispatch at `now` (sched_policies.cpp:207-243): FCFS batch of <= B
-    // from the FIFO, started at once (enqueue_batch + start_next_batch)
-    auto dispatch = [&](double now) {
-      const int take = min(B, f_tail - f_head);
-      int lin = 0, lout = 0;
-      long long so = 0, sg = 0;
-      for (int j0 = 0; j0 < take; j0 += 4) {  // four members per trip, loads first
-        int o[4], gm[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int id = w + (f_head + j0 + u) * W;
-          o[u] = j0 + u < take ? inp[id] : 0;
-          gm[u] = j0 + u < take ? min(tg[id], G) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          lin = max(lin, o[u]);
-          lout = max(lout, gm[u]);
-          so += o[u];
-          sg += gm[u];
-        }
-      }
-      // batch_end accounting (sched_policies.cpp:255-266): pad = l_in - orig,
-      // invalid = served - min(gen, G), summed over members
-      total_pad += (long long)take * lin - so;
-      total_inv += (long long)take * lout - sg;
-      b_head = f_head;
-      b_n = take;
-      b_lin = lin;
-      b_lout = lout;
-      f_head += take;
-      busy = true;
-      b_start = now;
-      done_t = __dadd_rn(now, batch_serve_time(lat, take, lin, lout));
-      n_disp += 1;
-      n_ev += 2;  // dispatch + batch_start
-    };
-    for (;;) {
-      const bool arrive = live && next_arr <= done_t && next_arr <= horizon;  // arrivals first at an instant
-      const bool done = live && !arrive && busy && done_t < next_arr && done_t < horizon;
-      if (!__any_sync(FULL, arrive || done)) break;
-      if (arrive) {
-        // on_arrival (sched_policies.cpp:194-201) + its policy event, which runs
-        // after every arrival of this instant
-        const double now = next_arr;
-        ++f_tail;
-        next_arr = next_arr2;
-        next_arr2 = f_tail + 1 < n_mine ? arr[w + (f_tail + 1) * W] : dinf();
-        if (!busy && next_arr != now) dispatch(now);
-      } else if (done) {
-        // BatchDone (sim_engine.cpp:151-158, sched_policies.cpp:245-273)
-        const double now = done_t;
-        ++batch_count;
-        batch_members += b_n;
-        last_end = fmax(last_end, now);
-        for (int j0 = 0; j0 < b_n; j0 += 4) {  // four members per trip, loads first
-          double av[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) av[u] = j0 + u < b_n ? arr[w + (b_head + j0 + u) * W] : 0.0;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u;
-            if (j < b_n) {
-              rt[comp + j] = now;
-              rp[comp + j] = b_start;
-              rr[comp + j] = now - av[u];
-              rn[comp + j] = j == 0 ? b_n : 0;
-            }
-          }
-        }
-        comp += b_n;
-        n_ev += 1 + b_n;  // batch_end + completions
-        last_comp = now;
-        busy = false;
-        done_t = dinf();
-        if (f_tail > f_head) dispatch(now);
-      }
-      live = live && comp < n_mine;
-    }
-    stuck = comp < n_mine;
-  }
-  if (__any_sync(FULL, stuck)) {
-    finish_report(lane, R, SCLS_ERR_NON_TERMINATION, n, W, 0, 0.0, 0.0, nullptr, bins, 0.0, 0, 0, 0, 0, 0, 0, 0, 0,
-                  0.0);
-    return;
-  }
-  const int completed = __reduce_add_sync(FULL, comp);
-  const long long n_events = n + __reduce_add_sync(FULL, (unsigned)n_ev);
-  const int n_disp_all = __reduce_add_sync(FULL, n_disp);
-  const int batch_all = __reduce_add_sync(FULL, batch_count);
-  for (int o = 16; o; o >>= 1) {
-    batch_members += __shfl_xor_sync(FULL, batch_members, o);
-    total_pad += __shfl_xor_sync(FULL, total_pad, o);
-    total_inv += __shfl_xor_sync(FULL, total_inv, o);
-  }
-  double last_completion = last_comp;
-  for (int o = 16; o; o >>= 1) last_completion = fmax(last_completion, __shfl_xor_sync(FULL, last_completion, o));
-  bool tie = false;
-  if (W == 1) {  // one list: already in completion order
-    const double* cr = (const double*)(base + Lay.cr);
-    __syncwarp();  // lane 0 wrote cr[] in the simulation phase
-    for (int i = lane; i < completed; i += 32) resp[i] = cr[i];
-  } else {
-    tie = merge_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),
-                            (const double*)(base + Lay.cp), (const double*)(base + Lay.cr),
-                            (const int32_t*)(base + Lay.cn), resp, swin_t[warp], swin_r[warp], swin_q[warp],
-                            swin_n[warp]);
-  }
-  if (tie) {  // the exact lock-step kernel re-runs this job
-    if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
-    return;
-  }
-  __syncwarp();
-  if (hist && P.hist_bins > 1 && lane == 0) hist[1] = completed;
-  finish_report(lane, R, SCLS_OK, n, W, completed, n > 0 ? arr[0] : dinf(), last_completion, resp, bins, last_end,
-                total_pad, total_inv, batch_all, batch_members, 0, n_events, n_disp_all, 0, last_completion);
+  const int W = P.cfgs[ci].W;
+  if (!pack_validate(P, &t, 1, ci, W, lane, bins)) return;
+  SlsSum s;
+  sls_simulate_worker(P, t, W, lane, lane < W, &s);
+  sls_finish_job(P, t, W, lane, s, swin_t[warp], swin_r[warp], swin_q[warp], swin_n[warp], bins, fb_count, fb_list);
 }
 
+// Split SLS, phase 1: packs of up to 32 / W jobs (pack_off / jobs), lane
+// gi * W + w simulates worker w of job gi; totals into the job's isum region.
+__global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
+    sim_sls_pack_kernel(SimParams P, const int32_t* __restrict__ pack_off, const int32_t* __restrict__ jobs,
+                        int32_t count) {
+  __shared__ int32_t sbins[kSimWarps][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (g >= count) return;
+  const int p0 = pack_off[g], np = pack_off[g + 1] - p0;
+  if (np <= 0) return;
+  const int32_t* pj = jobs + p0;
+  const int ci = P.cfg_index ? P.cfg_index[pj[0]] : 0;  // one config per pack
+  const int W = P.cfgs[ci].W;
+  const unsigned okm = pack_validate(P, pj, np, ci, W, lane, sbins[warp]);
+  if (lane == 0)
+    for (int q = 0; q < np; ++q)
+      if (!((okm >> q) & 1u)) {  // reported by pack_validate: the merge kernel skips it
+        const int t = pj[q];
+        const int ts = P.src ? P.src[t] : t;
+        const int n = (int)(P.req_off[ts + 1] - P.req_off[ts]);
+        const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_SLS, P.trace_cap[t], 1);
+        ((SlsSum*)(P.arena + P.trace_base[t] + Lay.isum))->stuck = -1;
+      }
+  __syncwarp();
+  const int gi = lane / W, w = lane - gi * W;
+  const bool active = gi < np && ((okm >> gi) & 1u);
+  const int t = pj[active ? gi : 0];
+  SlsSum s;
+  sls_simulate_worker(P, t, W, w, active, &s);
+  if (active) {
+    const int ts = P.src ? P.src[t] : t;
+    const int n = (int)(P.req_off[ts + 1] - P.req_off[ts]);
+    const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_SLS, P.trace_cap[t], 1);
+    ((SlsSum*)(P.arena + P.trace_base[t] + Lay.isum))[w] = s;
+  }
+}
+
+// Split SLS, phase 2: a warp per job (list order).
+__global__ void __launch_bounds__(kSimWarps * 32) sim_sls_merge_kernel(SimParams P, const int32_t* __restrict__ list,
+                                                                      int32_t count, int32_t* __restrict__ fb_count,
+                                                                      int32_t* __restrict__ fb_list) {
+  __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
+  __shared__ double swin_r[kSimWarps][kMergeWin];
+  __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
+  __shared__ uint8_t swin_n[kSimWarps][kMergeWin];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (g >= count) return;
+  const int t = list[g];
+  if (t < 0) return;
+  const int ci = P.cfg_index ? P.cfg_index[t] : 0;
+  const int W = P.cfgs[ci].W;
+  const int ts = P.src ? P.src[t] : t;
+  const int n = (int)(P.req_off[ts + 1] - P.req_off[ts]);
+  const SimLayout Lay = sim_layout(n, W, SCLS_POLICY_SLS, P.trace_cap[t], 1);
+  const SlsSum* sp = (const SlsSum*)(P.arena + P.trace_base[t] + Lay.isum);
+  if (__shfl_sync(FULL, lane == 0 ? sp[0].stuck : 0, 0) == -1) return;
+  SlsSum s{};
+  if (lane < W) s = sp[lane];
+  sls_finish_job(P, t, W, lane, s, swin_t[warp], swin_r[warp], swin_q[warp], swin_n[warp], (int32_t*)swin_t[warp],
+                 fb_count, fb_list);
+}
 }  // namespace
 }  // namespace scls

@@ -44,17 +44,18 @@ def main():
                 ctx.set_dp_kernel(mode)
                 print("dp mode", mode, "sweep", kernel_ms(ctx, specs(T), capi.sched_cfg()),
                       "one rate-25 trace", kernel_ms(ctx, specs(1, (25.0,)), capi.sched_cfg()))
-        elif cmd == "ils":  # SCLS_OPT_ILS_KERNEL 0 (split) vs 2 (one kernel), ILS alone and the step
+        elif cmd == "ils":  # SCLS_OPT_ILS_KERNEL 0 (split) vs 2 (one kernel): ILS / SLS alone and the step
             sp = specs(T)
             cfgs = [capi.sched_cfg(policy=p) for p in ("scls", "sls", "ils")]
             for mode in (0, 2, 0, 2):
                 ctx.set_ils_kernel(mode)
                 r_ils = kernel_ms(ctx, sp, capi.sched_cfg(policy="ils"))
+                r_sls = kernel_ms(ctx, sp, capi.sched_cfg(policy="sls"))
                 ts = []
                 for _ in range(2):
                     ctx.run_sweep(sp, cfgs, LAT, MEM, hist_bins=16)
                     ts.append(ctx.timings()["simulate"])
-                print("ils mode", mode, "ils alone", r_ils, "step", [round(t, 2) for t in ts])
+                print("mode", mode, "ils alone", r_ils, "sls alone", r_sls, "step", [round(t, 2) for t in ts])
             ctx.set_ils_kernel(0)
         elif cmd == "c4":  # every C4 job alone: device ms (and the compiled reference, 1 thread)
             from oracle.pyoracle import ref_lib
