@@ -367,8 +367,8 @@ def bench_configs(ctx, lib, capi, steps):
 
 
 SIM_NCU = {"scls": ("sim_kernel_scls_4096", "sim_kernel<SCLS>"),
-           "ils": ("sim_ils_indep_4096", "sim_ils_indep_kernel"),
-           "sls": ("sim_sls_indep_4096", "sim_sls_indep_kernel")}
+           "ils": ("sim_ils_indep_4096", "sim_ils_indep_kernel<split> (+ sim_ils_merge_kernel)"),
+           "sls": ("sim_sls_pack_4096", "sim_sls_pack_kernel (+ sim_sls_merge_kernel)")}
 REPORT_FIELDS = [f for f, _ in capi.TraceResult._fields_
                  if f not in ("sim_clock", "h_complete_ids", "h_dispatch", "h_complete_t", "h_log")]
 FIELD_WORD = {f: getattr(capi.TraceResult, f).offset // 8 for f, _ in capi.TraceResult._fields_}
