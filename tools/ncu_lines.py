@@ -51,3 +51,7 @@ for k, v in samples.most_common(top):
 print("== by L2 sectors")
 for k, v in sectors.most_common(top // 2):
     print(f"L2 {100 * v / tot_l2:5.1f}%  stall {100 * samples[k] / tot_s:5.1f}%  {k[0]}:{k[1]}  {text[k]}")
+tot_i = sum(insts.values()) or 1
+print("== by executed warp instructions")
+for k, v in insts.most_common(top):
+    print(f"inst {100 * v / tot_i:5.1f}%  stall {100 * samples[k] / tot_s:5.1f}%  {k[0]}:{k[1]}  {text[k]}")
