@@ -304,9 +304,28 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         // SCLS_DP_FAR_RR 2: all kSegs helpers deal the whole span [kmin, W]
         constexpr int kDeal = SCLS_DP_FAR_RR == 2 ? kSegs : kHalf;
         const int lim = SCLS_DP_FAR_RR == 2 ? span : rest;
-        for (int c0 = g * 8; c0 < lim; c0 += kDeal * 8) {
+#ifndef SCLS_DP_PRUNE_PRE
+#define SCLS_DP_PRUNE_PRE 0
+#endif
+        // the first SCLS_DP_PRUNE_PRE chunks' bounds loaded together, ahead of the scans
+        double lbv[SCLS_DP_PRUNE_PRE > 0 ? SCLS_DP_PRUNE_PRE : 1];
+#pragma unroll
+        for (int i = 0; i < SCLS_DP_PRUNE_PRE; ++i) {
+          const int c0 = g * 8 + i * kDeal * 8;
+          const int k0 = kmin + min(c0, lim - 1), k1 = min(kmin + lim - 1, k0 + 7);
+          lbv[i] = __dadd_rn(kGlobalT ? T[r - k1] : sm.ring[(r - k1) & M], cost[cb + k0]);
+        }
+        int ci = 0;
+        for (int c0 = g * 8; c0 < lim; c0 += kDeal * 8, ++ci) {
           const int k0 = kmin + c0, k1 = min(kmin + lim - 1, k0 + 7);
-          const double lb = __dadd_rn(kGlobalT ? T[r - k1] : sm.ring[(r - k1) & M], cost[cb + k0]);
+          double lb;
+          if (SCLS_DP_PRUNE_PRE > 0 && ci < SCLS_DP_PRUNE_PRE) {
+            lb = lbv[0];
+#pragma unroll
+            for (int i = 1; i < SCLS_DP_PRUNE_PRE; ++i) lb = ci == i ? lbv[i] : lb;
+          } else {
+            lb = __dadd_rn(kGlobalT ? T[r - k1] : sm.ring[(r - k1) & M], cost[cb + k0]);
+          }
           if (lb > ub) continue;
           double tv[8], cv[8];
 #pragma unroll

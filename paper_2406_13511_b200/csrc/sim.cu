@@ -341,6 +341,88 @@ __device__ bool warp_radix_sort(int n, uint64_t* k, int32_t* v, uint64_t* k2, in
 
 __device__ __forceinline__ int bits_of(uint32_t x) { return x ? 32 - __clz(x) : 0; }
 
+// The digit of a warp radix select: the smallest d with sum(bins[0..d]) > want
+// (want < the bins' total); want becomes the rank inside that digit.  Each
+// lane owns 8 consecutive digits, one warp scan finds the owner.
+__device__ __forceinline__ int select_digit(const int32_t* bins, int& want, int lane) {
+  int c[8], s = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    c[u] = bins[lane * 8 + u];
+    s += c[u];
+  }
+  int incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int owner = __ffs(__ballot_sync(FULL, incl > want)) - 1;
+  int digit = 0, acc = incl - s;
+  if (lane == owner) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (acc + c[u] > want) {
+        digit = lane * 8 + u;
+        break;
+      }
+      acc += c[u];
+    }
+  }
+  digit = __shfl_sync(FULL, digit, owner);
+  want -= __shfl_sync(FULL, acc, owner);
+  return digit;
+}
+
+// Report statistics over resp[0, completed) (completed > 0): the sum in
+// completion order (metrics.cpp:83-85: coalesced loads one chunk ahead, then
+// 32 dependent DADDs per chunk on broadcast values, every lane holding the
+// sum) and the nearest-rank p95 (metrics.cpp:87-91) by a radix select on the
+// order-preserving bits, whose first pass shares the sum's loads (the ILS /
+// SLS reports; out of line it cost the merge kernels 8%).
+#ifndef SCLS_RESP_STATS_INLINE
+#define SCLS_RESP_STATS_INLINE 1
+#endif
+#if SCLS_RESP_STATS_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void resp_stats(int lane, int completed, const double* resp, int32_t* bins, double* sum_out,
+                                        double* p95_out) {
+  const size_t rk = (size_t)ceil(__dmul_rn(0.95, (double)completed));
+  int want = (int)(rk > 1 ? rk : 1) - 1;
+  double sum = 0.0;
+  for (int i = lane; i < 256; i += 32) bins[i] = 0;
+  __syncwarp();
+  double v = lane < completed ? resp[lane] : 0.0;
+  for (int c = 0; c < completed; c += 32) {
+    const double vn = c + 32 + lane < completed ? resp[c + 32 + lane] : 0.0;
+    if (c + lane < completed) atomicAdd(&bins[ordered_bits(v) >> 56], 1);
+    const int m = min(32, completed - c);
+    for (int j = 0; j < m; ++j) sum = __dadd_rn(sum, __shfl_sync(FULL, v, j));
+    v = vn;
+  }
+  __syncwarp();
+  uint64_t prefix = (uint64_t)select_digit(bins, want, lane) << 56;
+  __syncwarp();
+  for (int shift = 48; shift >= 0; shift -= 8) {
+    for (int i = lane; i < 256; i += 32) bins[i] = 0;
+    __syncwarp();
+    const uint64_t hi_mask = ~0ull << (shift + 8);
+    for (int i = lane; i < completed; i += 32) {
+      const uint64_t k = ordered_bits(resp[i]);
+      if ((k & hi_mask) == prefix) atomicAdd(&bins[(k >> shift) & 0xff], 1);
+    }
+    __syncwarp();
+    prefix |= (uint64_t)select_digit(bins, want, lane) << shift;
+    __syncwarp();
+  }
+  const uint64_t u = (prefix & 0x8000000000000000ull) ? (prefix & ~0x8000000000000000ull) : ~prefix;
+  *sum_out = sum;
+  *p95_out = __longlong_as_double((long long)u);
+}
+
 // Per-worker (SCLS/SLS) / per-instance (ILS) state.  Worker w lives in lane
 // w & 31, slot w >> 5 of that lane's slots: V = 1 (W <= 32, one slot in
 // registers) or V = kWideV (any W > 32, the reference's worker_count >= 1 of
@@ -1494,7 +1576,10 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     const double span = last_completion - first_arrival;
     const double comp = (double)completed;
     thr = span > 0.0 ? __ddiv_rn(comp, span) : 0.0;
-    // mean in completion order (metrics.cpp:83-85)
+    // mean in completion order (metrics.cpp:83-85).  SCLS keeps this lane-0
+    // loop and the serial digit scan below: resp_stats() here measured 33.5
+    // -> 35.8 ms (inlined) / 36.4 ms (out of line) for the SCLS launch -- code
+    // layout and register allocation of the event loop, not this once-per-trace work.
     double sum = 0.0;
     if (lane == 0)
       for (int i = 0; i < completed; ++i) sum = __dadd_rn(sum, resp[i]);

@@ -154,46 +154,10 @@ __device__ void finish_report(int lane, scls_trace_result* R, int status, int n,
     const double span = last_completion - first_arrival;
     const double comp = (double)completed;
     thr = span > 0.0 ? __ddiv_rn(comp, span) : 0.0;
-    // sequential sum in completion order (metrics.cpp:83-85): coalesced loads,
-    // then 32 dependent DADDs per chunk on broadcast values (every lane holds it)
+    // sum in completion order (metrics.cpp:83-85) and nearest-rank p95 (metrics.cpp:87-91)
     double sum = 0.0;
-    for (int c = 0; c < completed; c += 32) {
-      const double v = c + lane < completed ? resp[c + lane] : 0.0;
-      const int m = min(32, completed - c);
-      for (int j = 0; j < m; ++j) sum = __dadd_rn(sum, shfl_d(v, j));
-    }
+    resp_stats(lane, completed, resp, bins, &sum, &p95);
     avg = __ddiv_rn(sum, comp);
-    const size_t rk = (size_t)ceil(__dmul_rn(0.95, comp));
-    int want = (int)(rk > 1 ? rk : 1) - 1;
-    uint64_t prefix = 0;
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      for (int i = lane; i < 256; i += 32) bins[i] = 0;
-      __syncwarp();
-      const uint64_t hi_mask = shift == 56 ? 0ull : (~0ull << (shift + 8));
-      for (int i = lane; i < completed; i += 32) {
-        const uint64_t k = ordered_bits(resp[i]);
-        if ((k & hi_mask) == prefix) atomicAdd(&bins[(k >> shift) & 0xff], 1);
-      }
-      __syncwarp();
-      int digit = 0;
-      if (lane == 0) {
-        int acc = 0;
-        for (int d = 0; d < 256; ++d) {
-          if (acc + bins[d] > want) {
-            digit = d;
-            break;
-          }
-          acc += bins[d];
-        }
-        want -= acc;
-      }
-      digit = shfl_i(digit, 0);
-      want = shfl_i(want, 0);
-      prefix |= (uint64_t)digit << shift;
-      __syncwarp();
-    }
-    const uint64_t u = (prefix & 0x8000000000000000ull) ? (prefix & ~0x8000000000000000ull) : ~prefix;
-    p95 = __longlong_as_double((long long)u);
     double mean = 0.0, var = 0.0;
     for (int w = 0; w < W; ++w) mean = __dadd_rn(mean, shfl_d(last_end, w));
     mean = __ddiv_rn(mean, (double)W);
