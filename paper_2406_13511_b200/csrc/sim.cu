@@ -2117,13 +2117,29 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
   for (int q = 0; q < 3; ++q) n_pol += !lists[q].empty() || !lists[3 + q].empty();
   const bool fork = ctx->sim_concurrent && n_pol > 1;
   if (fork) {
-    for (auto& st : ctx->side)
-      if (!st) SCLS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+#ifndef SCLS_SIM_PRIO
+#define SCLS_SIM_PRIO 0
+#endif
+    // SCLS_SIM_PRIO 1: the SCLS launch's stream (side[SCLS]) at the greatest
+    // priority, so its pending CTAs are placed before the other policies'
+    for (int q = 0; q < 3; ++q)
+      if (!ctx->side[q]) {
+        int lo = 0, hi = 0;
+        SCLS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        SCLS_CUDA(cudaStreamCreateWithPriority(&ctx->side[q], cudaStreamNonBlocking,
+                                               SCLS_SIM_PRIO && q == SCLS_POLICY_SCLS ? hi : lo));
+      }
     SCLS_CUDA(cudaEventRecord(ctx->ev[8], s));
   }
   int64_t at = 0;
   int k = 0;
-  for (int pol : {SCLS_POLICY_ILS, SCLS_POLICY_SCLS, SCLS_POLICY_SLS}) {  // longest first
+#ifndef SCLS_SIM_ORDER
+#define SCLS_SIM_ORDER 0
+#endif
+  constexpr int kOrder[3][3] = {{SCLS_POLICY_ILS, SCLS_POLICY_SCLS, SCLS_POLICY_SLS},
+                                {SCLS_POLICY_SCLS, SCLS_POLICY_ILS, SCLS_POLICY_SLS},
+                                {SCLS_POLICY_SCLS, SCLS_POLICY_SLS, SCLS_POLICY_ILS}};
+  for (int pol : kOrder[SCLS_SIM_ORDER]) {  // longest first
     const int32_t cnt = (int32_t)lists[pol].size(), wcnt = (int32_t)lists[3 + pol].size();
     int64_t off = 0, woff = 0;
     for (int q = 0; q < pol; ++q) off += (int64_t)lists[q].size();
@@ -2131,7 +2147,7 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
     if (cnt == 0 && wcnt == 0) continue;
     cudaStream_t ls = s;
     if (fork) {
-      ls = ctx->side[k];
+      ls = ctx->side[pol];
       SCLS_CUDA(cudaStreamWaitEvent(ls, ctx->ev[8], 0));
     }
     const int wpb = kSimWarps;

@@ -37,6 +37,14 @@ struct IlsRec {
   double* r;   // response (t - arrival)
 };
 
+#ifndef SCLS_MERGE_SORT
+#define SCLS_MERGE_SORT 1
+#endif
+// per policy: ILS keeps the W-way merge (alone 16.7 vs 18.1 ms sorted, the
+// step the same), SLS sorts (8.07 -> 7.88 ms alone)
+#ifndef SCLS_MERGE_SORT_ILS
+#define SCLS_MERGE_SORT_ILS 0
+#endif
 #ifndef SCLS_MERGE_WIN
 #define SCLS_MERGE_WIN 256
 #endif
@@ -170,6 +178,88 @@ __device__ bool merge_completions(int lane, int W, int comp, int completed, doub
   return false;
 }
 
+// The same replay by sorting instead of a W-way merge (SCLS_MERGE_SORT, the
+// split kernels' default): every completion becomes a 64-bit key -- the
+// 32-bit fixed-point image of its time over its source (record index << 5 |
+// instance) -- and a warp LSD radix sort on the image (4 passes, stable, so
+// equal images stay in instance-major order) orders the job in ~2.5 warp
+// instructions per completion, where a merge step costs ~50.  Equal images
+// from different instances are then put in exact (time, push time) order by
+// an insertion sort of their run (lane 0; rare), which also detects the exact
+// cross-instance tie that needs the lock-step kernel (returns true).  kA and
+// kB are per-job scratch of >= completed keys each (kB may alias resp); the
+// responses land in resp in the reference's order.
+__device__ bool sort_completions(int lane, int W, int comp, int completed, double last_completion, int64_t cap_w,
+                                 const double* __restrict__ ct, const double* __restrict__ cp,
+                                 const double* __restrict__ cr, double* resp, uint64_t* kA, uint64_t* kB,
+                                 int32_t* bins) {
+  if (completed == 0) return false;
+  const int mine = lane < W ? comp : 0;
+  double t_lo = mine > 0 ? ct[lane * cap_w] : dinf();
+  for (int o = 16; o; o >>= 1) t_lo = fmin(t_lo, __shfl_xor_sync(FULL, t_lo, o));
+  const double span = __dsub_rn(last_completion, t_lo);
+  const double scale = span > 0.0 ? __ddiv_rn(4294967040.0, span) : 0.0;
+  int off = mine;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, off, o);
+    if (lane >= o) off += y;
+  }
+  off -= mine;
+  for (int w = 0; w < W; ++w) {
+    const int cw = __shfl_sync(FULL, mine, w), ow = __shfl_sync(FULL, off, w);
+    for (int i = lane; i < cw; i += 32) {
+      const double tv = ct[w * cap_w + i];
+      const uint32_t q = (uint32_t)__dmul_rn(__dsub_rn(tv, t_lo), scale);
+      kA[ow + i] = ((uint64_t)q << 32) | ((uint32_t)i << 5) | (uint32_t)w;
+    }
+  }
+  __syncwarp();
+  uint64_t* keys = warp_radix_sort(completed, kA, nullptr, kB, nullptr, 64, lane, bins, 32) ? kB : kA;
+  auto rec = [&](uint64_t k) { return (int64_t)(k & 31u) * cap_w + (int64_t)((uint32_t)k >> 5); };
+  int fixed_end = 0;  // runs [.., fixed_end) already put in exact order
+  for (int c = 0; c + 1 < completed; c += 32) {
+    const int i = c + lane;
+    bool f = false;
+    if (i + 1 < completed) {
+      const uint64_t a = keys[i], b = keys[i + 1];
+      f = (a >> 32) == (b >> 32) && (a & 31u) != (b & 31u);
+    }
+    for (unsigned m = __ballot_sync(FULL, f); m; m &= m - 1u) {
+      const int p = c + __ffs(m) - 1;
+      int tie = 0;
+      if (lane == 0 && p >= fixed_end) {
+        const uint32_t img = (uint32_t)(keys[p] >> 32);
+        int a = p, b = p + 2;
+        while (a > 0 && (uint32_t)(keys[a - 1] >> 32) == img) --a;
+        while (b < completed && (uint32_t)(keys[b] >> 32) == img) ++b;
+        for (int x = a + 1; x < b && !tie; ++x) {  // stable insertion sort by exact (time, push time)
+          const uint64_t kx = keys[x];
+          const double tx = ct[rec(kx)], px = cp[rec(kx)];
+          int y = x - 1;
+          for (; y >= a; --y) {
+            const uint64_t ky = keys[y];
+            const double ty = ct[rec(ky)], py = cp[rec(ky)];
+            if (ty < tx || (ty == tx && py < px)) break;
+            if (ty == tx && py == px) {
+              tie = (ky & 31u) != (kx & 31u);  // the same event of one instance keeps its order
+              break;
+            }
+            keys[y + 1] = ky;
+          }
+          keys[y + 1] = kx;
+        }
+        fixed_end = b;
+      }
+      __syncwarp();
+      fixed_end = __shfl_sync(FULL, fixed_end, 0);
+      if (__shfl_sync(FULL, tie, 0)) return true;
+    }
+  }
+  __syncwarp();
+  for (int i = lane; i < completed; i += 32) resp[i] = cr[rec(keys[i])];
+  return false;
+}
+
 #ifndef SCLS_ILS_INDEP_MINB
 #define SCLS_ILS_INDEP_MINB 4
 #endif
@@ -273,9 +363,14 @@ __device__ void ils_finish_job(const SimParams& P, int t, int W, int MC, int lan
   double last_completion = lc;
   for (int o = 16; o; o >>= 1) last_completion = fmax(last_completion, __shfl_xor_sync(FULL, last_completion, o));
   double* resp = (double*)(J.base + J.Lay.resp);
-  const bool tie = merge_completions(lane, W, c, completed, last_completion, J.cap_w,
-                                     (const double*)(J.base + J.Lay.ct), (const double*)(J.base + J.Lay.cp),
-                                     (const double*)(J.base + J.Lay.cr), nullptr, resp, wt, wr, wq, nullptr);
+  const bool tie =
+      SCLS_MERGE_SORT && SCLS_MERGE_SORT_ILS && J.cap_w < (1 << 27)
+          ? sort_completions(lane, W, c, completed, last_completion, J.cap_w, (const double*)(J.base + J.Lay.ct),
+                             (const double*)(J.base + J.Lay.cp), (const double*)(J.base + J.Lay.cr), resp,
+                             (uint64_t*)(J.base + J.Lay.gen), (uint64_t*)resp, bins)
+          : merge_completions(lane, W, c, completed, last_completion, J.cap_w, (const double*)(J.base + J.Lay.ct),
+                              (const double*)(J.base + J.Lay.cp), (const double*)(J.base + J.Lay.cr), nullptr, resp,
+                              wt, wr, wq, nullptr);
   if (tie) {  // the exact lock-step kernel re-runs this job
     if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = J.t;
     return;
@@ -565,12 +660,18 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_ILS_INDEP_MINB)
 __global__ void __launch_bounds__(kSimWarps * 32) sim_ils_merge_kernel(SimParams P, const int32_t* __restrict__ list,
                                                                       int32_t count, int32_t* __restrict__ fb_count,
                                                                       int32_t* __restrict__ fb_list) {
-  __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
-  __shared__ double swin_r[kSimWarps][kMergeWin];
-  __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
+  // sort mode: the radix bins / p95 bins only (256 ints); merge mode: the windows too
+  constexpr bool kSort = SCLS_MERGE_SORT && SCLS_MERGE_SORT_ILS;
+  constexpr int kWin = kSort ? 128 : kMergeWin, kWin2 = kSort ? 1 : kMergeWin;
+  __shared__ uint64_t swin_t[kSimWarps][kWin];
+  __shared__ double swin_r[kSimWarps][kWin2];
+  __shared__ uint32_t swin_q[kSimWarps][kWin2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= count) return;
+#ifdef SCLS_SKIP_MERGE  // timing experiment only: no reports
+  return;
+#endif
   const int t = list[g];
   if (t < 0) return;
   const int ci = P.cfg_index ? P.cfg_index[t] : 0;
@@ -650,9 +751,13 @@ __device__ void sls_finish_job(const SimParams& P, int t, int W, int lane, const
     __syncwarp();
     for (int i = lane; i < completed; i += 32) resp[i] = cr[i];
   } else {
-    tie = merge_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),
-                            (const double*)(base + Lay.cp), (const double*)(base + Lay.cr),
-                            (const int32_t*)(base + Lay.cn), resp, wt, wr, wq, wn);
+    tie = SCLS_MERGE_SORT && cap_w < (1 << 27)
+              ? sort_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),
+                                 (const double*)(base + Lay.cp), (const double*)(base + Lay.cr), resp,
+                                 (uint64_t*)(base + Lay.gen), (uint64_t*)resp, bins)
+              : merge_completions(lane, W, comp, completed, last_completion, cap_w, (const double*)(base + Lay.ct),
+                                  (const double*)(base + Lay.cp), (const double*)(base + Lay.cr),
+                                  (const int32_t*)(base + Lay.cn), resp, wt, wr, wq, wn);
   }
   if (tie) {  // the exact lock-step kernel re-runs this job
     if (lane == 0) fb_list[atomicAdd(fb_count, 1)] = t;
@@ -840,13 +945,17 @@ __global__ void __launch_bounds__(kSimWarps * 32, SCLS_SLS_INDEP_MINB)
 __global__ void __launch_bounds__(kSimWarps * 32) sim_sls_merge_kernel(SimParams P, const int32_t* __restrict__ list,
                                                                       int32_t count, int32_t* __restrict__ fb_count,
                                                                       int32_t* __restrict__ fb_list) {
-  __shared__ uint64_t swin_t[kSimWarps][kMergeWin];
-  __shared__ double swin_r[kSimWarps][kMergeWin];
-  __shared__ uint32_t swin_q[kSimWarps][kMergeWin];
-  __shared__ uint8_t swin_n[kSimWarps][kMergeWin];
+  constexpr int kWin = SCLS_MERGE_SORT ? 128 : kMergeWin, kWin2 = SCLS_MERGE_SORT ? 1 : kMergeWin;
+  __shared__ uint64_t swin_t[kSimWarps][kWin];
+  __shared__ double swin_r[kSimWarps][kWin2];
+  __shared__ uint32_t swin_q[kSimWarps][kWin2];
+  __shared__ uint8_t swin_n[kSimWarps][kWin2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x * (blockDim.x >> 5) + warp;
   if (g >= count) return;
+#ifdef SCLS_SKIP_MERGE  // timing experiment only: no reports
+  return;
+#endif
   const int t = list[g];
   if (t < 0) return;
   const int ci = P.cfg_index ? P.cfg_index[t] : 0;

@@ -4,6 +4,7 @@
   python tools/probe.py scls-dp [traces]   SCLS kernel ms per tick-DP mode (auto / chain)
   python tools/probe.py one <policy> [traces] one device-generated sweep of one policy (ncu target)
   python tools/probe.py c4                 every C4 job alone, device ms next to the reference (1 thread)
+  python tools/probe.py step [traces]      the 3-policy C5 step (simulate phase), 5 reps
   python tools/probe.py scls-prof [traces] [rates]
                                            per-phase clock64 split of the SCLS kernel
                                            (needs SCLS_B200_LIB = a -DSCLS_SIM_PROF build)
@@ -39,6 +40,23 @@ def main():
         if cmd == "sweep":
             out = {p: kernel_ms(ctx, specs(T), capi.sched_cfg(policy=p)) for p in ("scls", "ils", "sls")}
             print(out, "sum", round(sum(out.values()), 2))
+        elif cmd == "step":  # the 3-policy C5 step (simulate only, device-generated traces), 5 reps
+            sp = specs(T)
+            cfgs = [capi.sched_cfg(policy=p) for p in ("scls", "sls", "ils")]
+            ts = []
+            for _ in range(5):
+                ctx.run_sweep(sp, cfgs, LAT, MEM, hist_bins=16)
+                ts.append(ctx.timings()["simulate"])
+            print("step simulate ms", [round(t, 2) for t in ts], "median %.2f" % sorted(ts)[2])
+        elif cmd == "pairs":  # which policy bounds the concurrent step: every subset's simulate ms
+            sp = specs(T)
+            for pols in (("scls", "sls", "ils"), ("scls", "sls"), ("scls", "ils"), ("sls", "ils"), ("scls",), ("ils",)):
+                cfgs = [capi.sched_cfg(policy=p) for p in pols]
+                ts = []
+                for _ in range(3):
+                    ctx.run_sweep(sp, cfgs, LAT, MEM, hist_bins=16)
+                    ts.append(ctx.timings()["simulate"])
+                print(pols, "%.2f" % min(ts))
         elif cmd == "scls-dp":
             for mode in (0, 1):
                 ctx.set_dp_kernel(mode)
