@@ -632,6 +632,35 @@ __global__ void __launch_bounds__(kDpThreads, 1)
 #endif
   constexpr bool kPipe = SCLS_DP_PIPE && kC == 1 && kStagers && !kGlobalT;
   constexpr int kBarFar = 2, kBarTile = 3;
+#ifndef SCLS_DP_MID_HELPERS
+#define SCLS_DP_MID_HELPERS 0
+#endif
+  // The mid candidates (sources in the previous tile) on the helpers: at the
+  // start of tile t each helper folds ~3 of the 32 sources into its own far
+  // partial of tile t, then arrives on kBarMid; the main warp waits there and
+  // merges the 12 partials as before -- its 32-candidate mid scan leaves the
+  // critical path.
+  constexpr bool kMidH = SCLS_DP_MID_HELPERS && kC == 1 && kStagers && SCLS_DP_MAIN_MERGE && !kPipe;
+  constexpr int kBarMid = 4, kMidThreads = 32 * (kMonoSegs + 1);
+  auto mid_fold = [&](int u) {
+    const int uB = u << 5;
+    const int b = u % 3, rs_ = sm.rs[b][lane];
+    double best = sm.Pv[u & 1][h][lane];
+    int bk = sm.Pk[u & 1][h][lane];
+    for (int jj = h; jj < 32; jj += kMonoSegs) {  // ascending j
+      const int j = uB - 31 + jj;
+      if (j >= 0) {
+        const int k = lane + 32 - jj;
+        const double cand = __dadd_rn(sm.ring[j & M], csv(b, rs_, k));
+        if (lex_lt(cand, k, best, bk)) {
+          best = cand;
+          bk = k;
+        }
+      }
+    }
+    sm.Pv[u & 1][h][lane] = best;
+    sm.Pk[u & 1][h][lane] = bk;
+  };
   for (int t = 0; t < ntiles; ++t) {
     const int tB = t << 5;
     if (kPipe && t > 0) {
@@ -651,12 +680,14 @@ __global__ void __launch_bounds__(kDpThreads, 1)
       double acc = kInf;
       int kb = 0;
       if (kC == 1 && SCLS_DP_MAIN_MERGE) {
+        if (kMidH) asm volatile("bar.sync %0, %1;" ::"n"(kBarMid), "n"(kMidThreads) : "memory");
         merge12(sm.Pv[t & 1], sm.Pk[t & 1], acc, kb);
       } else {
         acc = sm.Fv[t & 1][lane];
         kb = sm.Fk[t & 1][lane];
       }
       // mid: sources j = tB-31 .. tB (k = lane+32-jj), 4 interleaved chains
+      if (!kMidH) {
       double va[8] = {kInf, kInf, kInf, kInf, kInf, kInf, kInf, kInf};
       int ka[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
@@ -706,6 +737,7 @@ __global__ void __launch_bounds__(kDpThreads, 1)
             kb = ka[q];
           }
       }
+      }  // !kMidH
       // rounds
       if (prof) c_mid += clock64() - t0;
       const double c1 = csv(cbuf, rsl, 1);
@@ -785,6 +817,10 @@ __global__ void __launch_bounds__(kDpThreads, 1)
       t1 = prof ? clock64() : 0;
     } else if (helper) {
       if (kStagers) {
+        if (kMidH) {
+          mid_fold(t);
+          asm volatile("bar.arrive %0, %1;" ::"n"(kBarMid), "n"(kMidThreads) : "memory");
+        }
         t1 = prof ? clock64() : 0;
         far(t + 1);
       } else {
