@@ -10,3 +10,4 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
 $NCU -k regex:sim_kernel -o gpurun_out/prof_scls_${TAG} python tools/probe.py one scls 4096 > /dev/null 2>&1; echo scls=$?
 $NCU -k regex:dp_mono -o gpurun_out/prof_dp_${TAG} python tools/probe_c3_once.py > /dev/null 2>&1; echo dp=$?
 tail -1 gpurun_out/${TAG}_bench.log
+$NCU -k regex:sim_sls_merge -o gpurun_out/prof_slsm_${TAG} python tools/probe.py one sls 4096 > /dev/null 2>&1; echo slsm=$?
