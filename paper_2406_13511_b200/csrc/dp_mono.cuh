@@ -302,6 +302,10 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         double b2 = kInf;
         int k2 = 0;
         // SCLS_DP_FAR_RR 2: all kSegs helpers deal the whole span [kmin, W]
+#ifndef SCLS_DP_FAR_CHUNK
+#define SCLS_DP_FAR_CHUNK 16
+#endif
+        constexpr int kCh = SCLS_DP_FAR_CHUNK;
         constexpr int kDeal = SCLS_DP_FAR_RR == 2 ? kSegs : kHalf;
         const int lim = SCLS_DP_FAR_RR == 2 ? span : rest;
 #ifndef SCLS_DP_PRUNE_PRE
@@ -311,13 +315,13 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         double lbv[SCLS_DP_PRUNE_PRE > 0 ? SCLS_DP_PRUNE_PRE : 1];
 #pragma unroll
         for (int i = 0; i < SCLS_DP_PRUNE_PRE; ++i) {
-          const int c0 = g * 8 + i * kDeal * 8;
-          const int k0 = kmin + min(c0, lim - 1), k1 = min(kmin + lim - 1, k0 + 7);
+          const int c0 = g * kCh + i * kDeal * kCh;
+          const int k0 = kmin + min(c0, lim - 1), k1 = min(kmin + lim - 1, k0 + kCh - 1);
           lbv[i] = __dadd_rn(kGlobalT ? T[r - k1] : sm.ring[(r - k1) & M], cost[cb + k0]);
         }
         int ci = 0;
-        for (int c0 = g * 8; c0 < lim; c0 += kDeal * 8, ++ci) {
-          const int k0 = kmin + c0, k1 = min(kmin + lim - 1, k0 + 7);
+        for (int c0 = g * kCh; c0 < lim; c0 += kDeal * kCh, ++ci) {
+          const int k0 = kmin + c0, k1 = min(kmin + lim - 1, k0 + kCh - 1);
           double lb;
           if (SCLS_DP_PRUNE_PRE > 0 && ci < SCLS_DP_PRUNE_PRE) {
             lb = lbv[0];
@@ -327,16 +331,16 @@ __global__ void __launch_bounds__(kDpThreads, 1)
             lb = __dadd_rn(kGlobalT ? T[r - k1] : sm.ring[(r - k1) & M], cost[cb + k0]);
           }
           if (lb > ub) continue;
-          double tv[8], cv[8];
+          double tv[kCh], cv[kCh];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < kCh; ++i) {
             const int k = min(k0 + i, k1);
             const int j = r - k;
             tv[i] = kGlobalT ? T[j] : sm.ring[j & M];
             cv[i] = cost[cb + k];
           }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < kCh; ++i) {
             const double cand = k0 + i <= k1 ? __dadd_rn(tv[i], cv[i]) : kInf;
             if (i & 1) {
               if (cand < b2) {
