@@ -690,8 +690,21 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         acc = sm.Fv[t & 1][lane];
         kb = sm.Fk[t & 1][lane];
       }
-      // mid: sources j = tB-31 .. tB (k = lane+32-jj), 4 interleaved chains
-      if (!kMidH) {
+      // mid: sources j = tB-31 .. tB (k = lane+32-jj), 4 interleaved chains.
+      // Skipped when it cannot win (exact, monotone case): every mid
+      // candidate of row r is >= fl(T[tB-31] + c(L_r, lane+1)) -- T is
+      // non-decreasing in j and c in k -- so a row whose far minimum is
+      // strictly below that bound keeps it; on C3 the optimum batch (~89
+      // rows) lies in the far range and the whole warp usually skips.
+#ifndef SCLS_DP_MID_SKIP
+#define SCLS_DP_MID_SKIP 0
+#endif
+      bool mid_needed = true;
+      if (SCLS_DP_MID_SKIP) {
+        const double lbm = __dadd_rn(sm.ring[max(tB - 31, 0) & M], csv(cbuf, rsl, lane + 1));
+        mid_needed = __any_sync(0xffffffffu, !(lbm > acc));
+      }
+      if (!kMidH && mid_needed) {
       double va[8] = {kInf, kInf, kInf, kInf, kInf, kInf, kInf, kInf};
       int ka[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
