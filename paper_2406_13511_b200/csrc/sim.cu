@@ -600,10 +600,8 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   int32_t* tl_e = (int32_t*)(base + Lay.tl_e);
   int32_t* tl_s = (int32_t*)(base + Lay.tl_s);
   double* tl_a = (double*)(base + Lay.tl_a);
-  int32_t* b_start = (int32_t*)(base + Lay.b_start);
-  int32_t* b_n = (int32_t*)(base + Lay.b_n);
-  int32_t* b_lin = (int32_t*)(base + Lay.b_lin);
-  int32_t* b_served = (int32_t*)(base + Lay.b_served);
+  // batch descriptors {tick-log start, members, l_in, served l_out}: one 16 B load per use
+  int4* bd = (int4*)(base + Lay.b_start);
   int32_t* b_next = (int32_t*)(base + Lay.b_next);
   double* b_est = (double*)(base + Lay.b_est);
   const int cap_w = W > 0 ? (n + W - 1) / W : 0;
@@ -666,7 +664,8 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       k.q_head = nb_next;
       if (k.q_head < 0) k.q_tail = -1;
     }
-    const int bn = b_n[b], blin = b_lin[b], bsv = b_served[b];
+    const int4 d = bd[b];
+    const int bn = d.y, blin = d.z, bsv = d.w;
     sink.record(lane, 3, clock, -1, w, b, bn, blin, 0, 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
     const double serve = batch_serve_time(lat, bn, blin, bsv);
     if (MINE(w)) {
@@ -1039,15 +1038,12 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           const int beg = b == 0 ? 0 : segs[nb - b];
           const int bi = (int)next_batch + b;
           const int L = sv[end - 1];
-          b_start[bi] = tl_pos + beg;
-          b_n[bi] = end - beg;
-          b_lin[bi] = L;
           b_est[bi] = cost[coff[L] - 1 + (end - beg)];
           // slice_served_l_out (sched_policies.cpp:72-80): max over members
           int served = 0;
 #pragma unroll kEmitU
           for (int q = tl_pos + beg; q < tl_pos + end; ++q) served = max(served, min(tl_t[q] - tl_g[q], C.S));
-          b_served[bi] = served;
+          bd[bi] = make_int4(tl_pos + beg, end - beg, L, served);
         }
       }
       tl_pos += P_;
@@ -1087,8 +1083,9 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       const int w = argmin_worker_load<V>(ws, W, lane);  // min (load, worker id)
       if (MINE(w)) WK(w).load = __dadd_rn(WK(w).load, e);
       // dispatch record (served l_out computed at emit), enqueue
-      const int bn = b_n[b];
-      sink.record(lane, 2, clock, -1, w, b, bn, b_lin[b], C.S, 0, e, 0, 0, 0.0, 0, 0.0, 0);
+      const int4 d = bd[b];
+      const int bn = d.y;
+      sink.record(lane, 2, clock, -1, w, b, bn, d.z, C.S, 0, e, 0, 0, 0.0, 0, 0.0, 0);
       if (lane == 0) b_next[b] = -1;
       const int tail = shfl_i(WK(w).q_tail, WL(w));
       if (lane == 0 && tail >= 0) b_next[tail] = b;
@@ -1113,7 +1110,8 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
 
   // SCLS on_batch_done (sched_policies.cpp:149-188) for worker w, batch b.
   auto scls_done = [&](int w, int b) {
-    const int bn = b_n[b], bst = b_start[b], lin = b_lin[b], served = b_served[b];
+    const int4 d = bd[b];
+    const int bn = d.y, bst = d.x, lin = d.z, served = d.w;
     const double best = b_est[b];
     sink.record(lane, 4, clock, -1, w, b, bn, lin, C.S, served, 0.0, 0, 0, 0.0, 0, 0.0, bn);
     ++batch_count;

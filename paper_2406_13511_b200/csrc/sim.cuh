@@ -71,10 +71,8 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
     L.tl_e = take(4 * (cap + 1));
     L.tl_s = take(4 * (cap + 1));
     L.tl_a = take(8 * (cap + 1));
-    L.b_start = take(4 * (cap + 1));
-    L.b_n = take(4 * (cap + 1));
-    L.b_lin = take(4 * (cap + 1));
-    L.b_served = take(4 * (cap + 1));
+    L.b_start = take(16 * (cap + 1));  // int4 {start, n, l_in, served} per batch
+    L.b_n = L.b_lin = L.b_served = 0;
     L.b_next = take(4 * (cap + 1));
     L.b_est = take(8 * (cap + 1));
   } else if (policy == SCLS_POLICY_SLS) {
