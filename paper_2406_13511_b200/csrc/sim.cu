@@ -507,6 +507,21 @@ __device__ __forceinline__ double min_worker_load(Slots<V>& ws, int W, int lane)
 
 // ---- the per-trace simulation -------------------------------------------------------
 
+// SCLS records (sim.cuh layout): a repooled request's state by pool slot, and
+// a tick-log entry per batched slot; 32 B each, read as one 16 B vector and
+// one double from the same sector.
+struct __align__(32) PoolRec {
+  int4 gts;  // generated, true gen, slices, -
+  double a;  // arrival
+  double pad;
+};
+struct __align__(32) TickRec {
+  int4 igte;  // id, generated, true gen, effective input
+  int32_t s, pad;
+  double a;   // arrival
+};
+static_assert(sizeof(PoolRec) == 32 && sizeof(TickRec) == 32, "sim.cuh SCLS record sizes");
+
 template <int POL, bool kHash, bool kLog, int V>
 __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, int32_t* ssplit, double* sT) {
   const int ts = P.src ? P.src[t] : t;  // source trace of job t
@@ -584,22 +599,14 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   // Policy-specific arena views.
   int32_t* pool = (int32_t*)(base + Lay.pool);  // SCLS pool records: id, eff, generated, true gen, slices, arrival
   int32_t* p_eff = (int32_t*)(base + Lay.p_eff);
-  int32_t* p_g = (int32_t*)(base + Lay.p_g);
-  int32_t* p_t = (int32_t*)(base + Lay.p_t);
-  int32_t* p_s = (int32_t*)(base + Lay.p_s);
-  double* p_a = (double*)(base + Lay.p_a);
+  PoolRec* prec = (PoolRec*)(base + Lay.p_g);  // repooled records by pool slot
   uint64_t* sk = (uint64_t*)(base + Lay.sk);
   uint64_t* sk2 = (uint64_t*)(base + Lay.sk2);
   int32_t* sv = (int32_t*)(base + Lay.sv);
   double* Tg = (double*)(base + Lay.T);
   int32_t* split_g = (int32_t*)(base + Lay.split);
   int32_t* segs = (int32_t*)(base + Lay.segs);
-  int32_t* tlog = (int32_t*)(base + Lay.tlog);
-  int32_t* tl_g = (int32_t*)(base + Lay.tl_g);
-  int32_t* tl_t = (int32_t*)(base + Lay.tl_t);
-  int32_t* tl_e = (int32_t*)(base + Lay.tl_e);
-  int32_t* tl_s = (int32_t*)(base + Lay.tl_s);
-  double* tl_a = (double*)(base + Lay.tl_a);
+  TickRec* tlog = (TickRec*)(base + Lay.tlog);  // the tick log
   // batch descriptors {tick-log start, members, l_in, served l_out}: one 16 B load per use
   int4* bd = (int4*)(base + Lay.b_start);
   int32_t* b_next = (int32_t*)(base + Lay.b_next);
@@ -790,10 +797,16 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           L[u] = (int)(key[u] >> (kb_id + idb));
           // a repooled record, or a fresh arrival (slot >= n_rec: its input row)
           const bool rec = ok && q[u] < n_rec;
-          g_[u] = rec ? p_g[q[u]] : 0;
-          t_[u] = rec ? p_t[q[u]] : (ok ? tg[id[u]] : 0);
-          s_[u] = rec ? p_s[q[u]] : 0;
-          a_[u] = rec ? p_a[q[u]] : (ok ? arr[id[u]] : 0.0);
+          int4 pr = make_int4(0, 0, 0, 0);
+          double pa = 0.0;
+          if (rec) {
+            pr = prec[q[u]].gts;
+            pa = prec[q[u]].a;
+          }
+          g_[u] = pr.x;
+          t_[u] = rec ? pr.y : (ok ? tg[id[u]] : 0);
+          s_[u] = pr.z;
+          a_[u] = rec ? pa : (ok ? arr[id[u]] : 0.0);
           k_[u] = ok && L[u] <= P.Lmax ? __ldg(Kt + L[u]) : 0;
         }
 #pragma unroll
@@ -801,12 +814,9 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           const int i = i0 + 32 * u;
           if (i < P_) {
             const int64_t qq = tl_pos + i;
-            tlog[qq] = id[u];
-            tl_g[qq] = g_[u];
-            tl_t[qq] = t_[u];
-            tl_e[qq] = L[u];
-            tl_s[qq] = s_[u];
-            tl_a[qq] = a_[u];
+            tlog[qq].igte = make_int4(id[u], g_[u], t_[u], L[u]);
+            tlog[qq].s = s_[u];
+            tlog[qq].a = a_[u];
             sv[i] = L[u];
             if (L[u] > P.Lmax || k_[u] == 0) bad = min(bad, i);
           }
@@ -815,7 +825,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       bad = __reduce_min_sync(FULL, bad);
       __syncwarp();
       if (bad != 0x7fffffff) {
-        err_req = tlog[tl_pos + bad];
+        err_req = tlog[tl_pos + bad].igte.x;
         return SCLS_ERR_INFEASIBLE_REQUEST;
       }
       SIM_PROF(4);
@@ -1042,7 +1052,10 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           // slice_served_l_out (sched_policies.cpp:72-80): max over members
           int served = 0;
 #pragma unroll kEmitU
-          for (int q = tl_pos + beg; q < tl_pos + end; ++q) served = max(served, min(tl_t[q] - tl_g[q], C.S));
+          for (int q = tl_pos + beg; q < tl_pos + end; ++q) {
+            const int4 v = tlog[q].igte;
+            served = max(served, min(v.z - v.y, C.S));
+          }
           bd[bi] = make_int4(tl_pos + beg, end - beg, L, served);
         }
       }
@@ -1132,12 +1145,13 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       int ng = 0, tgv = 0;
       if (ok) {
         const int q = bst + i;
-        id = tlog[q];
-        const int gsf = tl_g[q];
-        tgv = tl_t[q];
-        eff = tl_e[q];
-        s1 = tl_s[q] + 1;
-        ta = tl_a[q];
+        const int4 v = tlog[q].igte;
+        id = v.x;
+        const int gsf = v.y;
+        tgv = v.z;
+        eff = v.w;
+        s1 = tlog[q].s + 1;
+        ta = tlog[q].a;
         g = min(tgv - gsf, served);
         pad = lin - eff;
         inv = served - g;
@@ -1154,10 +1168,8 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         const int d = pool_len + __popc(pm & lt);
         pool[d] = id;
         p_eff[d] = eff + g;
-        p_g[d] = ng;
-        p_t[d] = tgv;
-        p_s[d] = s1;
-        p_a[d] = ta;
+        prec[d].gts = make_int4(ng, tgv, s1, 0);
+        prec[d].a = ta;
       }
       pool_len += __popc(pm);
       if (one) {
@@ -1187,9 +1199,9 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     for (int c0 = 0; c0 < nfin; c0 += 32) {  // completions from the slot state
       const int cnt = min(32, nfin - c0);
       const int q = lane < cnt ? fin[c0 + lane] : 0;
-      const int id = lane < cnt ? tlog[q] : 0;
-      const double r = lane < cnt ? clock - tl_a[q] : 0.0;
-      const int s = lane < cnt ? tl_s[q] + 1 : 0;
+      const int id = lane < cnt ? tlog[q].igte.x : 0;
+      const double r = lane < cnt ? clock - tlog[q].a : 0.0;
+      const int s = lane < cnt ? tlog[q].s + 1 : 0;
       if (lane < cnt) {
         resp[completed + lane] = r;
         if (hist && s < P.hist_bins) atomicAdd((unsigned long long*)&hist[s], 1ull);

@@ -51,26 +51,24 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
     // arrivals are the id range since the last tick (their input rows).
     L.pool = take(4 * n1);
     L.p_eff = take(4 * n1);
-    L.p_g = take(4 * n1);
-    L.p_t = take(4 * n1);
-    L.p_s = take(4 * n1);
-    L.p_a = take(8 * n1);
+    // {generated, true gen, slices, -, arrival, -}: 32 B per repooled record,
+    // gathered by pool slot in the tick's rows pass (one sector per member)
+    o = (o + 31) & ~(int64_t)31;
+    L.p_g = take(32 * n1);
+    L.p_t = L.p_s = L.p_a = 0;
     L.sk = take(8 * n1);
     L.sk2 = take(8 * n1);
     L.sv = take(4 * n1);
     L.T = take(8 * (n1 + 1));
     L.split = take(4 * (n1 + 1));
     L.segs = take(4 * (n1 + 1));
-    L.tlog = take(4 * (cap + 1));
-    // per-slot request state captured when the slot is batched (the request's
-    // generated count, true gen, effective input, slices so far, arrival), so
-    // offload and batch completion read slot-contiguous memory instead of
-    // chasing request ids
-    L.tl_g = take(4 * (cap + 1));
-    L.tl_t = take(4 * (cap + 1));
-    L.tl_e = take(4 * (cap + 1));
-    L.tl_s = take(4 * (cap + 1));
-    L.tl_a = take(8 * (cap + 1));
+    // the tick log: per batched slot the request's state when it was batched
+    // {id, generated, true gen, effective input, slices, -, arrival}, 32 B,
+    // so offload and batch completion read slot-contiguous records instead
+    // of chasing request ids
+    o = (o + 31) & ~(int64_t)31;
+    L.tlog = take(32 * (cap + 1));
+    L.tl_g = L.tl_t = L.tl_e = L.tl_s = L.tl_a = 0;
     L.b_start = take(16 * (cap + 1));  // int4 {start, n, l_in, served} per batch
     L.b_n = L.b_lin = L.b_served = 0;
     L.b_next = take(4 * (cap + 1));
@@ -96,7 +94,7 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
     L.isum = take(48 * ((int64_t)W + 1));
   }
   L.ws = take(W > 32 ? kWorkerSlotBytes * 32 * (((int64_t)W + 31) / 32) : 0);
-  L.total = o;
+  L.total = (o + 127) & ~(int64_t)127;  // trace arenas 128 B aligned (the 32 B records stay in one sector)
   return L;
 }
 
