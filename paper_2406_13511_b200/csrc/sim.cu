@@ -520,7 +520,12 @@ struct __align__(32) TickRec {
   int32_t s, pad;
   double a;   // arrival
 };
-static_assert(sizeof(PoolRec) == 32 && sizeof(TickRec) == 32, "sim.cuh SCLS record sizes");
+struct __align__(32) BatchRec {
+  int4 d;      // tick-log start, members, l_in, served l_out
+  double est;  // estimated serve time
+  int32_t next, pad;  // next batch in its worker's queue
+};
+static_assert(sizeof(PoolRec) == 32 && sizeof(TickRec) == 32 && sizeof(BatchRec) == 32, "sim.cuh SCLS record sizes");
 
 template <int POL, bool kHash, bool kLog, int V>
 __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, int32_t* ssplit, double* sT) {
@@ -607,10 +612,9 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   int32_t* split_g = (int32_t*)(base + Lay.split);
   int32_t* segs = (int32_t*)(base + Lay.segs);
   TickRec* tlog = (TickRec*)(base + Lay.tlog);  // the tick log
-  // batch descriptors {tick-log start, members, l_in, served l_out}: one 16 B load per use
-  int4* bd = (int4*)(base + Lay.b_start);
-  int32_t* b_next = (int32_t*)(base + Lay.b_next);
-  double* b_est = (double*)(base + Lay.b_est);
+  // batches: {tick-log start, members, l_in, served l_out}, estimate, next in
+  // the worker queue -- one 32 B record
+  BatchRec* brec = (BatchRec*)(base + Lay.b_start);
   const int cap_w = W > 0 ? (n + W - 1) / W : 0;
   int32_t* fifo_base = (int32_t*)(base + Lay.fifo);
   double* pf_t = (double*)(base + Lay.pf_t);
@@ -665,13 +669,13 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
   auto start_next_scls = [&](int w) {
     const int b = shfl_i(WK(w).busy, WL(w)) ? -1 : shfl_i(WK(w).q_head, WL(w));
     if (b < 0) return;
-    const int nb_next = b_next[b];
+    const int nb_next = brec[b].next;
     if (MINE(w)) {
       WorkerState& k = WK(w);
       k.q_head = nb_next;
       if (k.q_head < 0) k.q_tail = -1;
     }
-    const int4 d = bd[b];
+    const int4 d = brec[b].d;
     const int bn = d.y, blin = d.z, bsv = d.w;
     sink.record(lane, 3, clock, -1, w, b, bn, blin, 0, 0, 0.0, 0, 0, 0.0, 0, 0.0, 0);
     const double serve = batch_serve_time(lat, bn, blin, bsv);
@@ -1048,7 +1052,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           const int beg = b == 0 ? 0 : segs[nb - b];
           const int bi = (int)next_batch + b;
           const int L = sv[end - 1];
-          b_est[bi] = cost[coff[L] - 1 + (end - beg)];
+          brec[bi].est = cost[coff[L] - 1 + (end - beg)];
           // slice_served_l_out (sched_policies.cpp:72-80): max over members
           int served = 0;
 #pragma unroll kEmitU
@@ -1056,7 +1060,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
             const int4 v = tlog[q].igte;
             served = max(served, min(v.z - v.y, C.S));
           }
-          bd[bi] = make_int4(tl_pos + beg, end - beg, L, served);
+          brec[bi].d = make_int4(tl_pos + beg, end - beg, L, served);
         }
       }
       tl_pos += P_;
@@ -1071,7 +1075,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     int32_t* order = segs;  // reuse
     if (nb > 0) {
       if (nb <= 32) {
-        const double e = lane < nb ? b_est[first + lane] : -dinf();
+        const double e = lane < nb ? brec[first + lane].est : -dinf();
         int rank = 0;
         for (int q = 0; q < nb; ++q) {
           const double eq = shfl_d(e, q);
@@ -1080,7 +1084,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         if (lane < nb) order[rank] = lane;
       } else {
         for (int i = lane; i < nb; i += 32) {
-          sk[i] = ~ordered_bits(b_est[first + i]);
+          sk[i] = ~ordered_bits(brec[first + i].est);
           sv[i] = i;
         }
         __syncwarp();
@@ -1092,16 +1096,16 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
     }
     for (int k = 0; k < nb; ++k) {
       const int b = first + order[k];
-      const double e = b_est[b];
+      const double e = brec[b].est;
       const int w = argmin_worker_load<V>(ws, W, lane);  // min (load, worker id)
       if (MINE(w)) WK(w).load = __dadd_rn(WK(w).load, e);
       // dispatch record (served l_out computed at emit), enqueue
-      const int4 d = bd[b];
+      const int4 d = brec[b].d;
       const int bn = d.y;
       sink.record(lane, 2, clock, -1, w, b, bn, d.z, C.S, 0, e, 0, 0, 0.0, 0, 0.0, 0);
-      if (lane == 0) b_next[b] = -1;
+      if (lane == 0) brec[b].next = -1;
       const int tail = shfl_i(WK(w).q_tail, WL(w));
-      if (lane == 0 && tail >= 0) b_next[tail] = b;
+      if (lane == 0 && tail >= 0) brec[tail].next = b;
       if (MINE(w)) {
         WorkerState& k = WK(w);
         if (k.q_tail < 0) k.q_head = b;
@@ -1123,9 +1127,9 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
 
   // SCLS on_batch_done (sched_policies.cpp:149-188) for worker w, batch b.
   auto scls_done = [&](int w, int b) {
-    const int4 d = bd[b];
+    const int4 d = brec[b].d;
     const int bn = d.y, bst = d.x, lin = d.z, served = d.w;
-    const double best = b_est[b];
+    const double best = brec[b].est;
     sink.record(lane, 4, clock, -1, w, b, bn, lin, C.S, served, 0.0, 0, 0, 0.0, 0, 0.0, bn);
     ++batch_count;
     batch_members += bn;

@@ -69,10 +69,9 @@ __host__ __device__ inline SimLayout sim_layout(int64_t n, int32_t W, int32_t po
     o = (o + 31) & ~(int64_t)31;
     L.tlog = take(32 * (cap + 1));
     L.tl_g = L.tl_t = L.tl_e = L.tl_s = L.tl_a = 0;
-    L.b_start = take(16 * (cap + 1));  // int4 {start, n, l_in, served} per batch
-    L.b_n = L.b_lin = L.b_served = 0;
-    L.b_next = take(4 * (cap + 1));
-    L.b_est = take(8 * (cap + 1));
+    o = (o + 31) & ~(int64_t)31;
+    L.b_start = take(32 * (cap + 1));  // {start, n, l_in, served; est; next} per batch
+    L.b_n = L.b_lin = L.b_served = L.b_next = L.b_est = 0;
   } else if (policy == SCLS_POLICY_SLS) {
     L.fifo = take(4 * (W * cap_w + 1));
     L.pf_t = take(8 * n1);
