@@ -35,7 +35,10 @@ namespace scls {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kSimWarps = 4;  // traces per CTA
+#ifndef SCLS_SIM_WARPS
+#define SCLS_SIM_WARPS 4
+#endif
+constexpr int kSimWarps = SCLS_SIM_WARPS;  // traces per CTA
 #ifndef SCLS_SPLIT_SMEM
 #define SCLS_SPLIT_SMEM 256
 #endif
