@@ -161,7 +161,7 @@ __device__ __forceinline__ uint64_t eb_bias64(int64_t x) { return (uint64_t)x ^ 
 // histogram per block of kEbChunk elements, then one global add per bin per
 // block; larger ranges: warp-aggregated global adds.
 constexpr int kEbSmemBins = 8192;
-constexpr int kEbChunk = 16384;
+constexpr int kEbChunk = 4096;  // 256 blocks for a 1M pool
 __global__ void __launch_bounds__(512) ebucket_hist_kernel(int64_t n, const int32_t* __restrict__ eff, int32_t emin,
                                                            int32_t nbins, int32_t* __restrict__ counts) {
   __shared__ int32_t h[kEbSmemBins];
@@ -268,18 +268,43 @@ __global__ void __launch_bounds__(512) ebucket_scatter_kernel(int64_t n, const i
   }
 }
 
-// One CTA per bucket (grid-stride): gather (ordered_bits(arrival),
-// bias64(id), position), bitonic sort in shared memory, write the positions.
-constexpr int kEbThreads = 512;
+// One CTA per bucket (grid-stride).  Fast path: every member gets a 32-bit
+// image of its arrival, (ordered_bits(arrival) - bucket min) >> shift with
+// the shift that fits the bucket's range in 32 bits -- monotone in the
+// arrival, so sorting (image, slot) with a register / shuffle bitonic network
+// (two members per thread; only the stages with partners 64+ members apart go
+// through shared memory) orders the bucket up to runs of equal images, which
+// are then put in (arrival, id, position) order by an insertion sort of the
+// full keys.  A run longer than kEbTieRun (e.g. a bucket of equal arrivals)
+// sends the bucket to the full-key bitonic sort in shared memory.
+constexpr int kEbThreads = 1024;  // two members per thread: kBucketCap = 2048
+constexpr int kEbTieRun = 32;
+static_assert(2 * kEbThreads == kBucketCap, "two members per thread");
+
+__device__ __forceinline__ bool eb_less_full(int xa, int xb, const double* arr, const int64_t* id) {
+  const uint64_t a0 = ordered_bits(arr[xa]), a1 = ordered_bits(arr[xb]);
+  if (a0 != a1) return a0 < a1;
+  const int64_t i0 = id[xa], i1 = id[xb];
+  if (i0 != i1) return i0 < i1;
+  return xa < xb;
+}
+
+// One compare-exchange of the bitonic network, seen from member i.
+__device__ __forceinline__ uint64_t eb_cx(uint64_t mine, uint64_t other, int i, int j, int k) {
+  return (((i & j) == 0) == ((i & k) == 0)) ? min(mine, other) : max(mine, other);
+}
+
 __global__ void __launch_bounds__(kEbThreads) ebucket_sort_kernel(int32_t nbins, const int32_t* __restrict__ counts,
                                                                   const int32_t* __restrict__ offs,
                                                                   const int32_t* __restrict__ idx,
                                                                   const double* __restrict__ arr,
                                                                   const int64_t* __restrict__ id,
                                                                   int32_t* __restrict__ perm) {
-  __shared__ uint64_t ka[kBucketCap], ki[kBucketCap];
-  __shared__ uint32_t kx[kBucketCap];
-  const int tid = threadIdx.x;
+  __shared__ uint64_t ka[kBucketCap], ki[kBucketCap];  // fast path: the two stage buffers
+  __shared__ uint32_t kx[kBucketCap];                  // fast path: slot -> position
+  __shared__ uint64_t red[2][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int e0 = 2 * tid, e1 = e0 + 1;
   for (int b = blockIdx.x; b < nbins; b += gridDim.x) {
     const int c = counts[b];
     if (c == 0 || c > kBucketCap) continue;
@@ -288,8 +313,126 @@ __global__ void __launch_bounds__(kEbThreads) ebucket_sort_kernel(int32_t nbins,
       if (tid == 0) perm[o] = idx[o];
       continue;
     }
-    int P = 2;
+    int P = 64;
     while (P < c) P <<= 1;
+    // ---- images
+    uint64_t o0 = 0, o1 = 0;
+    if (e0 < c) {
+      const int x = idx[o + e0];
+      kx[e0] = (uint32_t)x;
+      o0 = ordered_bits(arr[x]);
+    }
+    if (e1 < c) {
+      const int x = idx[o + e1];
+      kx[e1] = (uint32_t)x;
+      o1 = ordered_bits(arr[x]);
+    }
+    uint64_t mn = min(e0 < c ? o0 : ~0ull, e1 < c ? o1 : ~0ull);
+    uint64_t mx = max(e0 < c ? o0 : 0ull, e1 < c ? o1 : 0ull);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      mn = min(mn, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)mn, d));
+      mx = max(mx, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)mx, d));
+    }
+    if (lane == 0) {
+      red[0][warp] = mn;
+      red[1][warp] = mx;
+    }
+    __syncthreads();
+    mn = red[0][0];
+    mx = red[1][0];
+    for (int w = 1; w < kEbThreads / 32; ++w) {
+      mn = min(mn, red[0][w]);
+      mx = max(mx, red[1][w]);
+    }
+    const uint64_t span = mx - mn;
+    const int sh = span ? max(0, 32 - __clzll((long long)span)) : 0;
+    uint64_t k0 = e0 < c ? ((o0 - mn) >> sh) << 32 | (uint64_t)e0 : ~0ull;
+    uint64_t k1 = e1 < c ? ((o1 - mn) >> sh) << 32 | (uint64_t)e1 : ~0ull;
+    // ---- bitonic network on (image, slot): all keys distinct
+    const bool act = e0 < P;  // warp-uniform (P >= 64)
+    int buf = 0;
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j >= 64) {
+          uint64_t* sb = buf ? ki : ka;
+          buf ^= 1;
+          if (act) {
+            sb[e0] = k0;
+            sb[e1] = k1;
+          }
+          __syncthreads();
+          if (act) {
+            const uint64_t p0 = sb[e0 ^ j], p1 = sb[e1 ^ j];
+            k0 = eb_cx(k0, p0, e0, j, k);
+            k1 = eb_cx(k1, p1, e1, j, k);
+          }
+        } else if (j >= 2) {
+          if (act) {
+            const uint64_t p0 = __shfl_xor_sync(0xffffffffu, (unsigned long long)k0, j >> 1);
+            const uint64_t p1 = __shfl_xor_sync(0xffffffffu, (unsigned long long)k1, j >> 1);
+            k0 = eb_cx(k0, p0, e0, j, k);
+            k1 = eb_cx(k1, p1, e1, j, k);
+          }
+        } else if (act) {
+          const uint64_t lo = min(k0, k1), hi = max(k0, k1);
+          const bool asc = (e0 & k) == 0;
+          k0 = asc ? lo : hi;
+          k1 = asc ? hi : lo;
+        }
+      }
+    }
+    // ---- runs of equal images
+    uint64_t* sk = buf ? ki : ka;  // not the buffer the last shared stage read
+    if (act) {
+      sk[e0] = k0;
+      sk[e1] = k1;
+    }
+    __syncthreads();
+    const bool t0 = e1 < c && (k0 >> 32) == (k1 >> 32);
+    const bool t1 = e1 + 1 < c && (k1 >> 32) == (sk[e1 + 1] >> 32);
+    bool slow = false;
+    if (__syncthreads_or(t0 || t1)) {
+      // a run starts at s when image(s) == image(s + 1) != image(s - 1)
+      int run_len = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s = e0 + h;
+        if (s + 1 < c && (sk[s] >> 32) == (sk[s + 1] >> 32) && (s == 0 || (sk[s - 1] >> 32) != (sk[s] >> 32))) {
+          int e = s + 2;
+          while (e < c && (sk[e] >> 32) == (sk[s] >> 32) && e - s <= kEbTieRun) ++e;
+          run_len = max(run_len, e - s);
+        }
+      }
+      slow = __syncthreads_or(run_len > kEbTieRun);
+      if (!slow) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int s = e0 + h;
+          if (s + 1 < c && (sk[s] >> 32) == (sk[s + 1] >> 32) && (s == 0 || (sk[s - 1] >> 32) != (sk[s] >> 32))) {
+            int e = s + 1;
+            while (e < c && (sk[e] >> 32) == (sk[s] >> 32)) ++e;
+            for (int i = s + 1; i < e; ++i) {  // insertion sort of [s, e) by the full key
+              const uint64_t v = sk[i];
+              const int xv = (int)kx[(uint32_t)v];
+              int q = i;
+              while (q > s && eb_less_full(xv, (int)kx[(uint32_t)sk[q - 1]], arr, id)) {
+                sk[q] = sk[q - 1];
+                --q;
+              }
+              sk[q] = v;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (!slow) {
+      for (int q = tid; q < c; q += kEbThreads) perm[o + q] = (int32_t)kx[(uint32_t)sk[q]];
+      __syncthreads();
+      continue;
+    }
+    // ---- long runs of equal images: bitonic sort on the full keys
     for (int q = tid; q < P; q += kEbThreads) {
       if (q < c) {
         const int x = idx[o + q];

@@ -150,6 +150,9 @@ def test_offload_random_vs_oracle(ctx, orc):
         loads = rng.random(nw) * 10
         if trial % 4 == 0:
             loads = np.round(loads)  # load ties
+        if trial % 5 == 1:
+            loads = np.round(loads) - 5.0  # negative loads, -0.0 beside +0.0
+            loads[::2] = np.where(loads[::2] == 0.0, -0.0, loads[::2])
         est = 0.01 + rng.random(nb) * 5
         if trial % 3 == 0:
             est = np.round(est, 1)  # estimate ties
@@ -352,7 +355,8 @@ def test_bucket_sort_matches_lsd_sort(ctx, orc):
     sort (SCLS_OPT_BATCH_PATH 2) give the same batches as the oracle:
     uniform and skewed eff, a bucket above the shared-memory cap (the
     overflow fallback), eff ranges beyond 2^16 (LSD directly), equal and
-    +-0.0 arrivals, duplicate and negative ids."""
+    +-0.0 arrivals, duplicate and negative ids, buckets whose arrival images
+    tie in runs short enough for the in-place fix-up and too long for it."""
     lat = capi.builtin_latency_model()
     rng = np.random.default_rng(17)
     cases = []
@@ -366,6 +370,10 @@ def test_bucket_sort_matches_lsd_sort(ctx, orc):
     a[::7] = 0.0
     a[1::7] = -0.0
     cases.append((rng.integers(1, 300, n), a, rng.integers(-50, 50, n)))                      # ties, dup ids
+    cases.append((rng.integers(1, 100, n), np.full(n, 5.0), rng.permutation(n)))              # one arrival: long runs
+    a = np.floor(rng.random(n) * 24) * 0.5
+    a[: n // 2] = rng.random(n // 2) * 1e-300                                                  # subnormal spread
+    cases.append((rng.integers(1, 60, n), a, rng.permutation(n)))                              # runs of ~35 and short
     for i, (eff, arr, ids) in enumerate(cases):
         eff = eff.astype(np.int32)
         arr = np.asarray(arr, np.float64)
