@@ -262,9 +262,9 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
   key_stats_kernel<<<std::min(grid_n, ctx->sm_count * 8), threads, 0, s>>>(n, in.eff, in.id,
                                                                            in.arrival, st);
   SCLS_LAUNCHED();
-  SCLS_CUDA(cudaMemcpyAsync(hst, st, sizeof(KeyStats), cudaMemcpyDeviceToHost, s));
-  SCLS_CUDA(cudaStreamSynchronize(s));
-  const KeyStats ks = *hst;
+  // The key ranges reach the host only when the LSD sort needs them (forced,
+  // or after an eff-bucket overflow): the bucket sort plans on the device.
+  KeyStats ks{};
 
   // ---- 2. sort by (eff, arrival, id): eff buckets sorted in shared memory,
   //         or the stable LSD radix sort field by field
@@ -317,17 +317,18 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
     }
     return SCLS_OK;
   };
-  const uint64_t erange = ks.eff_max - ks.eff_min;
-  // buckets that fit the shared-memory sort on average (a skewed pool still
-  // falls back after the fact, below)
-  const bool bucketed = !ctx->force_lsd_sort && erange < (uint64_t)kBucketMaxBins &&
-                        n <= (int64_t)(erange + 1) * (kBucketCap * 3 / 4);
+  // eff buckets unless forced off; a pool they do not fit (eff range, average
+  // or largest bucket) sets bucket_overflow on the device and is re-sorted by
+  // the LSD path after the rows pass's read-back, below
+  const bool bucketed = !ctx->force_lsd_sort;
   if (bucketed) {
-    const int32_t emin = (int32_t)((uint32_t)ks.eff_min ^ 0x80000000u);
-    scls_status stt0 = bucket_sort_perm(ctx, n, in.eff, in.arrival, in.id, emin, (int32_t)erange + 1, vals,
+    scls_status stt0 = bucket_sort_perm(ctx, n, in.eff, in.arrival, in.id, &st->eff_min, vals,
                                         &st->bucket_overflow);
     if (stt0) return stt0;
   } else {
+    SCLS_CUDA(cudaMemcpyAsync(hst, st, sizeof(KeyStats), cudaMemcpyDeviceToHost, s));
+    SCLS_CUDA(cudaStreamSynchronize(s));
+    ks = *hst;
     scls_status stt0 = lsd_sort();
     if (stt0) return stt0;
   }
@@ -352,7 +353,9 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
   scls_status stt = rows_pass();
   if (stt) return stt;
   if (bucketed && hst->bucket_overflow) {
-    // an eff bucket beyond kBucketCap: redo the order with the LSD sort
+    // no eff buckets for this pool: redo the order with the LSD sort, on the
+    // key ranges of the rows pass's read-back
+    ks = *hst;
     init_stats_kernel<<<1, 1, 0, s>>>(st);
     SCLS_LAUNCHED();
     stt = lsd_sort();

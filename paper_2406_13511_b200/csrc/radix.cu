@@ -157,14 +157,35 @@ __global__ void total_kernel(const int32_t* __restrict__ in, const int32_t* __re
 
 __device__ __forceinline__ uint64_t eb_bias64(int64_t x) { return (uint64_t)x ^ 0x8000000000000000ull; }
 
+// The bucket plan from the device key stats (biased-int32 eff min / max):
+// usable when the eff range has at most kBucketMaxBins values and the
+// average bucket fits the shared-memory sort with room to spare.
+struct EbPlan {
+  bool ok;
+  int32_t emin, nbins;
+};
+__device__ __forceinline__ EbPlan eb_plan(int64_t n, const unsigned long long* erng) {
+  const uint64_t lo = erng[0], hi = erng[1];
+  const uint64_t r = hi - lo;
+  EbPlan pl;
+  pl.ok = hi >= lo && r < (uint64_t)kBucketMaxBins && n <= (int64_t)(r + 1) * (kBucketCap * 3 / 4);
+  pl.emin = (int32_t)((uint32_t)lo ^ 0x80000000u);
+  pl.nbins = pl.ok ? (int32_t)r + 1 : 0;
+  return pl;
+}
+
 // Histogram of eff - emin.  Small bin counts (<= kEbSmemBins): a shared
 // histogram per block of kEbChunk elements, then one global add per bin per
 // block; larger ranges: warp-aggregated global adds.
 constexpr int kEbSmemBins = 8192;
 constexpr int kEbChunk = 4096;  // 256 blocks for a 1M pool
-__global__ void __launch_bounds__(512) ebucket_hist_kernel(int64_t n, const int32_t* __restrict__ eff, int32_t emin,
-                                                           int32_t nbins, int32_t* __restrict__ counts) {
+__global__ void __launch_bounds__(512) ebucket_hist_kernel(int64_t n, const int32_t* __restrict__ eff,
+                                                           const unsigned long long* __restrict__ erng,
+                                                           int32_t* __restrict__ counts) {
   __shared__ int32_t h[kEbSmemBins];
+  const EbPlan pl = eb_plan(n, erng);
+  if (!pl.ok) return;
+  const int32_t emin = pl.emin, nbins = pl.nbins;
   const int64_t lo = (int64_t)blockIdx.x * kEbChunk, hi = min(n, lo + kEbChunk);
   if (nbins <= kEbSmemBins) {
     for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
@@ -186,11 +207,18 @@ __global__ void __launch_bounds__(512) ebucket_hist_kernel(int64_t n, const int3
 
 // One CTA: exclusive offsets of <= kBucketMaxBins counts, a cursor copy, and
 // the overflow flag for buckets beyond kBucketCap.
-__global__ void __launch_bounds__(1024) ebucket_scan_kernel(int32_t nbins, const int32_t* __restrict__ counts,
+__global__ void __launch_bounds__(1024) ebucket_scan_kernel(int64_t n, const unsigned long long* __restrict__ erng,
+                                                            const int32_t* __restrict__ counts,
                                                             int32_t* __restrict__ offs,
                                                             int32_t* __restrict__ cursor,
                                                             int32_t* __restrict__ overflow) {
   __shared__ int32_t ws[32];
+  const EbPlan pl = eb_plan(n, erng);
+  if (!pl.ok) {
+    if (threadIdx.x == 0) *overflow = 1;
+    return;
+  }
+  const int32_t nbins = pl.nbins;
   const int per = (nbins + 1023) / 1024;
   const int b0 = threadIdx.x * per;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -238,10 +266,14 @@ __global__ void __launch_bounds__(1024) ebucket_scan_kernel(int32_t nbins, const
 // reserves each bin's range for its kEbChunk elements with one global add,
 // then ranks locally in shared memory (the order inside a bucket does not
 // matter: the bucket sort's last key is the position).
-__global__ void __launch_bounds__(512) ebucket_scatter_kernel(int64_t n, const int32_t* __restrict__ eff, int32_t emin,
-                                                              int32_t nbins, int32_t* __restrict__ cursor,
+__global__ void __launch_bounds__(512) ebucket_scatter_kernel(int64_t n, const int32_t* __restrict__ eff,
+                                                              const unsigned long long* __restrict__ erng,
+                                                              int32_t* __restrict__ cursor,
                                                               int32_t* __restrict__ idx) {
   __shared__ int32_t h[kEbSmemBins];
+  const EbPlan pl = eb_plan(n, erng);
+  if (!pl.ok) return;
+  const int32_t emin = pl.emin, nbins = pl.nbins;
   const int64_t lo = (int64_t)blockIdx.x * kEbChunk, hi = min(n, lo + kEbChunk);
   const int lane = threadIdx.x & 31;
   if (nbins <= kEbSmemBins) {
@@ -268,18 +300,21 @@ __global__ void __launch_bounds__(512) ebucket_scatter_kernel(int64_t n, const i
   }
 }
 
-// One CTA per bucket (grid-stride).  Fast path: every member gets a 32-bit
+// One CTA per bucket (grid-stride).  Fast path: every member gets a 21-bit
 // image of its arrival, (ordered_bits(arrival) - bucket min) >> shift with
-// the shift that fits the bucket's range in 32 bits -- monotone in the
-// arrival, so sorting (image, slot) with a register / shuffle bitonic network
-// (two members per thread; only the stages with partners 64+ members apart go
-// through shared memory) orders the bucket up to runs of equal images, which
-// are then put in (arrival, id, position) order by an insertion sort of the
-// full keys.  A run longer than kEbTieRun (e.g. a bucket of equal arrivals)
-// sends the bucket to the full-key bitonic sort in shared memory.
-constexpr int kEbThreads = 1024;  // two members per thread: kBucketCap = 2048
+// the shift that fits the bucket's range in 21 bits -- monotone in the
+// arrival -- and the 32-bit key image << 11 | slot is sorted by a bitonic
+// network held in registers (four members per thread: partners 1-2 apart in
+// the thread, 4-64 apart by warp shuffles, 128+ apart through shared
+// memory).  That orders the bucket up to runs of equal images, which are then
+// put in (arrival, id, position) order by an insertion sort of the full keys.
+// A run longer than kEbTieRun (e.g. a bucket of equal arrivals) sends the
+// bucket to the full-key bitonic sort in shared memory.
+constexpr int kEbThreads = 512;  // four members per thread: kBucketCap = 2048
+constexpr int kEbPer = 4;
+constexpr int kEbImgBits = 21, kEbSlotBits = 11;
 constexpr int kEbTieRun = 32;
-static_assert(2 * kEbThreads == kBucketCap, "two members per thread");
+static_assert(kEbPer * kEbThreads == kBucketCap && (1 << kEbSlotBits) == kBucketCap, "bucket geometry");
 
 __device__ __forceinline__ bool eb_less_full(int xa, int xb, const double* arr, const int64_t* id) {
   const uint64_t a0 = ordered_bits(arr[xa]), a1 = ordered_bits(arr[xb]);
@@ -289,46 +324,61 @@ __device__ __forceinline__ bool eb_less_full(int xa, int xb, const double* arr, 
   return xa < xb;
 }
 
-// One compare-exchange of the bitonic network, seen from member i.
-__device__ __forceinline__ uint64_t eb_cx(uint64_t mine, uint64_t other, int i, int j, int k) {
-  return (((i & j) == 0) == ((i & k) == 0)) ? min(mine, other) : max(mine, other);
+// Compare-exchange seen from one member: keep the min when m == 0, the max
+// when m == ~0 (min of the complements).
+__device__ __forceinline__ uint32_t eb_keep(uint32_t mine, uint32_t other, uint32_t m) {
+  return min(mine ^ m, other ^ m) ^ m;
 }
 
-__global__ void __launch_bounds__(kEbThreads) ebucket_sort_kernel(int32_t nbins, const int32_t* __restrict__ counts,
+__global__ void __launch_bounds__(kEbThreads) ebucket_sort_kernel(int64_t n, const unsigned long long* __restrict__ erng,
+                                                                  const int32_t* __restrict__ counts,
                                                                   const int32_t* __restrict__ offs,
                                                                   const int32_t* __restrict__ idx,
                                                                   const double* __restrict__ arr,
                                                                   const int64_t* __restrict__ id,
                                                                   int32_t* __restrict__ perm) {
-  __shared__ uint64_t ka[kBucketCap], ki[kBucketCap];  // fast path: the two stage buffers
+  __shared__ uint64_t ka[kBucketCap], ki[kBucketCap];  // fast path: two 32-bit stage buffers in ka
   __shared__ uint32_t kx[kBucketCap];                  // fast path: slot -> position
-  __shared__ uint64_t red[2][32];
+  __shared__ uint64_t red[2][kEbThreads / 32];
+  uint32_t* const sbuf0 = (uint32_t*)ka;
+  uint32_t* const sbuf1 = sbuf0 + kBucketCap;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int e0 = 2 * tid, e1 = e0 + 1;
+  const int e0 = kEbPer * tid;
+  const EbPlan pl = eb_plan(n, erng);
+  if (!pl.ok) {  // no buckets: a valid (identity) permutation for the caller's rows pass, then the LSD sort
+    for (int64_t i = (int64_t)blockIdx.x * kEbThreads + tid; i < n; i += (int64_t)gridDim.x * kEbThreads)
+      perm[i] = (int32_t)i;
+    return;
+  }
+  const int32_t nbins = pl.nbins;
   for (int b = blockIdx.x; b < nbins; b += gridDim.x) {
     const int c = counts[b];
-    if (c == 0 || c > kBucketCap) continue;
+    if (c == 0) continue;
     const int o = offs[b];
+    if (c > kBucketCap) {  // overflow (the caller re-sorts): positions only, so the rows pass reads valid rows
+      for (int q = tid; q < c; q += kEbThreads) perm[o + q] = idx[o + q];
+      continue;
+    }
     if (c == 1) {
       if (tid == 0) perm[o] = idx[o];
       continue;
     }
-    int P = 64;
+    int P = 128;
     while (P < c) P <<= 1;
     // ---- images
-    uint64_t o0 = 0, o1 = 0;
-    if (e0 < c) {
-      const int x = idx[o + e0];
-      kx[e0] = (uint32_t)x;
-      o0 = ordered_bits(arr[x]);
+    uint64_t ob[kEbPer];
+    uint64_t mn = ~0ull, mx = 0ull;
+#pragma unroll
+    for (int h = 0; h < kEbPer; ++h) {
+      ob[h] = 0;
+      if (e0 + h < c) {
+        const int x = idx[o + e0 + h];
+        kx[e0 + h] = (uint32_t)x;
+        ob[h] = ordered_bits(arr[x]);
+        mn = min(mn, ob[h]);
+        mx = max(mx, ob[h]);
+      }
     }
-    if (e1 < c) {
-      const int x = idx[o + e1];
-      kx[e1] = (uint32_t)x;
-      o1 = ordered_bits(arr[x]);
-    }
-    uint64_t mn = min(e0 < c ? o0 : ~0ull, e1 < c ? o1 : ~0ull);
-    uint64_t mx = max(e0 < c ? o0 : 0ull, e1 < c ? o1 : 0ull);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
       mn = min(mn, (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)mn, d));
@@ -341,82 +391,97 @@ __global__ void __launch_bounds__(kEbThreads) ebucket_sort_kernel(int32_t nbins,
     __syncthreads();
     mn = red[0][0];
     mx = red[1][0];
+#pragma unroll
     for (int w = 1; w < kEbThreads / 32; ++w) {
       mn = min(mn, red[0][w]);
       mx = max(mx, red[1][w]);
     }
     const uint64_t span = mx - mn;
-    const int sh = span ? max(0, 32 - __clzll((long long)span)) : 0;
-    uint64_t k0 = e0 < c ? ((o0 - mn) >> sh) << 32 | (uint64_t)e0 : ~0ull;
-    uint64_t k1 = e1 < c ? ((o1 - mn) >> sh) << 32 | (uint64_t)e1 : ~0ull;
-    // ---- bitonic network on (image, slot): all keys distinct
-    const bool act = e0 < P;  // warp-uniform (P >= 64)
+    const int sh = span ? max(0, 64 - kEbImgBits - __clzll((long long)span)) : 0;
+    uint32_t k[kEbPer];
+#pragma unroll
+    for (int h = 0; h < kEbPer; ++h)
+      k[h] = e0 + h < c ? (uint32_t)((ob[h] - mn) >> sh) << kEbSlotBits | (uint32_t)(e0 + h) : ~0u;
+    // ---- bitonic network on the 32-bit keys (all distinct)
+    const bool act = e0 < P;  // warp-uniform (P >= 128)
     int buf = 0;
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        if (j >= 64) {
-          uint64_t* sb = buf ? ki : ka;
-          buf ^= 1;
-          if (act) {
-            sb[e0] = k0;
-            sb[e1] = k1;
-          }
-          __syncthreads();
-          if (act) {
-            const uint64_t p0 = sb[e0 ^ j], p1 = sb[e1 ^ j];
-            k0 = eb_cx(k0, p0, e0, j, k);
-            k1 = eb_cx(k1, p1, e1, j, k);
-          }
-        } else if (j >= 2) {
-          if (act) {
-            const uint64_t p0 = __shfl_xor_sync(0xffffffffu, (unsigned long long)k0, j >> 1);
-            const uint64_t p1 = __shfl_xor_sync(0xffffffffu, (unsigned long long)k1, j >> 1);
-            k0 = eb_cx(k0, p0, e0, j, k);
-            k1 = eb_cx(k1, p1, e1, j, k);
+    for (int kk = 2; kk <= P; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        if (j >= 4) {
+          // the four members share (i & j) and (i & kk): one direction per thread
+          const uint32_t m = ((e0 & j) == 0) == ((e0 & kk) == 0) ? 0u : ~0u;
+          if (j >= 128) {
+            uint32_t* sb = buf ? sbuf1 : sbuf0;
+            buf ^= 1;
+            if (act) *(uint4*)(sb + e0) = make_uint4(k[0], k[1], k[2], k[3]);
+            __syncthreads();
+            if (act) {
+              const uint4 p = *(const uint4*)(sb + (e0 ^ j));
+              k[0] = eb_keep(k[0], p.x, m);
+              k[1] = eb_keep(k[1], p.y, m);
+              k[2] = eb_keep(k[2], p.z, m);
+              k[3] = eb_keep(k[3], p.w, m);
+            }
+          } else if (act) {
+#pragma unroll
+            for (int h = 0; h < kEbPer; ++h) k[h] = eb_keep(k[h], __shfl_xor_sync(0xffffffffu, k[h], j >> 2), m);
           }
         } else if (act) {
-          const uint64_t lo = min(k0, k1), hi = max(k0, k1);
-          const bool asc = (e0 & k) == 0;
-          k0 = asc ? lo : hi;
-          k1 = asc ? hi : lo;
+          // partners inside the thread: (0, 2), (1, 3) for j = 2; (0, 1), (2, 3) for j = 1
+          auto cx = [&](uint32_t& a, uint32_t& z, int i) {
+            const bool asc = (i & kk) == 0;
+            const uint32_t lo = min(a, z), hi = max(a, z);
+            a = asc ? lo : hi;
+            z = asc ? hi : lo;
+          };
+          if (j == 2) {
+            cx(k[0], k[2], e0);
+            cx(k[1], k[3], e0 + 1);
+          } else {
+            cx(k[0], k[1], e0);
+            cx(k[2], k[3], e0 + 2);
+          }
         }
       }
     }
     // ---- runs of equal images
-    uint64_t* sk = buf ? ki : ka;  // not the buffer the last shared stage read
-    if (act) {
-      sk[e0] = k0;
-      sk[e1] = k1;
-    }
+    uint32_t* sk = buf ? sbuf1 : sbuf0;  // not the buffer the last shared stage read
+    if (act) *(uint4*)(sk + e0) = make_uint4(k[0], k[1], k[2], k[3]);
     __syncthreads();
-    const bool t0 = e1 < c && (k0 >> 32) == (k1 >> 32);
-    const bool t1 = e1 + 1 < c && (k1 >> 32) == (sk[e1 + 1] >> 32);
+    bool tie = false;
+#pragma unroll
+    for (int h = 0; h < kEbPer; ++h) {
+      const int i = e0 + h;
+      tie |= i + 1 < c && (sk[i] >> kEbSlotBits) == (sk[i + 1] >> kEbSlotBits);
+    }
     bool slow = false;
-    if (__syncthreads_or(t0 || t1)) {
+    if (__syncthreads_or(tie)) {
       // a run starts at s when image(s) == image(s + 1) != image(s - 1)
       int run_len = 0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < kEbPer; ++h) {
         const int s = e0 + h;
-        if (s + 1 < c && (sk[s] >> 32) == (sk[s + 1] >> 32) && (s == 0 || (sk[s - 1] >> 32) != (sk[s] >> 32))) {
+        const uint32_t is = sk[s] >> kEbSlotBits;
+        if (s + 1 < c && is == (sk[s + 1] >> kEbSlotBits) && (s == 0 || (sk[s - 1] >> kEbSlotBits) != is)) {
           int e = s + 2;
-          while (e < c && (sk[e] >> 32) == (sk[s] >> 32) && e - s <= kEbTieRun) ++e;
+          while (e < c && (sk[e] >> kEbSlotBits) == is && e - s <= kEbTieRun) ++e;
           run_len = max(run_len, e - s);
         }
       }
       slow = __syncthreads_or(run_len > kEbTieRun);
       if (!slow) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kEbPer; ++h) {
           const int s = e0 + h;
-          if (s + 1 < c && (sk[s] >> 32) == (sk[s + 1] >> 32) && (s == 0 || (sk[s - 1] >> 32) != (sk[s] >> 32))) {
+          const uint32_t is = sk[s] >> kEbSlotBits;
+          if (s + 1 < c && is == (sk[s + 1] >> kEbSlotBits) && (s == 0 || (sk[s - 1] >> kEbSlotBits) != is)) {
             int e = s + 1;
-            while (e < c && (sk[e] >> 32) == (sk[s] >> 32)) ++e;
+            while (e < c && (sk[e] >> kEbSlotBits) == is) ++e;
             for (int i = s + 1; i < e; ++i) {  // insertion sort of [s, e) by the full key
-              const uint64_t v = sk[i];
-              const int xv = (int)kx[(uint32_t)v];
+              const uint32_t v = sk[i];
+              const int xv = (int)kx[v & (kBucketCap - 1)];
               int q = i;
-              while (q > s && eb_less_full(xv, (int)kx[(uint32_t)sk[q - 1]], arr, id)) {
+              while (q > s && eb_less_full(xv, (int)kx[sk[q - 1] & (kBucketCap - 1)], arr, id)) {
                 sk[q] = sk[q - 1];
                 --q;
               }
@@ -428,7 +493,7 @@ __global__ void __launch_bounds__(kEbThreads) ebucket_sort_kernel(int32_t nbins,
       }
     }
     if (!slow) {
-      for (int q = tid; q < c; q += kEbThreads) perm[o + q] = (int32_t)kx[(uint32_t)sk[q]];
+      for (int q = tid; q < c; q += kEbThreads) perm[o + q] = (int32_t)kx[sk[q] & (kBucketCap - 1)];
       __syncthreads();
       continue;
     }
@@ -531,25 +596,24 @@ scls_status radix_sort_pairs(scls_ctx* ctx, int64_t n, uint64_t* keys, int32_t* 
 }
 
 scls_status bucket_sort_perm(scls_ctx* ctx, int64_t n, const int32_t* eff, const double* arr,
-                             const int64_t* id, int32_t eff_min, int32_t nbins, int32_t* perm,
+                             const int64_t* id, const unsigned long long* d_eff_range, int32_t* perm,
                              int32_t* d_overflow) {
-  if (nbins < 1 || nbins > kBucketMaxBins) return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "eff range");
   cudaStream_t s = ctx->stream;
-  int32_t* counts = (int32_t*)ctx->buf(kSlotBucket + 0, sizeof(int32_t) * nbins);
-  int32_t* offs = (int32_t*)ctx->buf(kSlotBucket + 1, sizeof(int32_t) * nbins);
-  int32_t* cursor = (int32_t*)ctx->buf(kSlotBucket + 2, sizeof(int32_t) * nbins);
+  int32_t* counts = (int32_t*)ctx->buf(kSlotBucket + 0, sizeof(int32_t) * kBucketMaxBins);
+  int32_t* offs = (int32_t*)ctx->buf(kSlotBucket + 1, sizeof(int32_t) * kBucketMaxBins);
+  int32_t* cursor = (int32_t*)ctx->buf(kSlotBucket + 2, sizeof(int32_t) * kBucketMaxBins);
   int32_t* idx = (int32_t*)ctx->buf(kSlotBucket + 3, sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1));
   if (!counts || !offs || !cursor || !idx) return set_error(ctx, SCLS_ERR_CUDA, "scratch allocation failed");
-  SCLS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * nbins, s));
+  SCLS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * kBucketMaxBins, s));
   const int grid = (int)div_up(n, kEbChunk);
-  ebucket_hist_kernel<<<grid, 512, 0, s>>>(n, eff, eff_min, nbins, counts);
+  ebucket_hist_kernel<<<grid, 512, 0, s>>>(n, eff, d_eff_range, counts);
   SCLS_LAUNCHED();
-  ebucket_scan_kernel<<<1, 1024, 0, s>>>(nbins, counts, offs, cursor, d_overflow);
+  ebucket_scan_kernel<<<1, 1024, 0, s>>>(n, d_eff_range, counts, offs, cursor, d_overflow);
   SCLS_LAUNCHED();
-  ebucket_scatter_kernel<<<grid, 512, 0, s>>>(n, eff, eff_min, nbins, cursor, idx);
+  ebucket_scatter_kernel<<<grid, 512, 0, s>>>(n, eff, d_eff_range, cursor, idx);
   SCLS_LAUNCHED();
-  ebucket_sort_kernel<<<std::min(nbins, ctx->sm_count * 8), kEbThreads, 0, s>>>(nbins, counts, offs, idx, arr, id,
-                                                                                perm);
+  // four 512-thread CTAs per SM; buckets grid-strided
+  ebucket_sort_kernel<<<ctx->sm_count * 4, kEbThreads, 0, s>>>(n, d_eff_range, counts, offs, idx, arr, id, perm);
   SCLS_LAUNCHED();
   return SCLS_OK;
 }

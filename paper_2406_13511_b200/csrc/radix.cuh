@@ -22,13 +22,16 @@ scls_status scan_exclusive(scls_ctx* ctx, int64_t n, const int32_t* in, int32_t*
 // LSD path on (bias32(eff), ordered_bits(arrival), bias64(id)), input position
 // last -- through eff buckets: a counting scatter by eff (one histogram, one
 // scan, one scatter), then one CTA per bucket sorting (arrival, id, position)
-// bitonically in shared memory.  For eff ranges of at most kBucketMaxBins
-// values.  A bucket larger than kBucketCap sets *d_overflow (device int) and
-// leaves its part of perm unwritten; the caller then uses the LSD sort.
+// in registers and shared memory.  The plan comes from the device: the eff
+// range d_eff_range[0..1] (biased int32, the key-stats kernel's min / max),
+// so no host round trip precedes the sort.  When the range has more than
+// kBucketMaxBins values, the average bucket is too large, or one bucket is
+// larger than kBucketCap, *d_overflow (device int) is set and perm holds a
+// valid but unsorted permutation; the caller then uses the LSD sort.
 constexpr int kBucketMaxBins = 1 << 16;
 constexpr int kBucketCap = 2048;
 scls_status bucket_sort_perm(scls_ctx* ctx, int64_t n, const int32_t* eff, const double* arr,
-                             const int64_t* id, int32_t eff_min, int32_t nbins, int32_t* perm,
+                             const int64_t* id, const unsigned long long* d_eff_range, int32_t* perm,
                              int32_t* d_overflow);
 
 // Number of significant bits of v (0 for v == 0).
