@@ -129,8 +129,8 @@ __global__ void rows_kernel(int64_t n, const int32_t* __restrict__ perm,
                             int32_t* __restrict__ flag, KeyStats* st) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int kmax = 0;
+  const int32_t L = p < n ? eff[perm[p]] : 0;
   if (p < n) {
-    const int32_t L = eff[perm[p]];
     Lrow[p] = L;
     // batcher.cpp:40-46: singleton feasibility; first offender in sorted order.
     if (would_oom(mem, 1, L, slice)) {
@@ -144,11 +144,21 @@ __global__ void rows_kernel(int64_t n, const int32_t* __restrict__ perm,
       Krow[p] = (int32_t)(K < row ? K : row);
       kmax = Krow[p];
     }
-    flag[p] = (p == 0 || eff[perm[p - 1]] != L) ? 1 : 0;
   }
+  // the previous row's L from the neighbouring lane (lane 0 gathers it)
+  int32_t Lp = __shfl_up_sync(~0u, L, 1);
+  if ((threadIdx.x & 31) == 0 && p > 0 && p < n) Lp = eff[perm[p - 1]];
+  if (p < n) flag[p] = (p == 0 || Lp != L) ? 1 : 0;
+  // k_max: one atomic per block (per-warp atomics on one address serialise)
+  __shared__ int32_t wmax[32];
 #pragma unroll
   for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(~0u, kmax, o));
-  if ((threadIdx.x & 31) == 0 && kmax) atomicMax(&st->k_max, kmax);
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = kmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) kmax = max(kmax, wmax[w]);
+    if (kmax) atomicMax(&st->k_max, kmax);
+  }
 }
 
 // For each run (maximal block of equal L): first sorted position and the
@@ -386,14 +396,19 @@ scls_status batch_requests_device(scls_ctx* ctx, const BatchInputs& in, const Ba
   SCLS_LAUNCHED();
   stt = scan_exclusive(ctx, n_runs, run_need, run_off, run_off + n_runs);
   if (stt) return stt;
-  int32_t total_cost = 0;
-  SCLS_CUDA(cudaMemcpyAsync(&hst->first_infeasible, run_off + n_runs, sizeof(int32_t),
-                            cudaMemcpyDeviceToHost, s));
-  SCLS_CUDA(cudaStreamSynchronize(s));
-  total_cost = hst->first_infeasible;
-  if (total_cost < 0 || (int64_t)total_cost > (int64_t)1 << 28)
-    return set_error(ctx, SCLS_ERR_CAPACITY, "candidate cost table exceeds 2^28 entries");
-  double* cost = (double*)ctx->buf(kSlotCost, sizeof(double) * (size_t)std::max(total_cost, 1));
+  // Every run needs at most k_max entries: when n_runs * k_max is small the
+  // table is sized by that bound and the exact total stays on the device
+  // (no second host round trip); otherwise it is read back and checked.
+  int64_t total_cost = (int64_t)n_runs * std::max(k_max, 1);
+  if (total_cost > ((int64_t)1 << 24)) {
+    SCLS_CUDA(cudaMemcpyAsync(&hst->first_infeasible, run_off + n_runs, sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, s));
+    SCLS_CUDA(cudaStreamSynchronize(s));
+    total_cost = hst->first_infeasible;
+    if (total_cost < 0 || total_cost > (int64_t)1 << 28)
+      return set_error(ctx, SCLS_ERR_CAPACITY, "candidate cost table exceeds 2^28 entries");
+  }
+  double* cost = (double*)ctx->buf(kSlotCost, sizeof(double) * (size_t)std::max<int64_t>(total_cost, 1));
   if (!cost) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
   cost_table_kernel<<<std::min(n_runs, ctx->sm_count * 16), 128, 0, s>>>(
       n_runs, run_first, run_need, run_off, Lrow, in.slice_len, lat, cost);
