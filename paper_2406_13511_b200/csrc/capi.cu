@@ -51,6 +51,20 @@ void* scls_ctx::host_pinned(size_t bytes) {
   return pinned;
 }
 
+void* scls_ctx::host_stage(size_t bytes) {
+  if (stage_cap >= bytes) return stage;
+  if (stage) {
+    cudaStreamSynchronize(stream);
+    cudaFreeHost(stage);
+  }
+  stage_cap = std::max(bytes, (size_t)65536);
+  if (cudaMallocHost(&stage, stage_cap) != cudaSuccess) {
+    stage = nullptr;
+    stage_cap = 0;
+  }
+  return stage;
+}
+
 namespace scls {
 
 scls_status set_error(scls_ctx* ctx, scls_status st, const std::string& msg) {
@@ -189,6 +203,7 @@ void scls_ctx_destroy(scls_ctx* ctx) {
   for (auto& b : ctx->bufs)
     if (b.p) cudaFree(b.p);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->stage) cudaFreeHost(ctx->stage);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   for (auto& st : ctx->side)
@@ -398,10 +413,24 @@ scls_status scls_max_batch_size(scls_ctx* ctx, int64_t count, const int32_t* l_i
 
 // ---- batcher / offloader / fused tick -----------------------------------------------
 
+// Host-memory calls on pools up to kPackMax requests stage their three input
+// arrays through one pinned buffer (one H2D copy) and read their five result
+// arrays back as one region (one D2H copy, scattered on the host after the
+// sync): at these sizes each pageable copy costs more than the kernels.
+constexpr int64_t kPackMax = 1 << 16;
+struct BatchPack {
+  bool on = false;
+  char* h_out = nullptr;  // pinned: the result region after the D2H copy
+  char* d_out = nullptr;  // device: order | seg_begin | l_in | est | member_id
+  size_t off[5] = {}, bytes = 0;
+};
+
+static size_t pack_align(size_t x) { return (x + 15) & ~(size_t)15; }
+
 static scls_status batch_impl(scls_ctx* ctx, int64_t n, const int32_t* eff_len, const double* arrival,
                               const int64_t* id, int32_t slice_len, const scls_latency* lat,
                               const scls_memory* memm, int64_t first_batch_id, scls_batches* out,
-                              int32_t mem, BatchOutputs* dev_out_keep) {
+                              int32_t mem, BatchOutputs* dev_out_keep, BatchPack* pk) {
   scls_status st;
   if (n < 0 || !lat || !check_memory_arg(ctx, memm) || !out || (n && (!eff_len || !arrival || !id)) ||
       (n && (!out->seg_begin || !out->l_in || !out->est)))
@@ -415,15 +444,44 @@ static scls_status batch_impl(scls_ctx* ctx, int64_t n, const int32_t* eff_len, 
   const int32_t* d_eff;
   const double* d_arr;
   const int64_t* d_id;
-  if ((st = stage_in(ctx, 0, eff_len, n, mem, &d_eff)) || (st = stage_in(ctx, 1, arrival, n, mem, &d_arr)) ||
-      (st = stage_in(ctx, 2, id, n, mem, &d_id)))
-    return st;
   BatchOutputs d{};
-  d.order = stage_out_buf(ctx, 3, out->order, n, mem);
-  d.seg_begin = stage_out_buf(ctx, 4, out->seg_begin, n + 1, mem);
-  d.l_in = stage_out_buf(ctx, 5, out->l_in, n, mem);
-  d.est = stage_out_buf(ctx, 6, out->est, n, mem);
-  d.member_id = stage_out_buf(ctx, 7, out->member_id, n, mem);
+  pk->on = mem == SCLS_MEM_HOST && n <= kPackMax;
+  if (pk->on) {
+    const size_t be = pack_align(4 * (size_t)n), ba = pack_align(8 * (size_t)n), bi = pack_align(8 * (size_t)n);
+    const size_t in_bytes = be + ba + bi;
+    pk->off[0] = 0;                                          // order
+    pk->off[1] = pk->off[0] + pack_align(4 * (size_t)n);     // seg_begin (n + 1)
+    pk->off[2] = pk->off[1] + pack_align(4 * (size_t)(n + 1));  // l_in
+    pk->off[3] = pk->off[2] + pack_align(4 * (size_t)n);     // est
+    pk->off[4] = pk->off[3] + pack_align(8 * (size_t)n);     // member_id
+    pk->bytes = pk->off[4] + pack_align(8 * (size_t)n);
+    char* h = (char*)ctx->host_stage(in_bytes + pk->bytes);
+    char* din = (char*)ctx->buf(kSlotStage + 8, in_bytes);
+    pk->d_out = (char*)ctx->buf(kSlotStage + 9, pk->bytes);
+    if (!h || !din || !pk->d_out) return set_error(ctx, SCLS_ERR_CUDA, "staging allocation failed");
+    std::memcpy(h, eff_len, 4 * (size_t)n);
+    std::memcpy(h + be, arrival, 8 * (size_t)n);
+    std::memcpy(h + be + ba, id, 8 * (size_t)n);
+    SCLS_CUDA(cudaMemcpyAsync(din, h, in_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    pk->h_out = h + in_bytes;
+    d_eff = (const int32_t*)din;
+    d_arr = (const double*)(din + be);
+    d_id = (const int64_t*)(din + be + ba);
+    d.order = out->order ? (int32_t*)(pk->d_out + pk->off[0]) : nullptr;
+    d.seg_begin = (int32_t*)(pk->d_out + pk->off[1]);
+    d.l_in = (int32_t*)(pk->d_out + pk->off[2]);
+    d.est = (double*)(pk->d_out + pk->off[3]);
+    d.member_id = out->member_id ? (int64_t*)(pk->d_out + pk->off[4]) : nullptr;
+  } else {
+    if ((st = stage_in(ctx, 0, eff_len, n, mem, &d_eff)) || (st = stage_in(ctx, 1, arrival, n, mem, &d_arr)) ||
+        (st = stage_in(ctx, 2, id, n, mem, &d_id)))
+      return st;
+    d.order = stage_out_buf(ctx, 3, out->order, n, mem);
+    d.seg_begin = stage_out_buf(ctx, 4, out->seg_begin, n + 1, mem);
+    d.l_in = stage_out_buf(ctx, 5, out->l_in, n, mem);
+    d.est = stage_out_buf(ctx, 6, out->est, n, mem);
+    d.member_id = stage_out_buf(ctx, 7, out->member_id, n, mem);
+  }
   if (!d.seg_begin || !d.l_in || !d.est) return set_error(ctx, SCLS_ERR_CUDA, "allocation failed");
   BatchInputs in{n, d_eff, d_arr, d_id, slice_len, lat, memm};
   int64_t nb = 0;
@@ -434,14 +492,31 @@ static scls_status batch_impl(scls_ctx* ctx, int64_t n, const int32_t* eff_len, 
   return SCLS_OK;
 }
 
-static scls_status batch_copy_out(scls_ctx* ctx, int64_t n, const BatchOutputs& d, scls_batches* out, int32_t mem) {
+static scls_status batch_copy_out(scls_ctx* ctx, int64_t n, const BatchOutputs& d, scls_batches* out, int32_t mem,
+                                  const BatchPack& pk) {
   scls_status st;
   const int64_t nb = out->n_batches;
+  if (pk.on) {  // the used prefix of the result region (member_id is last)
+    const size_t used = out->member_id ? pk.bytes : pk.off[4];
+    SCLS_CUDA(cudaMemcpyAsync(pk.h_out, pk.d_out, used, cudaMemcpyDeviceToHost, ctx->stream));
+    return SCLS_OK;
+  }
   if ((st = copy_out(ctx, out->order, d.order, n, mem)) || (st = copy_out(ctx, out->seg_begin, d.seg_begin, nb + 1, mem)) ||
       (st = copy_out(ctx, out->l_in, d.l_in, nb, mem)) || (st = copy_out(ctx, out->est, d.est, nb, mem)) ||
       (st = copy_out(ctx, out->member_id, d.member_id, n, mem)))
     return st;
   return SCLS_OK;
+}
+
+// After the stream sync: scatter the packed result region into the caller's arrays.
+static void batch_finish(int64_t n, scls_batches* out, const BatchPack& pk) {
+  if (!pk.on || n == 0) return;
+  const int64_t nb = out->n_batches;
+  if (out->order) std::memcpy(out->order, pk.h_out + pk.off[0], 4 * (size_t)n);
+  std::memcpy(out->seg_begin, pk.h_out + pk.off[1], 4 * (size_t)(nb + 1));
+  std::memcpy(out->l_in, pk.h_out + pk.off[2], 4 * (size_t)nb);
+  std::memcpy(out->est, pk.h_out + pk.off[3], 8 * (size_t)nb);
+  if (out->member_id) std::memcpy(out->member_id, pk.h_out + pk.off[4], 8 * (size_t)n);
 }
 
 scls_status scls_batch_requests(scls_ctx* ctx, int64_t n, const int32_t* eff_len, const double* arrival,
@@ -450,10 +525,12 @@ scls_status scls_batch_requests(scls_ctx* ctx, int64_t n, const int32_t* eff_len
   scls_status st = begin_call(ctx);
   if (st) return st;
   BatchOutputs d{};
-  if ((st = batch_impl(ctx, n, eff_len, arrival, id, slice_len, lat, memm, first_batch_id, out, mem, &d))) return st;
+  BatchPack pk;
+  if ((st = batch_impl(ctx, n, eff_len, arrival, id, slice_len, lat, memm, first_batch_id, out, mem, &d, &pk))) return st;
   if (n == 0) return SCLS_OK;
-  if ((st = batch_copy_out(ctx, n, d, out, mem))) return st;
+  if ((st = batch_copy_out(ctx, n, d, out, mem, pk))) return st;
   SCLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  batch_finish(n, out, pk);
   collect_timings(ctx, 4);
   ctx->timings[7] = ctx->dp_last_mono ? 1.f : 0.f;
   return SCLS_OK;
@@ -509,7 +586,8 @@ scls_status scls_schedule(scls_ctx* ctx, int64_t n, const int32_t* eff_len, cons
   if (n_workers < 0 || (n_workers && (!worker_id || !load_inout)) || (n && (!out_batch_id || !out_worker)))
     return set_error(ctx, SCLS_ERR_INVALID_ARGUMENT, "bad arguments");
   BatchOutputs d{};
-  if ((st = batch_impl(ctx, n, eff_len, arrival, id, slice_len, lat, memm, first_batch_id, out, mem, &d))) return st;
+  BatchPack pk;
+  if ((st = batch_impl(ctx, n, eff_len, arrival, id, slice_len, lat, memm, first_batch_id, out, mem, &d, &pk))) return st;
   const int64_t nb = out->n_batches;
   if (nb > 0 && n_workers == 0) return set_error(ctx, SCLS_ERR_NO_WORKERS, "cannot offload batches: no workers configured");
   if (nb > 0) {
@@ -538,8 +616,9 @@ scls_status scls_schedule(scls_ctx* ctx, int64_t n, const int32_t* eff_len, cons
   } else if (n > 0) {
     SCLS_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
   }
-  if (n > 0 && (st = batch_copy_out(ctx, n, d, out, mem))) return st;
+  if (n > 0 && (st = batch_copy_out(ctx, n, d, out, mem, pk))) return st;
   SCLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  batch_finish(n, out, pk);
   if (n > 0) collect_timings(ctx, 5);
   ctx->timings[7] = ctx->dp_last_mono ? 1.f : 0.f;
   return SCLS_OK;

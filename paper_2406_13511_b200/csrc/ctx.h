@@ -46,9 +46,14 @@ struct scls_ctx {
   // Pinned host staging for small readbacks.
   void* pinned = nullptr;
   size_t pinned_cap = 0;
+  // Pinned host staging for small entry-point arguments and results (one
+  // host<->device copy each way instead of one pageable copy per array).
+  void* stage = nullptr;
+  size_t stage_cap = 0;
 
   void* buf(int slot, size_t bytes);
   void* host_pinned(size_t bytes);
+  void* host_stage(size_t bytes);
 };
 
 namespace scls {

@@ -5,8 +5,9 @@
 // pools: ~150 launches and 4 host round trips, which at these sizes ARE the
 // latency.  Here the whole call is four launches and one host read-back:
 //
-//   prep   one CTA: stable LSD radix sort by (eff, arrival, id) in shared
-//          memory (per-warp digit counts, stable scatter), then per sorted
+//   prep   one CTA: the order by (eff, arrival, id, position) in shared
+//          memory (a bitonic network on three 64-bit words per member for
+//          pools up to 1024, stable LSD radix passes above), then per sorted
 //          row L, K(L) and singleton feasibility (batcher.cpp:40-46), the
 //          runs of equal L, and the cost table c(L, k) per run
 //          (cost_model.cpp:49-51); the DP kernel to use is decided on device
@@ -174,49 +175,99 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     st->gate = -1;  // no DP kernel runs unless this call reaches the end
   }
   __syncthreads();
-  // 1. key ranges (so that fields / bits that never vary cost no pass)
-  {
-    unsigned long long mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0, 0, 0};
-    for (int i = tid; i < n; i += kSmallThreads) {
-      const uint64_t f[3] = {bias64(id[i]), ordered_bits(arr[i]), bias32(eff[i])};
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        mn[q] = min(mn[q], (unsigned long long)f[q]);
-        mx[q] = max(mx[q], (unsigned long long)f[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        mn[q] = min(mn[q], __shfl_xor_sync(~0u, mn[q], o));
-        mx[q] = max(mx[q], __shfl_xor_sync(~0u, mx[q], o));
-      }
-      if (lane == 0) {
-        atomicMin(&sm.red[2 * q], mn[q]);
-        atomicMax(&sm.red[2 * q + 1], mx[q]);
-      }
-    }
-  }
-  __syncthreads();
-  // 2. stable LSD sort, field by field from the least significant: id,
-  //    arrival, eff (batcher.cpp:35-38 tuple order)
+  // The order (eff, arrival, id), input position last: pools of up to
+  // kSmallThreads by a bitonic network (few stages, no histogram rounds),
+  // larger ones by the stable LSD passes.
   int src = 0;
-  for (int i = tid; i < n; i += kSmallThreads) sm.perm[0][i] = i;
-  __syncthreads();
-  for (int q = 0; q < 3; ++q) {
-    const uint64_t lo = sm.red[2 * q], range = sm.red[2 * q + 1] - lo;
-    const int bits = range ? 64 - __clzll((long long)range) : 0;
-    if (bits == 0) continue;
-    for (int p = tid; p < n; p += kSmallThreads) {
-      const int i = sm.perm[src][p];
-      const uint64_t f = q == 0 ? bias64(id[i]) : (q == 1 ? ordered_bits(arr[i]) : bias32(eff[i]));
-      sm.key[src][p] = f - lo;
+  if (n <= kSmallThreads) {
+    // a bitonic network in shared memory on three 64-bit words per member --
+    //    A = eff | arrival[63:32], B = arrival[31:0] | id[63:32],
+    //    C = id[31:0] | position -- compared lexicographically: 10 stages for
+    //    16 members, where the LSD passes (up to 11, each a full 256-bin
+    //    histogram round over 32 warps) cost 28 us; at 4096 members the
+    //    network's 78 stages lose to them (measured 122 vs 94 us)
+    uint64_t* const wa = sm.key[0];
+    uint64_t* const wb = sm.key[1];
+    uint64_t* const wc = reinterpret_cast<uint64_t*>(&sm.perm[0][0]);  // perm[2][kSmallPool] = kSmallPool words
+    int P = 2;
+    while (P < n) P <<= 1;
+    for (int i = tid; i < P; i += kSmallThreads) {
+      if (i < n) {
+        const uint64_t a = ordered_bits(arr[i]), d = bias64(id[i]);
+        wa[i] = bias32(eff[i]) << 32 | a >> 32;
+        wb[i] = a << 32 | d >> 32;
+        wc[i] = d << 32 | (uint64_t)(uint32_t)i;
+      } else {
+        wa[i] = wb[i] = wc[i] = ~0ull;
+      }
     }
     __syncthreads();
-    for (int shift = 0; shift < bits; shift += 8) {
-      block_radix_pass(sm, src, n, shift);
-      src ^= 1;
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int t = tid; t < (P >> 1); t += kSmallThreads) {
+          const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), h = i + j;  // j is a power of two
+          const uint64_t a0 = wa[i], a1 = wa[h], b0 = wb[i], b1 = wb[h], c0 = wc[i], c1 = wc[h];
+          const bool gt = a0 != a1 ? a0 > a1 : (b0 != b1 ? b0 > b1 : c0 > c1);
+          if (gt == ((i & k) == 0)) {  // ascending blocks swap a greater first element
+            wa[i] = a1;
+            wa[h] = a0;
+            wb[i] = b1;
+            wb[h] = b0;
+            wc[i] = c1;
+            wc[h] = c0;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const int32_t pos = tid < n ? (int32_t)(uint32_t)wc[tid] : 0;  // n <= kSmallThreads here
+    __syncthreads();
+    if (tid < n) sm.perm[0][tid] = pos;
+    __syncthreads();
+  } else {
+    // 1. key ranges (so that fields / bits that never vary cost no pass)
+    {
+      unsigned long long mn[3] = {~0ull, ~0ull, ~0ull}, mx[3] = {0, 0, 0};
+      for (int i = tid; i < n; i += kSmallThreads) {
+        const uint64_t f[3] = {bias64(id[i]), ordered_bits(arr[i]), bias32(eff[i])};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          mn[q] = min(mn[q], (unsigned long long)f[q]);
+          mx[q] = max(mx[q], (unsigned long long)f[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          mn[q] = min(mn[q], __shfl_xor_sync(~0u, mn[q], o));
+          mx[q] = max(mx[q], __shfl_xor_sync(~0u, mx[q], o));
+        }
+        if (lane == 0) {
+          atomicMin(&sm.red[2 * q], mn[q]);
+          atomicMax(&sm.red[2 * q + 1], mx[q]);
+        }
+      }
+    }
+    __syncthreads();
+    // 2. stable LSD sort, field by field from the least significant: id,
+    //    arrival, eff (batcher.cpp:35-38 tuple order)
+    for (int i = tid; i < n; i += kSmallThreads) sm.perm[0][i] = i;
+    __syncthreads();
+    for (int q = 0; q < 3; ++q) {
+      const uint64_t lo = sm.red[2 * q], range = sm.red[2 * q + 1] - lo;
+      const int bits = range ? 64 - __clzll((long long)range) : 0;
+      if (bits == 0) continue;
+      for (int p = tid; p < n; p += kSmallThreads) {
+        const int i = sm.perm[src][p];
+        const uint64_t f = q == 0 ? bias64(id[i]) : (q == 1 ? ordered_bits(arr[i]) : bias32(eff[i]));
+        sm.key[src][p] = f - lo;
+      }
+      __syncthreads();
+      for (int shift = 0; shift < bits; shift += 8) {
+        block_radix_pass(sm, src, n, shift);
+        src ^= 1;
+      }
     }
   }
   // 3. rows: L, K(L) (memory_model.cpp:72-90), singleton feasibility, runs

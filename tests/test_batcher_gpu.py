@@ -313,6 +313,18 @@ def test_small_pool_path_matches_large_path(ctx, orc):
             assert_same_batches(small, want, (n, mname, "small"))
             assert_same_batches(large, want, (n, mname, "large"))
             assert np.array_equal(small["order"], large["order"])
+    # the bitonic (n <= 1024) and LSD (above) sorts on full-key ties: few eff
+    # values, arrivals that tie (+-0.0 included) and duplicate ids
+    mem = MEMORIES["rule"]()
+    for n in (2, 16, 500, 1023, 1024, 1025, 3000):
+        eff = rng.integers(1, 6, n).astype(np.int32)
+        arr = np.round(rng.random(n) * 3, 0)
+        arr[::5] = -0.0
+        ids = rng.integers(-3, 4, n).astype(np.int64)
+        want = orc.batch_requests(eff, arr, ids, 128, lat, mem)
+        small = ctx.batch_requests(eff, arr, ids, 128, lat, mem)
+        assert_same_batches(small, want, (n, "ties"))
+        assert np.array_equal(ids[small["order"]], small["member_id"])
 
 
 def lib_error():
