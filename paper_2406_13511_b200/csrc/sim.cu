@@ -70,6 +70,9 @@ constexpr int kEmitU = SCLS_EMIT_U;  // tick emit: served l_out scan unroll
 #define SCLS_PUSH_U 4
 #endif
 constexpr int kPushU = SCLS_PUSH_U;
+#ifndef SCLS_SIM_DISCARD
+#define SCLS_SIM_DISCARD 0  // 1: dead SCLS tick scratch and consumed tick-log lines dropped from L2 (measured slower)
+#endif
 #ifndef SCLS_DP_BRANCHFREE
 #define SCLS_DP_BRANCHFREE 0  // tick DP: clamped loads + selects instead of divergent branches
 #endif
@@ -139,6 +142,20 @@ __device__ __forceinline__ int trace_input_status(const double* arr, const int32
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(FULL, v, src); }
 __device__ __forceinline__ int shfl_i(int v, int src) { return __shfl_sync(FULL, v, src); }
 __device__ __forceinline__ long long shfl_l(long long v, int src) { return __shfl_sync(FULL, v, src); }
+
+// Drop the L2 lines that lie wholly inside [lo, hi) without writing them
+// back (discard.global.L2): for arena scratch that is dead -- every later
+// read of it is preceded by a write of the same bytes -- so its dirty lines
+// neither cost a DRAM write-back nor hold L2 capacity the live tick log and
+// pool records need.  Lines shared with a neighbouring range are kept.
+__device__ __forceinline__ void l2_discard(const void* lo, const void* hi, int lane) {
+#if SCLS_SIM_DISCARD
+  uintptr_t a = ((uintptr_t)lo + 127) & ~(uintptr_t)127;
+  const uintptr_t e = (uintptr_t)hi & ~(uintptr_t)127;
+  for (a += (uintptr_t)128 * lane; a < e; a += (uintptr_t)128 * 32)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+#endif
+}
 
 // ---- event-log sink: counters always, digests / records on demand ------------------
 
@@ -1118,6 +1135,20 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       start_next_scls(w);
     }
     SIM_PROF(7);
+    // the tick's scratch is dead until the next tick rewrites it: the pool
+    // records it consumed, the sort keys, rows, T / split and segments
+    if (P_ > 0) {
+      const int m = max(P_, nb);
+      l2_discard(prec, prec + n_rec, lane);
+      l2_discard(pool, pool + n_rec, lane);
+      l2_discard(p_eff, p_eff + n_rec, lane);
+      l2_discard(sk, sk + m, lane);
+      l2_discard(sk2, sk2 + m, lane);
+      l2_discard(sv, sv + m + 1, lane);
+      l2_discard(Tg, Tg + m + 1, lane);
+      l2_discard(split_g, split_g + m + 1, lane);
+      l2_discard(segs, segs + nb + 1, lane);
+    }
     // sched_policies.cpp:134-146: adaptive interval from the post-offload loads
     const double ml = min_worker_load<V>(ws, W, lane);
     const double a = __dmul_rn(C.lambda, ml);
@@ -1224,6 +1255,9 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       k.load = k.load - best;  // offloader.cpp:56-59 complete_batch
       if (k.load < 0.0) k.load = 0.0;
     }
+    // this batch's tick-log entries are consumed (the log is append-only)
+    __syncwarp();
+    l2_discard(tlog + bst, tlog + bst + bn, lane);
   };
 
   // SLS on_batch_done (sched_policies.cpp:245-273).

@@ -399,3 +399,23 @@ def test_bucket_sort_matches_lsd_sort(ctx, orc):
                 ctx.set_batch_path(0)
             assert_same_batches(got, want, (i, path))
             assert np.array_equal(ids[got["order"]], got["member_id"])
+
+
+def test_host_staging_boundary(ctx, orc):
+    """Host-memory calls up to 2^16 requests stage through one pinned buffer
+    (capi.cu BatchPack), larger ones array by array: both sides of the
+    boundary against the oracle, batch_requests and schedule."""
+    lat = capi.builtin_latency_model()
+    mem = MEMORIES["analytic"]()
+    for n in (65535, 65536, 65537):
+        eff, arr, ids, _ = orc.make_pool(n, 11)
+        want = orc.batch_requests(eff, arr, ids, 128, lat, mem)
+        got = ctx.batch_requests(eff, arr, ids, 128, lat, mem)
+        assert_same_batches(got, want, n)
+        assert np.array_equal(ids[got["order"]], got["member_id"])
+        loads = [0.25 * w for w in range(8)]
+        s = ctx.schedule(eff, arr, ids, 128, lat, mem, np.arange(8, dtype=np.int32), loads)
+        ob, ow, nl = orc.offload(want["batch_id"], want["est"], np.arange(8, dtype=np.int32), loads)
+        assert_same_batches(s, want, (n, "schedule"))
+        assert np.array_equal(s["assign_batch"], ob) and np.array_equal(s["assign_worker"], ow)
+        assert np.array_equal(s["loads"], nl)
