@@ -73,6 +73,9 @@ constexpr int kPushU = SCLS_PUSH_U;
 #ifndef SCLS_SIM_DISCARD
 #define SCLS_SIM_DISCARD 0  // 1: dead SCLS tick scratch and consumed tick-log lines dropped from L2 (measured slower)
 #endif
+#ifndef SCLS_DP_PAIR
+#define SCLS_DP_PAIR 1  // tick DP chain: two steps per broadcast (T[tb+s] formed on every lane)
+#endif
 #ifndef SCLS_DP_BRANCHFREE
 #define SCLS_DP_BRANCHFREE 0  // tick DP: clamped loads + selects instead of divergent branches
 #endif
@@ -1023,6 +1026,45 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           acc = tk ? cand : acc;
           kb = tk ? lane + 2 - s : kb;
           Tj = shfl_d(acc, s - 1);
+        }
+#elif SCLS_DP_PAIR
+        // Two steps per broadcast.  T[tb+s] is lane s-1's acc after its k = 1
+        // candidate at step s: min-select of fl(T[tb+s-1] + c(L, 1)) against
+        // its acc before step s -- the same operands and the same accept as
+        // on that lane, so every lane forms it itself from (acc, c(L, 1)) of
+        // lane s-1, shuffled one pair ahead, and step s+1 needs no broadcast:
+        // one shuffle latency per two rows on the chain instead of one per row.
+        const double* __restrict__ cp = crow + lane;       // c(L_r, lane + 2 - s) = cp[2 - s]
+        const double c1own = valid ? __ldg(crow + 1) : 0.0;
+        Tj = shfl_d(acc, 0);  // step 1 offers nothing (sources <= tb were the far part): T[tb+1]
+        double Ab = shfl_d(acc, 1), c1b = shfl_d(c1own, 1);  // lane 1 before step 2
+        double ca = kval(2) ? __ldg(cp) : 0.0;               // step 2
+        double cb = kval(3) ? __ldg(cp - 1) : 0.0;           // step 3
+        int s = 2;
+        for (; s + 1 <= rows; s += 2) {
+          const double na = kval(s + 2) ? __ldg(cp - s) : 0.0;      // step s + 2
+          const double nb = kval(s + 3) ? __ldg(cp - s - 1) : 0.0;  // step s + 3
+          const double t1 = __dadd_rn(Tj, c1b);
+          const double Ts = t1 <= Ab ? t1 : Ab;  // T[tb+s]
+          const double cand = __dadd_rn(Tj, ca);  // step s: source tb+s-1
+          const bool tk = kval(s) && cand <= acc;
+          acc = tk ? cand : acc;
+          kb = tk ? lane + 2 - s : kb;
+          const double cand2 = __dadd_rn(Ts, cb);  // step s+1: source tb+s
+          const bool tk2 = kval(s + 1) && cand2 <= acc;
+          acc = tk2 ? cand2 : acc;
+          kb = tk2 ? lane + 1 - s : kb;
+          Tj = shfl_d(acc, s);  // T[tb+s+1]: lane s is final after step s+1
+          Ab = shfl_d(acc, s + 1);
+          c1b = shfl_d(c1own, s + 1);
+          ca = na;
+          cb = nb;
+        }
+        if (s == rows) {  // a last single step
+          const double cand = __dadd_rn(Tj, ca);
+          const bool tk = kval(s) && cand <= acc;
+          acc = tk ? cand : acc;
+          kb = tk ? lane + 2 - s : kb;
         }
 #else
         const double* __restrict__ cp = crow + lane;       // c(L_r, lane + 2 - s) = cp[2 - s]
