@@ -29,6 +29,10 @@
 
 namespace scls {
 
+#ifndef SCLS_DPC_PAIR
+#define SCLS_DPC_PAIR 1  // the in-tile chain takes two steps per broadcast
+#endif
+
 constexpr int kDpThreads = 512;
 constexpr int kDpRing = 4096;   // ring of recent T values
 constexpr int kDpStageK = 64;   // staged costs per row (mid+near need k <= 63)
@@ -202,6 +206,46 @@ __global__ void __launch_bounds__(kDpThreads, 1)
 #pragma unroll
       for (int s = 1; s <= kAhead; ++s) c2[s] = sm.cs[nb][32 + lane - s][lane];
       double Tj = Tlast;
+#if SCLS_DPC_PAIR
+      // Two steps per broadcast: T[tB+s+1] is lane s's acc after its k = 1
+      // candidate at step s -- every lane forms it from lane s's (acc before
+      // step s, c(L, 1)), shuffled a pair ahead, with the same operands and
+      // the same accept as lane s, so step s+1 needs no broadcast.
+      const double c1own = sm.cs[cb][0][lane];
+      double Ab = __shfl_sync(0xffffffffu, acc, 0), c1b = __shfl_sync(0xffffffffu, c1own, 0);
+#pragma unroll
+      for (int s = 0; s < 32; s += 2) {
+        if (s + kAhead <= 31 && s + kAhead >= 1) c2[s + kAhead] = sm.cs[nb][32 + lane - s - kAhead][lane];
+        if (s + 1 + kAhead <= 31) c2[s + 1 + kAhead] = sm.cs[nb][32 + lane - s - 1 - kAhead][lane];
+        const double t1 = __dadd_rn(Tj, c1b);
+        const double Tn = le<kIntCmp>(t1, Ab) ? t1 : Ab;  // T[tB+s+1]
+        // step s: T[tB+s], k = lane+1-s; the next-tile row with k2 = 33+lane-s
+        const double cand = __dadd_rn(Tj, cn[s]);
+        const bool take = le<kIntCmp>(cand, acc);
+        acc = take ? cand : acc;
+        kb = take ? lane + 1 - s : kb;
+        if (s >= 1) {
+          const double cand2 = __dadd_rn(Tj, c2[s]);
+          const bool take2 = le<kIntCmp>(cand2, accN);
+          accN = take2 ? cand2 : accN;
+          kbN = take2 ? 33 + lane - s : kbN;
+        }
+        // step s+1: T[tB+s+1]
+        const double candb = __dadd_rn(Tn, cn[s + 1]);
+        const bool takeb = le<kIntCmp>(candb, acc);
+        acc = takeb ? candb : acc;
+        kb = takeb ? lane - s : kb;
+        const double cand2b = __dadd_rn(Tn, c2[s + 1]);
+        const bool take2b = le<kIntCmp>(cand2b, accN);
+        accN = take2b ? cand2b : accN;
+        kbN = take2b ? 32 + lane - s : kbN;
+        Tj = __shfl_sync(0xffffffffu, acc, s + 1);
+        if (s + 2 < 32) {
+          Ab = __shfl_sync(0xffffffffu, acc, s + 2);
+          c1b = __shfl_sync(0xffffffffu, c1own, s + 2);
+        }
+      }
+#else
 #pragma unroll
       for (int s = 0; s < 32; ++s) {
         if (s + kAhead <= 31 && s + kAhead >= 1) c2[s + kAhead] = sm.cs[nb][32 + lane - s - kAhead][lane];
@@ -219,6 +263,7 @@ __global__ void __launch_bounds__(kDpThreads, 1)
         }
         Tj = __shfl_sync(0xffffffffu, acc, s);
       }
+#endif
       // T[tB+32] reaches the next rows as step s = 0 of the next chain.
       Tlast = Tj;
       const int r = tB + 1 + lane;
