@@ -73,6 +73,9 @@ constexpr int kPushU = SCLS_PUSH_U;
 #ifndef SCLS_SIM_DISCARD
 #define SCLS_SIM_DISCARD 0  // 1: dead SCLS tick scratch and consumed tick-log lines dropped from L2 (measured slower)
 #endif
+#ifndef SCLS_DP_PUSH
+#define SCLS_DP_PUSH 1  // tick DP chain mode, windows <= 32: the next tile's far candidates ride this tile's chain
+#endif
 #ifndef SCLS_DP_PAIR
 #define SCLS_DP_PAIR 1  // tick DP chain: two steps per broadcast (T[tb+s] formed on every lane)
 #endif
@@ -806,6 +809,9 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       // 2. rows: the batched state of every member, L, K(L) and its cost row,
       //    singleton feasibility (batcher.cpp:40-46)
       int bad = 0x7fffffff;
+#if SCLS_DP_PUSH
+      int kmx = 0;  // the largest K(L) of the pool
+#endif
       for (int i0 = lane; i0 < P_; i0 += 32 * kRowsU) {  // kRowsU rows per lane per trip, loads first
         uint64_t key[kRowsU];
         int q[kRowsU];
@@ -846,10 +852,16 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
             tlog[qq].a = a_[u];
             sv[i] = L[u];
             if (L[u] > P.Lmax || k_[u] == 0) bad = min(bad, i);
+#if SCLS_DP_PUSH
+            kmx = max(kmx, k_[u]);
+#endif
           }
         }
       }
       bad = __reduce_min_sync(FULL, bad);
+#if SCLS_DP_PUSH
+      kmx = __reduce_max_sync(FULL, kmx);
+#endif
       __syncwarp();
       if (bad != 0x7fffffff) {
         err_req = tlog[tl_pos + bad].igte.x;
@@ -869,6 +881,14 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
       }
       __syncwarp();
       const double kInf = dinf();
+#if SCLS_DP_PUSH
+      // chain mode with every window <= 32: a row's sources other than its
+      // own tile's are all in the previous tile, whose chain offers them to
+      // it in ascending order (accN), so the far loop is skipped
+      const bool push = !C.mono && kmx <= 32;
+      double accN = kInf;
+      int kbN = 0;
+#endif
       for (int tb = 0; tb < P_; tb += 32) {
         SIM_PROF(5);
         const int r = tb + 1 + lane;
@@ -880,6 +900,14 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         int kb = 0;
         const int wmax = __reduce_max_sync(FULL, Wr);
         // candidates with j <= tb, ascending j (k descending)
+#if SCLS_DP_PUSH
+        if (push && tb > 0) {
+          acc = accN;
+          kb = kbN;
+        } else {
+#else
+        {
+#endif
         int j = max(0, tb + 1 - wmax);
 #if SCLS_DP_BRANCHFREE
         {
@@ -949,6 +977,7 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           }
         }
 #endif
+        }
         SIM_PROF(11);  // tile setup + far candidates (the rest of the tile goes to slot 5)
         if (C.mono) {
           // decision rounds (dp_mono.cuh): with T[0..a] final, a pending row
@@ -1036,6 +1065,19 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
         // one shuffle latency per two rows on the chain instead of one per row.
         const double* __restrict__ cp = crow + lane;       // c(L_r, lane + 2 - s) = cp[2 - s]
         const double c1own = valid ? __ldg(crow + 1) : 0.0;
+#if SCLS_DP_PUSH
+        // the next tile's row r + 32 takes source tb+s-1 at step s with
+        // k' = 34 + lane - s (<= its window <= 32, so s >= 2)
+        const int rN = r + 32;
+        const bool vN = push && rN <= P_;
+        const int LN = vN ? sv[rN - 1] : 0;
+        const int WrN = vN ? min(__ldg(Kt + LN), rN) : 0;
+        const double* __restrict__ cpN = cost + (vN ? __ldg(coff + LN) - 1 : 0) + 34 + lane;  // cpN[-s]
+        auto kvN = [&](int st) { return 34 + lane - st <= WrN; };
+        accN = kInf;
+        kbN = 0;
+        double caN = kvN(2) ? __ldg(cpN - 2) : 0.0, cbN = kvN(3) ? __ldg(cpN - 3) : 0.0;
+#endif
         Tj = shfl_d(acc, 0);  // step 1 offers nothing (sources <= tb were the far part): T[tb+1]
         double Ab = shfl_d(acc, 1), c1b = shfl_d(c1own, 1);  // lane 1 before step 2
         double ca = kval(2) ? __ldg(cp) : 0.0;               // step 2
@@ -1054,6 +1096,22 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           const bool tk2 = kval(s + 1) && cand2 <= acc;
           acc = tk2 ? cand2 : acc;
           kb = tk2 ? lane + 1 - s : kb;
+#if SCLS_DP_PUSH
+          {
+            const double naN = kvN(s + 2) ? __ldg(cpN - s - 2) : 0.0;
+            const double nbN = kvN(s + 3) ? __ldg(cpN - s - 3) : 0.0;
+            const double d1 = __dadd_rn(Tj, caN);
+            const bool u1 = kvN(s) && d1 <= accN;
+            accN = u1 ? d1 : accN;
+            kbN = u1 ? 34 + lane - s : kbN;
+            const double d2 = __dadd_rn(Ts, cbN);
+            const bool u2 = kvN(s + 1) && d2 <= accN;
+            accN = u2 ? d2 : accN;
+            kbN = u2 ? 33 + lane - s : kbN;
+            caN = naN;
+            cbN = nbN;
+          }
+#endif
           Tj = shfl_d(acc, s);  // T[tb+s+1]: lane s is final after step s+1
           Ab = shfl_d(acc, s + 1);
           c1b = shfl_d(c1own, s + 1);
@@ -1066,6 +1124,19 @@ __device__ void run_trace(const SimParams& P, int t, int lane, int32_t* bins, in
           acc = tk ? cand : acc;
           kb = tk ? lane + 2 - s : kb;
         }
+#if SCLS_DP_PUSH
+        if (rows == 32) {  // then s == 32: sources tb+31 (Tj) and tb+32 (lane 31's final acc)
+          const double d1 = __dadd_rn(Tj, caN);
+          const bool u1 = kvN(32) && d1 <= accN;
+          accN = u1 ? d1 : accN;
+          kbN = u1 ? 2 + lane : kbN;
+          const double Tl = shfl_d(acc, 31);
+          const double d2 = __dadd_rn(Tl, cbN);
+          const bool u2 = kvN(33) && d2 <= accN;
+          accN = u2 ? d2 : accN;
+          kbN = u2 ? 1 + lane : kbN;
+        }
+#endif
 #else
         const double* __restrict__ cp = crow + lane;       // c(L_r, lane + 2 - s) = cp[2 - s]
         double c1 = 0.0;                                   // step s (never valid at s = 1)
