@@ -73,6 +73,9 @@ constexpr int kPushU = SCLS_PUSH_U;
 #ifndef SCLS_SIM_DISCARD
 #define SCLS_SIM_DISCARD 0  // 1: dead SCLS tick scratch and consumed tick-log lines dropped from L2 (measured slower)
 #endif
+#ifndef SCLS_CHAIN_ALWAYS
+#define SCLS_CHAIN_ALWAYS 1  // the tick DP's chain mode also for launches with few jobs (windows <= 32)
+#endif
 #ifndef SCLS_DP_PUSH
 #define SCLS_DP_PUSH 1  // tick DP chain mode, windows <= 32: the next tile's far candidates ride this tile's chain
 #endif
@@ -2079,15 +2082,16 @@ static scls_status simulate_core(scls_ctx* ctx, int32_t n_src, const int64_t* re
       SCLS_CUDA(cudaMemcpyAsync(&tot, off + Lmax + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       SCLS_CUDA(cudaMemcpyAsync(&kmax, d_kmax, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       SCLS_CUDA(cudaStreamSynchronize(s));
-      // Tick DP variant: when every window fits one 32-row tile and the
-      // launch holds more SCLS jobs than there are SMs (a contended sweep),
-      // the in-tile chain issues less than the decision rounds (C5 sweep:
-      // ~1.5 ms of ~37 ms); a lightly loaded GPU keeps the rounds, whose
-      // per-trace latency is lower.
+      // Tick DP variant: when every window fits one 32-row tile the in-tile
+      // chain (two steps per broadcast, the next tile's far candidates on
+      // it) beats the decision rounds -- in a contended sweep (C5: it issues
+      // less) and, since round 2's paired / pushed chain, also for single
+      // traces (C1 1.68 -> 1.61, C2 12.3 -> 11.4, C4 377 -> 354 ms);
+      // SCLS_CHAIN_ALWAYS 0 keeps the rounds for launches with <= one job per SM.
       if (kmax <= 32 && ctx->dp_mode == 0) {
         int64_t jobs = 0;
         for (int t = 0; t < n_traces; ++t) jobs += (cfg_index ? h_idx[t] : 0) == c;
-        if (jobs > ctx->sm_count) hc[c].mono = 0;
+        if (jobs > ctx->sm_count || SCLS_CHAIN_ALWAYS) hc[c].mono = 0;
       }
       if (grand + tot > (1ll << 30)) return set_error(ctx, SCLS_ERR_CAPACITY, "simulator cost tables exceed 2^30 entries");
       totals[hc[c].table] = tot;
