@@ -279,7 +279,10 @@ constexpr size_t kIlsPackSmem = (size_t)kSimWarps * kPackSlots * (sizeof(int4) +
 // summary next to its completion records; a second kernel merges and reports
 // every job with a warp of its own, so the merges no longer run in series
 // behind a pack.
-constexpr int kIlsPackMaxSplit = 4;
+#ifndef SCLS_ILS_PACK_SPLIT
+#define SCLS_ILS_PACK_SPLIT 4
+#endif
+constexpr int kIlsPackMaxSplit = SCLS_ILS_PACK_SPLIT;
 constexpr int kPackSlotsSplit = 2 * kPackSlots;
 constexpr size_t kIlsPackSmemSplit =
     (size_t)kSimWarps * kPackSlotsSplit * (sizeof(int4) + sizeof(double) + sizeof(int32_t));
